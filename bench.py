@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark: CIA Kuramoto RK4 on BASELINE.json configs[1] (config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric (BASELINE.json:2): node-updates/s = N_nodes x RK4 steps / time, one
+node-update = one node advanced by one full RK4 step (4 CIA RHS evaluations).
+
+Timing protocol (ours):
+* inputs (graph CSR, theta, omega) resident in HBM before the timed region;
+* every timed step is one replay of a captured CUDA graph holding one RK4 step
+  (4 fused stage kernels + 1 bookkeeping kernel); L2 (126 MB) is FLUSHED
+  before every step by writing a 512 MB buffer outside the events, so each
+  step streams its CSR from HBM in stage 1 (config 2's inputs, ~60 MB
+  compressed, are smaller than L2);
+* CUDA events on the launching stream, barrier + synchronize on both sides,
+  max over ranks; value = N x K / sum(step times).
+Extra keys: roofline of the dominant (stage) kernel, the CPU baseline (oracle
+C port, 1 thread, bounded sample), e2e through the public integrate() API
+with host arrays, clocks sampled during the run, gpu_launches.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle C port of commdyn/_kernels.py, all host threads) on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+METRIC = "node-updates/sec (CIA Kuramoto RK4 RHS)"
+UNIT = "node-updates/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes_per_rhs(n: int, nnz_dir: int, d: int = 1, n_param: int = 1) -> int:
+    """B_rhs = 4 nnz_dir + 8 (N+1) + N (16 d + 8 n_param)."""
+    return 4 * nnz_dir + 8 * (n + 1) + n * (16 * d + 8 * n_param)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        util = [float(s[6]) for s in self.samples if s[6].replace(".", "").isdigit()]
+        loaded = [c for c, u in zip(sm, util) if u > 0] or sm
+        reasons = sorted({n for s in self.samples for n, v in zip(self.NAMES, s[2:6])
+                          if v.lower().startswith("active")})
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline_sample(case, dec, omega, theta0, steps: int = 3, threads: int = 1):
+    """Oracle C port (restatement of commdyn/_kernels.py, numba's single-thread
+    order) over `steps` full RK4 steps of the whole graph."""
+    from oracle import cia
+    from oracle import kernels as K
+
+    K.set_threads(threads)
+    s = dec.correction
+
+    def rhs(x):
+        return cia.kuramoto_rhs_cia(K, x, omega, dec.offsets, s.iu, s.iv, s.sgn, case.coupling,
+                                    case.n)
+
+    rhs(theta0[: case.n])  # warm (page-in)
+    t = time.perf_counter()
+    cia.rk4_integrate(rhs, theta0, case.dt, steps)
+    el = time.perf_counter() - t
+    K.set_threads(1)
+    return case.n * steps / el, el
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return 0
+    from oracle import kernels as K
+    from paper_2203_16657_b200 import configs
+
+    case = configs.config2()
+    dec = case.decomposition()
+    omega, theta0 = case.state()
+    threads = max(1, os.cpu_count() or 1)
+    # per-step cost probe, then bound the run to a few minutes
+    rate1, el1 = cpu_baseline_sample(case, dec, omega, theta0, steps=1, threads=threads)
+    budget_s = 150.0
+    steps = int(max(1, min(args.steps, budget_s // max(el1, 1e-3))))
+    warm = min(args.warmup, 1)
+    if warm:
+        cpu_baseline_sample(case, dec, omega, theta0, steps=warm, threads=threads)
+    rate, el = cpu_baseline_sample(case, dec, omega, theta0, steps=steps, threads=threads)
+    sample = (f"{steps} full RK4 step(s) of config 2 (N={case.n}, nnz_dir={dec.nnz_dir}) "
+              f"of the requested {args.steps}; oracle C port of commdyn/_kernels.py "
+              f"(pairs_trig OpenMP per-thread buffers), {threads} threads")
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "warmup": warm, "ms_per_step": 1e3 * el / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "cfg2 Kuramoto CIA RK4, SBM N=200000, 200 power-law communities, "
+                   "p_in .95, inter degree 5, dt .01", "n_nodes": case.n,
+                   "nnz_dir": dec.nnz_dir, "parallelism": "host threads"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = _dist_env()
+    if world > 1:
+        from paper_2203_16657_b200 import multi
+
+        return multi.bench_main(args)
+    torch.cuda.set_device(local)
+    from paper_2203_16657_b200 import _lib, configs
+    from paper_2203_16657_b200.engine import KuramotoEngine
+    from paper_2203_16657_b200.plan import DeviceGraph
+
+    lib = _lib.lib()
+    case = configs.config2()
+    t0 = time.perf_counter()
+    dec = case.decomposition()
+    t_gen = time.perf_counter() - t0
+    omega, theta0 = case.state()
+    t0 = time.perf_counter()
+    dg = DeviceGraph(dec)
+    t_plan = time.perf_counter() - t0
+    eng = KuramotoEngine(dec, omega, coupling=case.coupling, norm=case.n, graph=dg)
+    eng.set_state(theta0)
+    n, nnz = case.n, dec.nnz_dir
+    dt = case.dt
+
+    stream = torch.cuda.Stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        flush.fill_(float(np.random.random()))
+
+    # capture one RK4 step as a CUDA graph
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        eng.rk4(dt, 1, stream=stream)  # warm + attribute setup outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        eng.rk4(dt, 1, stream=stream)
+    torch.cuda.synchronize()
+
+    W, K = max(3, args.warmup), args.steps
+    sampler = ClockSampler(local)
+    with sampler:
+        for _ in range(W):
+            flush_l2()
+            graph.replay()
+        torch.cuda.synchronize()
+        eng.set_state(theta0)  # the timed trajectory starts at theta0
+        torch.cuda.synchronize()
+        _barrier(world)
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        l0 = int(lib.cdk_launch_count())
+        cur = torch.cuda.current_stream()
+        for i in range(K):
+            flush_l2()
+            starts[i].record(cur)
+            graph.replay()
+            ends[i].record(cur)
+        torch.cuda.synchronize()
+        _barrier(world)
+        step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        # graph replays do not go through the library's launch counter: count
+        # the kernels each captured step holds (4 stage + 1 bookkeeping)
+        launches = int(lib.cdk_launch_count()) - l0 + 5 * K
+        eng.check()
+        total_ms = _max_over_ranks(float(np.sum(step_ms)), world)
+
+        # --- roofline pass: the stage kernel alone, events around each launch
+        eng.set_state(theta0)
+        Kr = min(K, 200)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(Kr)]
+        torch.cuda.synchronize()
+        for i in range(Kr):
+            flush_l2()
+            with torch.cuda.stream(stream):
+                ev[i][0].record(stream)
+                for s in range(1, 5):
+                    eng.rk4_stage(dt, s, stream=stream)
+                    ev[i][s].record(stream)
+        torch.cuda.synchronize()
+        stage_ms = np.array([[ev[i][s - 1].elapsed_time(ev[i][s]) for s in range(1, 5)]
+                             for i in range(Kr)])
+
+        # --- e2e: public API with host arrays (fresh model: omega + theta0 uploaded,
+        #     final state read back), inside the timed region
+        from paper_2203_16657_b200 import IntegrationPlan, integrate, kuramoto_model
+
+        dec._cache["device_graph"] = dg
+        e2e_times = []
+        for rep in range(2):
+            model = kuramoto_model(omega.copy(), case.coupling, case.n)
+            flush_l2()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            tr = integrate(model, dec, theta0, IntegrationPlan(t_end=K * dt, dt=dt))
+            final = tr.final
+            torch.cuda.synchronize()
+            e2e_times.append(time.perf_counter() - t)
+        e2e_s = min(e2e_times)
+    clocks = sampler.summary()
+
+    # parity spot check of the timed trajectory vs the e2e run (same K steps)
+    if not np.all(np.isfinite(final)):
+        raise RuntimeError("non-finite final state")
+
+    value = n * K / (total_ms / 1e3)
+    b_rhs = algorithmic_bytes_per_rhs(n, nnz)
+    stage_mean_ms = float(stage_ms.mean())
+    stage1_ms = float(stage_ms[:, 0].mean())
+    peak, peak_kind = _peaks()
+    achieved = b_rhs / (stage_mean_ms / 1e3) / 1e9
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": "cfg2 Kuramoto CIA RK4, SBM N=200000, 200 power-law communities, "
+                        "p_in .95, inter degree 5, dt .01",
+            "n_nodes": n, "n_comm": len(case.sizes), "nnz_dir": nnz,
+            "csr_device_bytes": dg.device_bytes(), "l2": "flushed (512 MB write) before every "
+            "timed step", "parallelism": f"dp{world} (replicas)" if world > 1 else "1 GPU",
+            "graph_gen_s": round(t_gen, 2), "plan_build_s": round(t_plan, 2),
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+            "kernel": "kuramoto_stage_kernel", "algorithmic_bytes_per_launch": b_rhs,
+            "stage_ms_mean": stage_mean_ms, "stage1_ms_mean": stage1_ms,
+            "stage_ms_by_stage": [float(x) for x in stage_ms.mean(axis=0)],
+        },
+        "e2e": {"value": n * K / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(2 * 8 * n / K),
+                "d2h_bytes_per_step": int(2 * 8 * n / K),
+                "note": "integrate() via the public API: omega + theta0 from host, "
+                        "initial + final states back to host; CSR already on device"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, el = cpu_baseline_sample(case, dec, omega, theta0, steps=args.cpu_steps, threads=1)
+        res["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{args.cpu_steps} full RK4 steps of config 2 ({el:.1f} s), oracle C port "
+                      "of commdyn/_kernels.py, single thread as the reference's numba kernels",
+        }
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

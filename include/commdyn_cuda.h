@@ -1,0 +1,176 @@
+/*
+ * commdyn_cuda.h — C ABI of libcommdyn_cuda.so, the B200 (sm_100a) drop-in for
+ * the Community Integration Algorithm hot path of the reference package
+ * `commdyn` (arXiv 2203.16657).
+ *
+ * Conventions (all entry points):
+ *   - every array argument is a DEVICE pointer unless marked [host];
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *     work is stream-ordered, nothing synchronises unless stated;
+ *   - complex arrays are interleaved (re, im) float64, i.e. numpy complex128;
+ *   - return value is a status: CDK_OK, CDK_INPUT (bad shape/argument),
+ *     CDK_CUDA (CUDA runtime error; cdk_last_error() has the text).  Numeric
+ *     guards (blow-up, imaginary residue) are REPORTED through output counters
+ *     (as the reference's dense_complex reports (n_viol, max_imag)); the Python
+ *     layer maps them onto commdyn/errors.py classes.
+ *   - the caller allocates every buffer (reference ownership convention,
+ *     SURVEY §8b); kernels accumulate into `out`, they never zero it.
+ *   - no exceptions cross the ABI; no hidden global state beyond per-process
+ *     function attributes and the last-error string.
+ */
+#ifndef COMMDYN_CUDA_H
+#define COMMDYN_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CDK_API __attribute__((visibility("default")))
+#else
+#define CDK_API
+#endif
+
+#define CDK_OK 0
+#define CDK_NUMERIC 1
+#define CDK_INPUT 2
+#define CDK_CUDA 3
+
+#define CDK_ABI_VERSION 1
+#define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
+
+/* ------------------------------------------------------------------------ */
+/* Kernel-level twins of the reference dispatchers (commdyn/_kernels.py).   */
+/* Same array contracts; `pi_over_l` = pi / half_width as the dispatchers   */
+/* compute it.  Reductions are fixed-order (deterministic); the pair        */
+/* kernels scatter with fp64 atomics (SPEC.md:408 parallel mode, 1e-12).    */
+/* ------------------------------------------------------------------------ */
+
+/* replaces order_params_blocks, _kernels.py:68-73 (numba body :34-51).
+ * x f64[>= offsets[m_comm]], offsets i64[m_comm+1] -> r c128[m_comm][2p+1]. */
+CDK_API int cdk_order_params_blocks(const double *x, const int64_t *offsets, int64_t m_comm, int p,
+                            double pi_over_l, double norm, double *r, void *stream);
+
+/* replaces dense_complex, _kernels.py:165-169 (:124-149).  out += ...;
+ * guard[0] (int64) += violations, guard[1] (f64 bits) = max(|imag|). */
+CDK_API int cdk_dense_complex(const double *x, const int64_t *offsets, int64_t m_comm, const double *tbl,
+                      int p, double pi_over_l, double *out, void *guard, void *stream);
+
+/* replaces dense_real, _kernels.py:199-204 (:172-187). */
+CDK_API int cdk_dense_real(const double *x, const int64_t *offsets, int64_t m_comm,
+                   const double *tbl_cos, const double *tbl_sin, int p, double pi_over_l,
+                   double *out, void *stream);
+
+/* replaces pairs_trig, _kernels.py:353-362 (:246-261, :274-283). */
+CDK_API int cdk_pairs_trig(const int64_t *iu, const int64_t *iv, int64_t n_pairs, const double *x,
+                   double inv_n, const double *d_cos, const double *d_sin, int p,
+                   double pi_over_l, const double *sgn, double *out, void *stream);
+
+/* replaces pairs_cs, _kernels.py:372-376 (:297-314).  pos/vel/out f64[n][ndim]. */
+CDK_API int cdk_pairs_cs(const int64_t *iu, const int64_t *iv, int64_t n_pairs, const double *pos,
+                 const double *vel, int ndim, double inv_n, double amp, double sigma2,
+                 double beta, const double *sgn, double *out, void *stream);
+
+/* replaces moments_blocks, _kernels.py:109-113 (:81-93).  w f64[m_comm][p+1]. */
+CDK_API int cdk_moments_blocks(const double *x, const int64_t *offsets, int64_t m_comm, int p, double x0,
+                       double norm, double *w, void *stream);
+
+/* replaces dense_poly, _kernels.py:231-235 (:207-217). */
+CDK_API int cdk_dense_poly(const double *x, const int64_t *offsets, int64_t m_comm, const double *tbl,
+                   int p, double scale, double shift, double *out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Fused CIA path: Kuramoto RHS (E1 + E2) inside RK4 stages.                */
+/* ------------------------------------------------------------------------ */
+
+/* Device form of a Decomposition as a directed CSR without
+ * the diagonal, rows in permuted (community-contiguous) order, plus the
+ * static work schedule built by the host planner (paper_2203_16657_b200/plan.py).
+ *   rows [comm_off[c], comm_off[c+1]) form community c; rows >= comm_off[M]
+ *   are the NONE pool (sparse contributions only, SPEC.md evaluator:205).
+ *   intra entries (sign -1): community-local column (uint16), each row's run
+ *   padded to a multiple of 8 with CDK_INTRA_PAD; inter entries (sign +1,
+ *   also every entry of a NONE-pool row): global column (int32).
+ *   rblock = <= 32 consecutive rows of one community (or of the pool);
+ *   segment = a CTA's run of rblocks inside one community. */
+typedef struct cdk_graph {
+  int64_t n_rows;
+  int64_t n_comm;
+  const int64_t *comm_off;      /* [n_comm+1] */
+  const int64_t *intra_ptr;     /* [n_rows+1], multiples of 8 */
+  const uint16_t *intra_col;    /* [intra_ptr[n_rows]] */
+  const int64_t *inter_ptr;     /* [n_rows+1] */
+  const int32_t *inter_col;     /* [inter_ptr[n_rows]] */
+  int32_t n_rblk;
+  int32_t n_seg;
+  int32_t n_cta;
+  int32_t cta_threads;          /* 256 | 512 | 1024 */
+  int32_t smem_nodes;           /* communities with lambda <= smem_nodes are staged in smem */
+  int32_t reserved0;
+  const int64_t *rblk_row0;     /* [n_rblk] */
+  const int32_t *rblk_comm;     /* [n_rblk], -1 = NONE pool */
+  const int32_t *comm_rblk_off; /* [n_comm+1] */
+  const int32_t *seg_rblk;      /* [n_seg+1] rblock boundaries of segments */
+  const int32_t *cta_seg;       /* [n_cta+1] segment boundaries per CTA */
+} cdk_graph;
+
+/* device-side run status (lives inside the workspace) */
+typedef struct cdk_run_status {
+  int64_t nonfinite;      /* number of node-steps that produced a non-finite phase */
+  int64_t first_bad_step; /* first step (1-based, counted from the last prepare) or INT64_MAX */
+  int64_t steps_done;     /* steps advanced since the last prepare */
+  int64_t reserved;
+} cdk_run_status;
+
+/* bytes of device workspace the fused Kuramoto path needs for graph g */
+CDK_API size_t cdk_kuramoto_workspace_bytes(const cdk_graph *g);
+
+/* z = exp(i theta), community sums R, counters and status reset.
+ * Must precede cdk_kuramoto_rk4 whenever theta was changed outside it. */
+CDK_API int cdk_kuramoto_prepare(const cdk_graph *g, const double *theta, void *workspace, void *stream);
+
+/* One CIA right-hand side (eval_rhs_cia + kuramoto_rhs):
+ *   out[i] = omega[i] + k_over_n * Im( (R_c(i) + sum_j s_ij z_j) * conj(z_i) )
+ * with k_over_n = K / N (h = K sin, global 1/N).  Runs prepare internally. */
+CDK_API int cdk_kuramoto_rhs(const cdk_graph *g, const double *theta, const double *omega,
+                     double k_over_n, double *out, void *workspace, void *stream);
+
+/* n_steps classical RK4 steps, phases wrapped to (-pi, pi] after
+ * each full step.  theta is updated in place; the workspace
+ * stays consistent so calls chain without another prepare.  4 kernel launches
+ * per step; graph-capturable. */
+CDK_API int cdk_kuramoto_rk4(const cdk_graph *g, double *theta, const double *omega, double k_over_n,
+                     double dt, int64_t n_steps, void *workspace, void *stream);
+
+/* exactly one RK4 stage kernel (stage 1..4) of the step cdk_kuramoto_rk4 runs;
+ * four calls in order == one step without the status bookkeeping.  Used by the
+ * bench to time the stage kernel alone. */
+CDK_API int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const double *omega,
+                                   double k_over_n, double dt, int stage, void *workspace,
+                                   void *stream);
+
+/* n_steps explicit Euler steps, same wrap/blow-up semantics. */
+CDK_API int cdk_kuramoto_euler(const cdk_graph *g, double *theta, const double *omega, double k_over_n,
+                       double dt, int64_t n_steps, void *workspace, void *stream);
+
+/* copy the workspace's run status to [host] *out (synchronises `stream`). */
+CDK_API int cdk_kuramoto_status(const cdk_graph *g, const void *workspace, cdk_run_status *out,
+                        void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* misc                                                                      */
+/* ------------------------------------------------------------------------ */
+CDK_API int cdk_abi_version(void);
+CDK_API const char *cdk_last_error(void);
+/* number of kernel launches issued by this library since load (for the bench's gpu_launches) */
+CDK_API int64_t cdk_launch_count(void);
+/* max dynamic shared memory per block (opt-in) on the current device */
+CDK_API int cdk_max_smem_optin(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COMMDYN_CUDA_H */

@@ -1,0 +1,134 @@
+"""ctypes binding of libcommdyn_cuda.so (include/commdyn_cuda.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, ``lib()`` raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import CDK_CUDA, CDK_INPUT, CDK_NUMERIC, CDK_OK, DeviceError, InputError, NumericError
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_build", "libcommdyn_cuda.so")
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+D = ctypes.c_double
+I = ctypes.c_int
+
+
+class CdkGraph(ctypes.Structure):
+    _fields_ = [
+        ("n_rows", I64),
+        ("n_comm", I64),
+        ("comm_off", P),
+        ("intra_ptr", P),
+        ("intra_col", P),
+        ("inter_ptr", P),
+        ("inter_col", P),
+        ("n_rblk", I32),
+        ("n_seg", I32),
+        ("n_cta", I32),
+        ("cta_threads", I32),
+        ("smem_nodes", I32),
+        ("reserved0", I32),
+        ("rblk_row0", P),
+        ("rblk_comm", P),
+        ("comm_rblk_off", P),
+        ("seg_rblk", P),
+        ("cta_seg", P),
+    ]
+
+
+class CdkRunStatus(ctypes.Structure):
+    _fields_ = [("nonfinite", I64), ("first_bad_step", I64), ("steps_done", I64),
+                ("reserved", I64)]
+
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+_SIGS = {
+    "cdk_order_params_blocks": [P, P, I64, I, D, D, P, P],
+    "cdk_dense_complex": [P, P, I64, P, I, D, P, P, P],
+    "cdk_dense_real": [P, P, I64, P, P, I, D, P, P],
+    "cdk_pairs_trig": [P, P, I64, P, D, P, P, I, D, P, P, P],
+    "cdk_pairs_cs": [P, P, I64, P, P, I, D, D, D, D, P, P, P],
+    "cdk_moments_blocks": [P, P, I64, I, D, D, P, P],
+    "cdk_dense_poly": [P, P, I64, P, I, D, D, P, P],
+    "cdk_kuramoto_workspace_bytes": [ctypes.POINTER(CdkGraph)],
+    "cdk_kuramoto_prepare": [ctypes.POINTER(CdkGraph), P, P, P],
+    "cdk_kuramoto_rhs": [ctypes.POINTER(CdkGraph), P, P, D, P, P, P],
+    "cdk_kuramoto_rk4": [ctypes.POINTER(CdkGraph), P, P, D, D, I64, P, P],
+    "cdk_kuramoto_rk4_stage": [ctypes.POINTER(CdkGraph), P, P, D, D, I, P, P],
+    "cdk_kuramoto_euler": [ctypes.POINTER(CdkGraph), P, P, D, D, I64, P, P],
+    "cdk_kuramoto_status": [ctypes.POINTER(CdkGraph), P, ctypes.POINTER(CdkRunStatus), P],
+    "cdk_abi_version": [],
+    "cdk_last_error": [],
+    "cdk_launch_count": [],
+    "cdk_max_smem_optin": [],
+}
+_RESTYPES = {
+    "cdk_kuramoto_workspace_bytes": ctypes.c_size_t,
+    "cdk_last_error": ctypes.c_char_p,
+    "cdk_launch_count": I64,
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the shared library and bind every declared symbol (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise DeviceError(
+                f"{path} is missing: build it with __graft_entry__.build() "
+                "(there is no CPU fallback for the CUDA path)"
+            )
+        lib = ctypes.CDLL(path)
+        for name, argtypes in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        if lib.cdk_abi_version() != 1:
+            raise DeviceError("libcommdyn_cuda.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def lib():
+    """The loaded library, after checking a CUDA device is present."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the commdyn CUDA backend has no CPU fallback")
+    return load_library()
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == CDK_OK:
+        return
+    msg = (_lib.cdk_last_error() or b"").decode() if _lib is not None else ""
+    if rc == CDK_INPUT:
+        raise InputError(f"{what}: {msg}")
+    if rc == CDK_NUMERIC:
+        raise NumericError(f"{what}: {msg}")
+    if rc == CDK_CUDA:
+        raise DeviceError(f"{what}: {msg}")
+    raise DeviceError(f"{what}: unknown status {rc}")
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

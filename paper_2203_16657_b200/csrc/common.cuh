@@ -1,0 +1,60 @@
+// Shared device helpers for libcommdyn_cuda.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/commdyn_cuda.h"
+
+namespace cdk {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// --- error plumbing ---------------------------------------------------------
+void set_error(const std::string &msg);
+extern std::atomic<int64_t> g_launches;
+
+inline int cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return CDK_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return CDK_CUDA;
+}
+
+#define CDK_CHECK_LAUNCH(what)                                   \
+  do {                                                           \
+    ::cdk::g_launches.fetch_add(1, std::memory_order_relaxed);   \
+    cudaError_t _e = cudaGetLastError();                         \
+    if (_e != cudaSuccess) return ::cdk::cuda_status(_e, what);  \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// --- IEEE ops that must not be contracted into FMA (mirror numpy rounding) --
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// wrap to (-pi, pi]: x - 2pi*ceil((x - pi)/(2pi)), same formula as oracle/cia.py
+__device__ __forceinline__ double wrap_phase(double x) {
+  const double PI = 3.141592653589793;
+  const double TWO_PI = 6.283185307179586;
+  double k = ceil(__ddiv_rn(__dsub_rn(x, PI), TWO_PI));
+  return __dsub_rn(x, __dmul_rn(TWO_PI, k));
+}
+
+// --- loads ------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T ldg(const T *p) { return __ldg(p); }
+
+__device__ __forceinline__ double2 ldcg2(const double2 *p) { return __ldcg(p); }
+
+// --- warp reductions (xor butterfly: every lane ends with the same bits) ----
+__device__ __forceinline__ double warp_sum(double v, int width = 32) {
+  for (int o = width >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+}  // namespace cdk

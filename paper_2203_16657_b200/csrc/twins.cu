@@ -1,0 +1,333 @@
+// Kernel-level twins of the reference dispatchers (commdyn/_kernels.py), same
+// array contracts, for literal drop-in and per-kernel parity testing.  The
+// trajectory hot path does NOT use these (it runs the fused kernels in
+// kuramoto.cu); they exist so every reference dispatcher on the path has a
+// device counterpart.
+#include "common.cuh"
+
+namespace cdk {
+
+constexpr int TW_MAXP = 16;  // order/moment twins support p <= 16
+constexpr int TW_THREADS = 256;
+
+// block-wide fixed-order sum (warp butterflies, then warp 0 over warp totals)
+__device__ double block_sum(double v, double *sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = (lane < nw) ? sh[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sh[32] = r;
+  __syncthreads();
+  return sh[32];
+}
+
+__device__ __forceinline__ int find_comm(const int64_t *offsets, int64_t m_comm, int64_t node) {
+  int64_t lo = 0, hi = m_comm;  // offsets[lo] <= node < offsets[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ldg(offsets + mid) <= node) lo = mid; else hi = mid;
+  }
+  return (int)lo;
+}
+
+// _kernels.py:34-51
+__global__ void order_params_kernel(const double *x, const int64_t *offsets, int p,
+                                    double pi_over_l, double norm, double2 *r) {
+  __shared__ double sh[33];
+  const int c = blockIdx.x;
+  const int64_t b = offsets[c], e = offsets[c + 1];
+  double ar[TW_MAXP], ai[TW_MAXP];
+#pragma unroll
+  for (int a = 0; a < TW_MAXP; ++a) ar[a] = ai[a] = 0.0;
+  for (int64_t m = b + threadIdx.x; m < e; m += blockDim.x) {
+    double s, co;
+    sincos(pi_over_l * x[m], &s, &co);
+    double pr = 1.0, pim = 0.0;
+#pragma unroll
+    for (int a = 0; a < TW_MAXP; ++a) {
+      if (a < p) {
+        const double nr = pr * co - pim * s;
+        const double ni = pr * s + pim * co;
+        pr = nr;
+        pim = ni;
+        ar[a] += pr;
+        ai[a] += pim;
+      }
+    }
+  }
+  const int w = 2 * p + 1;
+  for (int a = 0; a < p; ++a) {
+    const double sr = block_sum(ar[a], sh);
+    const double si = block_sum(ai[a], sh);
+    if (threadIdx.x == 0) {
+      r[(int64_t)c * w + p + 1 + a] = make_double2(sr / norm, si / norm);
+      r[(int64_t)c * w + p - 1 - a] = make_double2(sr / norm, -(si / norm));
+    }
+  }
+  if (threadIdx.x == 0) r[(int64_t)c * w + p] = make_double2((double)(e - b) / norm, 0.0);
+}
+
+// _kernels.py:124-149
+__global__ void dense_complex_kernel(const double *x, const int64_t *offsets, int64_t m_comm,
+                                     const double2 *tbl, int p, double pi_over_l, double *out,
+                                     unsigned long long *guard) {
+  const int64_t n_in = offsets[m_comm];
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n_in) return;
+  const int c = find_comm(offsets, m_comm, m);
+  const double2 *tc = tbl + (int64_t)c * (2 * p + 1);
+  double wi, wr;
+  sincos(pi_over_l * x[m], &wi, &wr);
+  double accr = tc[2 * p].x, acci = tc[2 * p].y;
+  for (int j = 2 * p - 1; j >= 0; --j) {
+    const double nr = accr * wr - acci * wi + tc[j].x;
+    const double ni = accr * wi + acci * wr + tc[j].y;
+    accr = nr;
+    acci = ni;
+  }
+  double sr = 1.0, si = 0.0;  // wbar^p
+  for (int k = 0; k < p; ++k) {
+    const double nr = sr * wr + si * wi;
+    const double ni = si * wr - sr * wi;
+    sr = nr;
+    si = ni;
+  }
+  const double vr = accr * sr - acci * si;
+  const double vi = fabs(accr * si + acci * sr);
+  out[m] += vr;
+  if (vi > 1e-9 * (1.0 + fabs(vr))) atomicAdd(guard, 1ull);
+  atomicMax(reinterpret_cast<unsigned long long *>(guard + 1),
+            (unsigned long long)__double_as_longlong(vi));
+}
+
+// _kernels.py:172-187
+__global__ void dense_real_kernel(const double *x, const int64_t *offsets, int64_t m_comm,
+                                  const double *tcos, const double *tsin, int p, double pi_over_l,
+                                  double *out) {
+  const int64_t n_in = offsets[m_comm];
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n_in) return;
+  const int c = find_comm(offsets, m_comm, m);
+  double s1, c1;
+  sincos(pi_over_l * x[m], &s1, &c1);
+  double ck = 1.0, sk = 0.0, val = tcos[(int64_t)c * (p + 1)];
+  for (int b = 1; b <= p; ++b) {
+    const double nck = ck * c1 - sk * s1;
+    const double nsk = sk * c1 + ck * s1;
+    ck = nck;
+    sk = nsk;
+    val += tcos[(int64_t)c * (p + 1) + b] * ck + tsin[(int64_t)c * (p + 1) + b] * sk;
+  }
+  out[m] += val;
+}
+
+// _kernels.py:246-283 (scatter to both ends, fp64 atomics)
+__global__ void pairs_trig_kernel(const int64_t *iu, const int64_t *iv, int64_t n_pairs,
+                                  const double *x, double inv_n, const double *d_cos,
+                                  const double *d_sin, int p, double pi_over_l, const double *sgn,
+                                  double *out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_pairs) return;
+  const int64_t u = iu[e], v = iv[e];
+  const double s = sgn[e] * inv_n;
+  double s1, c1;
+  sincos(pi_over_l * (x[v] - x[u]), &s1, &c1);
+  double ck = 1.0, sk = 0.0, hp = d_cos[0], hm = d_cos[0];
+  for (int a = 1; a <= p; ++a) {
+    const double nck = ck * c1 - sk * s1;
+    const double nsk = sk * c1 + ck * s1;
+    ck = nck;
+    sk = nsk;
+    hp += d_cos[a] * ck + d_sin[a] * sk;
+    hm += d_cos[a] * ck - d_sin[a] * sk;
+  }
+  atomicAdd(out + u, s * hp);
+  if (u != v) atomicAdd(out + v, s * hm);
+}
+
+// _kernels.py:297-314
+__global__ void pairs_cs_kernel(const int64_t *iu, const int64_t *iv, int64_t n_pairs,
+                                const double *pos, const double *vel, int ndim, double inv_n,
+                                double amp, double sigma2, double beta, const double *sgn,
+                                double *out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_pairs) return;
+  const int64_t u = iu[e], v = iv[e];
+  if (u == v) return;
+  double d2 = 0.0;
+  for (int d = 0; d < ndim; ++d) {
+    const double dd = pos[v * ndim + d] - pos[u * ndim + d];
+    d2 += dd * dd;
+  }
+  const double eta = amp / pow(sigma2 + d2, beta);
+  const double s = sgn[e] * inv_n * eta;
+  for (int d = 0; d < ndim; ++d) {
+    const double dv = vel[v * ndim + d] - vel[u * ndim + d];
+    atomicAdd(out + u * ndim + d, s * dv);
+    atomicAdd(out + v * ndim + d, -(s * dv));
+  }
+}
+
+// _kernels.py:81-93
+__global__ void moments_kernel(const double *x, const int64_t *offsets, int p, double x0,
+                               double norm, double *w) {
+  __shared__ double sh[33];
+  const int c = blockIdx.x;
+  const int64_t b = offsets[c], e = offsets[c + 1];
+  double acc[TW_MAXP + 1];
+#pragma unroll
+  for (int a = 0; a <= TW_MAXP; ++a) acc[a] = 0.0;
+  for (int64_t m = b + threadIdx.x; m < e; m += blockDim.x) {
+    const double t = x[m] - x0;
+    double tp = 1.0;
+    acc[0] += 1.0;
+#pragma unroll
+    for (int a = 1; a <= TW_MAXP; ++a) {
+      if (a <= p) {
+        tp = tp * t;
+        acc[a] += tp;
+      }
+    }
+  }
+  for (int a = 0; a <= p; ++a) {
+    const double sa = block_sum(acc[a], sh);
+    if (threadIdx.x == 0) w[(int64_t)c * (p + 1) + a] = sa / norm;
+  }
+}
+
+// _kernels.py:207-217
+__global__ void dense_poly_kernel(const double *x, const int64_t *offsets, int64_t m_comm,
+                                  const double *tbl, int p, double scale, double shift,
+                                  double *out) {
+  const int64_t n_in = offsets[m_comm];
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n_in) return;
+  const int c = find_comm(offsets, m_comm, m);
+  const double *tc = tbl + (int64_t)c * (p + 1);
+  const double t = scale * x[m] + shift;
+  double val = tc[p];
+  for (int b = p - 1; b >= 0; --b) val = val * t + tc[b];
+  out[m] += val;
+}
+
+static inline unsigned grid_for(int64_t n) {
+  return (unsigned)((n + TW_THREADS - 1) / TW_THREADS);
+}
+
+static int need_offsets_host(const int64_t *offsets_dev, int64_t m_comm, int64_t *n_in,
+                             cudaStream_t st) {
+  // n_in = offsets[m_comm] is read on the device by every per-node twin; only
+  // an emptiness check is needed on the host to avoid zero-size grids.
+  cudaError_t e = cudaMemcpyAsync(n_in, offsets_dev + m_comm, sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_status(e, "read offsets[-1]");
+}
+
+}  // namespace cdk
+
+using namespace cdk;
+
+extern "C" int cdk_order_params_blocks(const double *x, const int64_t *offsets, int64_t m_comm,
+                                       int p, double pi_over_l, double norm, double *r,
+                                       void *stream) {
+  if (p < 0 || p > TW_MAXP || m_comm < 0) {
+    set_error("order_params_blocks: need 0 <= p <= 16");
+    return CDK_INPUT;
+  }
+  if (m_comm == 0) return CDK_OK;
+  order_params_kernel<<<(unsigned)m_comm, TW_THREADS, 0, as_stream(stream)>>>(
+      x, offsets, p, pi_over_l, norm, reinterpret_cast<double2 *>(r));
+  CDK_CHECK_LAUNCH("order_params_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_dense_complex(const double *x, const int64_t *offsets, int64_t m_comm,
+                                 const double *tbl, int p, double pi_over_l, double *out,
+                                 void *guard, void *stream) {
+  if (p < 0 || m_comm < 0) return set_error("dense_complex: bad p"), CDK_INPUT;
+  if (m_comm == 0) return CDK_OK;
+  cudaStream_t st = as_stream(stream);
+  int64_t n_in = 0;
+  int rc = need_offsets_host(offsets, m_comm, &n_in, st);
+  if (rc || n_in == 0) return rc;
+  dense_complex_kernel<<<grid_for(n_in), TW_THREADS, 0, st>>>(
+      x, offsets, m_comm, reinterpret_cast<const double2 *>(tbl), p, pi_over_l, out,
+      reinterpret_cast<unsigned long long *>(guard));
+  CDK_CHECK_LAUNCH("dense_complex_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_dense_real(const double *x, const int64_t *offsets, int64_t m_comm,
+                              const double *tbl_cos, const double *tbl_sin, int p,
+                              double pi_over_l, double *out, void *stream) {
+  if (p < 0 || m_comm < 0) return set_error("dense_real: bad p"), CDK_INPUT;
+  if (m_comm == 0) return CDK_OK;
+  cudaStream_t st = as_stream(stream);
+  int64_t n_in = 0;
+  int rc = need_offsets_host(offsets, m_comm, &n_in, st);
+  if (rc || n_in == 0) return rc;
+  dense_real_kernel<<<grid_for(n_in), TW_THREADS, 0, st>>>(x, offsets, m_comm, tbl_cos, tbl_sin,
+                                                            p, pi_over_l, out);
+  CDK_CHECK_LAUNCH("dense_real_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_pairs_trig(const int64_t *iu, const int64_t *iv, int64_t n_pairs,
+                              const double *x, double inv_n, const double *d_cos,
+                              const double *d_sin, int p, double pi_over_l, const double *sgn,
+                              double *out, void *stream) {
+  if (p < 0 || n_pairs < 0) return set_error("pairs_trig: bad sizes"), CDK_INPUT;
+  if (n_pairs == 0) return CDK_OK;
+  pairs_trig_kernel<<<grid_for(n_pairs), TW_THREADS, 0, as_stream(stream)>>>(
+      iu, iv, n_pairs, x, inv_n, d_cos, d_sin, p, pi_over_l, sgn, out);
+  CDK_CHECK_LAUNCH("pairs_trig_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_pairs_cs(const int64_t *iu, const int64_t *iv, int64_t n_pairs,
+                            const double *pos, const double *vel, int ndim, double inv_n,
+                            double amp, double sigma2, double beta, const double *sgn,
+                            double *out, void *stream) {
+  if (ndim < 1 || n_pairs < 0) return set_error("pairs_cs: bad sizes"), CDK_INPUT;
+  if (n_pairs == 0) return CDK_OK;
+  pairs_cs_kernel<<<grid_for(n_pairs), TW_THREADS, 0, as_stream(stream)>>>(
+      iu, iv, n_pairs, pos, vel, ndim, inv_n, amp, sigma2, beta, sgn, out);
+  CDK_CHECK_LAUNCH("pairs_cs_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_moments_blocks(const double *x, const int64_t *offsets, int64_t m_comm, int p,
+                                  double x0, double norm, double *w, void *stream) {
+  if (p < 0 || p > TW_MAXP || m_comm < 0) {
+    set_error("moments_blocks: need 0 <= p <= 16");
+    return CDK_INPUT;
+  }
+  if (m_comm == 0) return CDK_OK;
+  moments_kernel<<<(unsigned)m_comm, TW_THREADS, 0, as_stream(stream)>>>(x, offsets, p, x0, norm,
+                                                                          w);
+  CDK_CHECK_LAUNCH("moments_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_dense_poly(const double *x, const int64_t *offsets, int64_t m_comm,
+                              const double *tbl, int p, double scale, double shift, double *out,
+                              void *stream) {
+  if (p < 0 || m_comm < 0) return set_error("dense_poly: bad p"), CDK_INPUT;
+  if (m_comm == 0) return CDK_OK;
+  cudaStream_t st = as_stream(stream);
+  int64_t n_in = 0;
+  int rc = need_offsets_host(offsets, m_comm, &n_in, st);
+  if (rc || n_in == 0) return rc;
+  dense_poly_kernel<<<grid_for(n_in), TW_THREADS, 0, st>>>(x, offsets, m_comm, tbl, p, scale,
+                                                            shift, out);
+  CDK_CHECK_LAUNCH("dense_poly_kernel");
+  return CDK_OK;
+}

@@ -1,0 +1,111 @@
+"""Device-resident CIA engine for the Kuramoto family (the fused hot path).
+
+``KuramotoEngine`` owns the DeviceGraph, the workspace and the device state
+(theta, omega in permuted order) and drives the C ABI:
+
+    eng = KuramotoEngine(dec, omega_perm, coupling=K, norm=N)
+    eng.set_state(theta_perm)      # prepare: z = exp(i theta), community sums
+    eng.rk4(dt, n_steps)           # 4 fused stage kernels per step
+    eng.status()                   # -> BlowUpError on non-finite state
+
+No CPU fallback: every method calls libcommdyn_cuda.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import BlowUpError, InputError
+from .plan import DeviceGraph
+
+
+class KuramotoEngine:
+    def __init__(self, dec, omega, coupling: float = 1.0, norm: float | None = None,
+                 device=None, graph: DeviceGraph | None = None):
+        import torch
+
+        self.lib = _lib.lib()
+        self.graph = graph if graph is not None else DeviceGraph(dec, device=device)
+        self.device = self.graph.device
+        n = self.graph.n_rows
+        self.n = n
+        self.coupling = float(coupling)
+        self.norm = float(norm if norm is not None else n)
+        self.k_over_n = self.coupling / self.norm
+        omega = torch.as_tensor(np.asarray(omega, dtype=np.float64) if not torch.is_tensor(omega)
+                                else omega, dtype=torch.float64)
+        if omega.shape != (n,):
+            raise InputError(f"omega must have shape ({n},)")
+        self.omega = omega.to(self.device).contiguous()
+        self.theta = torch.zeros(n, dtype=torch.float64, device=self.device)
+        nbytes = int(self.lib.cdk_kuramoto_workspace_bytes(ctypes.byref(self.graph.struct)))
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        self._gp = ctypes.byref(self.graph.struct)
+        self._rhs_ws = None
+
+    # -- state --------------------------------------------------------------
+    def set_state(self, theta, stream=None) -> None:
+        import torch
+
+        t = theta if torch.is_tensor(theta) else torch.from_numpy(np.ascontiguousarray(theta,
+                                                                                   np.float64))
+        if t.shape != (self.n,):
+            raise InputError(f"state must have shape ({self.n},)")
+        self.theta.copy_(t.to(self.device, torch.float64), non_blocking=True)
+        self.prepare(stream)
+
+    def prepare(self, stream=None) -> None:
+        _lib.check(self.lib.cdk_kuramoto_prepare(self._gp, self.theta.data_ptr(),
+                                                 self.workspace.data_ptr(),
+                                                 _lib.stream_ptr(stream)), "prepare")
+
+    # -- evaluation ---------------------------------------------------------
+    def rhs(self, theta=None, out=None, stream=None):
+        """One CIA RHS at ``theta`` (default: current state).  Returns a device tensor."""
+        import torch
+
+        th = self.theta if theta is None else torch.as_tensor(theta, dtype=torch.float64,
+                                                              device=self.device).contiguous()
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        if self._rhs_ws is None:  # separate workspace: never disturbs a running trajectory
+            self._rhs_ws = torch.empty_like(self.workspace)
+        _lib.check(self.lib.cdk_kuramoto_rhs(self._gp, th.data_ptr(), self.omega.data_ptr(),
+                                             self.k_over_n, out.data_ptr(),
+                                             self._rhs_ws.data_ptr(), _lib.stream_ptr(stream)),
+                   "kuramoto_rhs")
+        return out
+
+    def rk4(self, dt: float, n_steps: int, stream=None) -> None:
+        _lib.check(self.lib.cdk_kuramoto_rk4(self._gp, self.theta.data_ptr(),
+                                             self.omega.data_ptr(), self.k_over_n, float(dt),
+                                             int(n_steps), self.workspace.data_ptr(),
+                                             _lib.stream_ptr(stream)), "kuramoto_rk4")
+
+    def rk4_stage(self, dt: float, stage: int, stream=None) -> None:
+        _lib.check(self.lib.cdk_kuramoto_rk4_stage(self._gp, self.theta.data_ptr(),
+                                                   self.omega.data_ptr(), self.k_over_n,
+                                                   float(dt), int(stage),
+                                                   self.workspace.data_ptr(),
+                                                   _lib.stream_ptr(stream)), "rk4_stage")
+
+    def euler(self, dt: float, n_steps: int, stream=None) -> None:
+        _lib.check(self.lib.cdk_kuramoto_euler(self._gp, self.theta.data_ptr(),
+                                               self.omega.data_ptr(), self.k_over_n, float(dt),
+                                               int(n_steps), self.workspace.data_ptr(),
+                                               _lib.stream_ptr(stream)), "kuramoto_euler")
+
+    def status(self, stream=None) -> _lib.CdkRunStatus:
+        st = _lib.CdkRunStatus()
+        _lib.check(self.lib.cdk_kuramoto_status(self._gp, self.workspace.data_ptr(),
+                                                ctypes.byref(st), _lib.stream_ptr(stream)),
+                   "status")
+        return st
+
+    def check(self, step_offset: int = 0, stream=None) -> None:
+        st = self.status(stream)
+        if st.nonfinite:
+            raise BlowUpError(int(st.first_bad_step) + step_offset)

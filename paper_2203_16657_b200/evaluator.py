@@ -1,0 +1,68 @@
+"""Evaluator: CIA right-hand side and the direct-sum RHS.
+
+* ``eval_rhs_cia``   SPEC.md:359-366 — E1 (community observables) + E2 (signed
+                     sparse correction with the exact coupling) + intrinsic term,
+                     one fused kernel (cdk_kuramoto_rhs).
+* ``eval_rhs_naive`` SPEC.md:368-374 — direct sum over the graph's edges with the
+                     exact coupling (cdk_pairs_trig over the full edge list,
+                     sgn = +1).  Memory guard N > 2^15 as SPEC.md:614.
+
+Both take and return states in ORIGINAL node order (numpy).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _kernels
+from .engine import KuramotoEngine
+from .errors import InputError, MemoryGuardError
+from .graph import Decomposition, Graph
+from .models import Kuramoto
+from .plan import DeviceGraph
+
+NAIVE_N_CAP = 2**15
+
+
+def _engine(model: Kuramoto, dec: Decomposition) -> KuramotoEngine:
+    cached = dec._cache.get("engine")  # (model, engine) of the most recent model
+    eng = cached[1] if cached is not None and cached[0] is model else None
+    if eng is None:
+        perm = dec.partition.perm
+        dg = dec._cache.get("device_graph")
+        if dg is None:
+            dg = dec._cache["device_graph"] = DeviceGraph(dec)
+        eng = KuramotoEngine(dec, np.asarray(model.omega)[perm], coupling=model.coupling,
+                             norm=model.norm_value(), graph=dg)
+        dec._cache["engine"] = (model, eng)
+    return eng
+
+
+def eval_rhs_cia(model, dec: Decomposition, state) -> np.ndarray:
+    if not isinstance(model, Kuramoto):
+        raise InputError(f"eval_rhs_cia: unsupported model {type(model).__name__}")
+    x = np.asarray(state, dtype=np.float64)
+    if x.shape != (dec.n_nodes,):
+        raise InputError("state shape does not match the decomposition")
+    perm = dec.partition.perm
+    eng = _engine(model, dec)
+    out_perm = eng.rhs(x[perm]).cpu().numpy()
+    out = np.empty_like(out_perm)
+    out[perm] = out_perm
+    return out
+
+
+def eval_rhs_naive(model, graph: Graph, state) -> np.ndarray:
+    if not isinstance(model, Kuramoto):
+        raise InputError(f"eval_rhs_naive: unsupported model {type(model).__name__}")
+    if graph.n_nodes > NAIVE_N_CAP:
+        raise MemoryGuardError(f"naive mode refuses N = {graph.n_nodes} > {NAIVE_N_CAP} "
+                               "(O(N^2) edge list; SPEC.md:614)")
+    x = np.asarray(state, dtype=np.float64)
+    out = np.array(model.omega, dtype=np.float64, copy=True)
+    e = graph.edges
+    _kernels.pairs_trig(e[:, 0], e[:, 1], x, 1.0 / model.norm_value(), np.zeros(2),
+                        np.array([0.0, model.coupling]), math.pi, np.ones(e.shape[0]), out)
+    return out

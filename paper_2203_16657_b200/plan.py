@@ -1,0 +1,225 @@
+"""Host planner: Decomposition -> device CSR layout + static work schedule.
+
+Turns the reference's wire format (sorted unordered COO triples (iu, iv, sgn)
+with the diagonal) into the layout the fused kernels
+stream (include/commdyn_cuda.h, struct cdk_graph):
+
+* directed CSR without the diagonal (sin(0) = 0 for the Kuramoto family;
+  for general h the diagonal is a per-node constant);
+* the sign is implied by the column's community, so no sign bytes are
+  stored: intra (-1) entries as uint16 community-local columns, each row's
+  run padded to a multiple of 8 (one 16-byte vector load per lane), inter
+  (+1) entries as int32 global columns;
+* 32-row "rblocks" (never straddling a community), cost-balanced contiguous
+  CTA ranges, and "segments" = a CTA's run inside one community (the unit of
+  shared-memory staging of that community's state).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import InputError
+from .graph import NONE, Decomposition
+
+RB = 32
+INTRA_PAD = 0xFFFF
+ROW_COST = 24.0  # per-row overhead in "entry" units (pointer loads, epilogue, sincos)
+INTER_COST = 3.0  # an inter entry: 4-byte index + an L2 gather
+DEFAULT_SMS = 148
+SMEM_OPTIN = 232448  # B200 max dynamic smem per block (227 KB)
+SMEM_PER_SM = 233472  # 228 KB per SM
+
+
+@dataclass
+class HostLayout:
+    n_rows: int
+    n_comm: int
+    comm_off: np.ndarray
+    intra_ptr: np.ndarray
+    intra_col: np.ndarray
+    inter_ptr: np.ndarray
+    inter_col: np.ndarray
+    rblk_row0: np.ndarray
+    rblk_comm: np.ndarray
+    comm_rblk_off: np.ndarray
+    row_cost: np.ndarray
+    nnz_intra: int
+    nnz_inter: int
+
+    @property
+    def nnz_dir(self) -> int:
+        return self.nnz_intra + self.nnz_inter
+
+    @property
+    def n_rblk(self) -> int:
+        return int(self.rblk_row0.shape[0])
+
+    def nbytes(self) -> int:
+        return int(sum(a.nbytes for a in (self.comm_off, self.intra_ptr, self.intra_col,
+                                           self.inter_ptr, self.inter_col)))
+
+
+@dataclass
+class Schedule:
+    n_cta: int
+    cta_threads: int
+    smem_nodes: int
+    seg_rblk: np.ndarray  # int32[n_seg+1]
+    cta_seg: np.ndarray  # int32[n_cta+1]
+
+    @property
+    def n_seg(self) -> int:
+        return int(self.seg_rblk.shape[0] - 1)
+
+
+def _row_runs(rows_sorted: np.ndarray, n_rows: int):
+    counts = np.bincount(rows_sorted, minlength=n_rows).astype(np.int64)
+    start = np.zeros(n_rows + 1, dtype=np.int64)
+    np.cumsum(counts, out=start[1:])
+    return counts, start
+
+
+def build_layout(dec: Decomposition) -> HostLayout:
+    part = dec.partition
+    n = int(dec.n_nodes)
+    off = part.offsets
+    m = part.n_comm
+    if m and int(part.sizes.max()) > INTRA_PAD:
+        raise InputError("community larger than 65535 nodes: uint16 intra columns do not fit")
+    comm = part.comm_of_permuted()
+    rows, cols, sg = dec.directed()
+    cr = comm[rows]
+    intra = (cr == comm[cols]) & (cr != NONE)
+    if np.any(sg[intra] != -1) or np.any(sg[~intra] != 1):
+        raise InputError("sparse correction signs inconsistent with the partition "
+                         "(-1 must be intra-community, +1 inter-community)")
+
+    # intra: uint16 local columns, rows padded to multiples of 8
+    key = (rows[intra].astype(np.int64) << 16) | (cols[intra] - off[cr[intra]])
+    key.sort()
+    ri = key >> 16
+    ci = (key & 0xFFFF).astype(np.uint16)
+    counts, start = _row_runs(ri, n)
+    padded = (counts + 7) // 8 * 8
+    intra_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(padded, out=intra_ptr[1:])
+    intra_col = np.full(int(intra_ptr[-1]), INTRA_PAD, dtype=np.uint16)
+    rank = np.arange(ri.shape[0], dtype=np.int64) - start[ri]
+    intra_col[intra_ptr[ri] + rank] = ci
+    nnz_intra = int(ri.shape[0])
+    del key, ri, ci, rank
+
+    # inter: int32 global columns
+    rx = rows[~intra]
+    cx = cols[~intra]
+    order = np.lexsort((cx, rx))
+    rx = rx[order]
+    inter_col = cx[order].astype(np.int32)
+    xcounts, inter_ptr = _row_runs(rx, n)
+    nnz_inter = int(rx.shape[0])
+
+    # rblocks: communities, then the NONE pool
+    n_in = int(off[-1])
+    sizes = np.diff(off)
+    nb = (sizes + RB - 1) // RB
+    comm_rblk_off = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(nb, out=comm_rblk_off[1:])
+    rc = np.repeat(np.arange(m, dtype=np.int64), nb)
+    within = np.arange(rc.shape[0], dtype=np.int64) - comm_rblk_off[rc]
+    row0 = off[rc] + RB * within
+    pool_row0 = np.arange(n_in, n, RB, dtype=np.int64)
+    rblk_row0 = np.concatenate([row0, pool_row0])
+    rblk_comm = np.concatenate([rc, np.full(pool_row0.shape[0], -1, np.int64)]).astype(np.int32)
+    row_cost = padded.astype(np.float64) + INTER_COST * xcounts + ROW_COST
+    return HostLayout(n, m, off.astype(np.int64), intra_ptr, intra_col, inter_ptr, inter_col,
+                      rblk_row0, rblk_comm, comm_rblk_off.astype(np.int32), row_cost,
+                      nnz_intra, nnz_inter)
+
+
+def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, cta_threads: int = 512,
+                   smem_optin: int = SMEM_OPTIN, ctas_per_sm: int | None = None) -> Schedule:
+    sizes = np.diff(lay.comm_off)
+    fits = sizes[sizes * 16 <= smem_optin - 1024]
+    smem_nodes = int(fits.max()) if fits.size else 0
+    if ctas_per_sm is None:
+        per_cta = 16 * smem_nodes + 2048
+        ctas_per_sm = max(1, min(2, SMEM_PER_SM // max(per_cta, 1)))
+    n_cta = max(1, sm_count * ctas_per_sm)
+    nrb = lay.n_rblk
+    # cost per rblock (rows are contiguous across rblocks)
+    cum = np.concatenate([[0.0], np.cumsum(lay.row_cost)])
+    rb_end = np.concatenate([lay.rblk_row0[1:], [lay.n_rows]]) if nrb else np.empty(0, np.int64)
+    rb_cost = cum[rb_end] - cum[lay.rblk_row0] if nrb else np.empty(0)
+    # staging cost: charge lambda/8 once per rblock's community start (approximation)
+    cum_rb = np.concatenate([[0.0], np.cumsum(rb_cost)])
+    total = cum_rb[-1]
+    targets = total * np.arange(1, n_cta) / n_cta
+    cuts = np.searchsorted(cum_rb, targets, side="left").astype(np.int64)
+    cuts = np.clip(cuts, 0, nrb)
+    cta_bounds = np.concatenate([[0], cuts, [nrb]]).astype(np.int64)
+    cta_bounds = np.maximum.accumulate(cta_bounds)
+    comm_starts = lay.comm_rblk_off.astype(np.int64)
+    bounds = np.unique(np.concatenate([cta_bounds, comm_starts, [lay.comm_rblk_off[-1], nrb]]))
+    bounds = bounds[(bounds >= 0) & (bounds <= nrb)]
+    seg_rblk = bounds.astype(np.int32)
+    cta_seg = np.searchsorted(bounds, cta_bounds).astype(np.int32)
+    return Schedule(n_cta, cta_threads, smem_nodes, seg_rblk, cta_seg)
+
+
+class DeviceGraph:
+    """Device-resident layout + schedule; owns the torch tensors behind the
+    cdk_graph struct handed to the C ABI."""
+
+    def __init__(self, dec: Decomposition, device=None, sm_count: int | None = None):
+        import torch
+
+        from ._lib import CdkGraph
+
+        dev = torch.device(device if device is not None else "cuda")
+        if sm_count is None:
+            sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        lay = build_layout(dec)
+        sch = build_schedule(lay, sm_count=sm_count)
+        self.layout = lay
+        self.schedule = sch
+        self.n_rows = lay.n_rows
+        self.n_comm = lay.n_comm
+        self.device = dev
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+        # uint16 has no torch dtype with from_numpy in older builds: ship as int16 bits
+        self._t = {
+            "comm_off": up(lay.comm_off),
+            "intra_ptr": up(lay.intra_ptr),
+            "intra_col": up(lay.intra_col.view(np.int16)),
+            "inter_ptr": up(lay.inter_ptr),
+            "inter_col": up(lay.inter_col),
+            "rblk_row0": up(lay.rblk_row0),
+            "rblk_comm": up(lay.rblk_comm),
+            "comm_rblk_off": up(lay.comm_rblk_off),
+            "seg_rblk": up(sch.seg_rblk),
+            "cta_seg": up(sch.cta_seg),
+        }
+        # keep a 16-byte tail on intra_col so uint4 loads never run past the allocation
+        if self._t["intra_col"].numel() == 0:
+            self._t["intra_col"] = torch.full((8,), -1, dtype=torch.int16, device=dev)
+        t = self._t
+        self.struct = CdkGraph(
+            n_rows=lay.n_rows, n_comm=lay.n_comm,
+            comm_off=t["comm_off"].data_ptr(), intra_ptr=t["intra_ptr"].data_ptr(),
+            intra_col=t["intra_col"].data_ptr(), inter_ptr=t["inter_ptr"].data_ptr(),
+            inter_col=t["inter_col"].data_ptr() if t["inter_col"].numel() else 0,
+            n_rblk=lay.n_rblk, n_seg=sch.n_seg, n_cta=sch.n_cta, cta_threads=sch.cta_threads,
+            smem_nodes=sch.smem_nodes, reserved0=0,
+            rblk_row0=t["rblk_row0"].data_ptr(), rblk_comm=t["rblk_comm"].data_ptr(),
+            comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
+            cta_seg=t["cta_seg"].data_ptr(),
+        )
+
+    def device_bytes(self) -> int:
+        return int(sum(v.numel() * v.element_size() for v in self._t.values()))
