@@ -294,11 +294,14 @@ static int launch_stage(const StageArgs &a, cudaStream_t st) {
   static int attr_bytes = -1;  // opt-in set once per instantiation (single-device process)
   const size_t smem = stage_smem(&a.g);
   if (attr_bytes < 0) {
-    const int optin = cdk_max_smem_optin();
-    cudaError_t e = cudaFuncSetAttribute(kuramoto_stage_kernel<MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, kuramoto_stage_kernel<MODE>);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncGetAttributes(stage)");
+    const int dyn_max = cdk_max_smem_optin() - (int)fa.sharedSizeBytes;
+    e = cudaFuncSetAttribute(kuramoto_stage_kernel<MODE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(stage)");
-    attr_bytes = optin;
+    attr_bytes = dyn_max;
   }
   if ((int)smem > attr_bytes) {
     set_error("community state does not fit the shared-memory opt-in limit");
