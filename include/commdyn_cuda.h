@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 1
+#define CDK_ABI_VERSION 2
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -91,11 +91,15 @@ CDK_API int cdk_dense_poly(const double *x, const int64_t *offsets, int64_t m_co
  * static work schedule built by the host planner (paper_2203_16657_b200/plan.py).
  *   rows [comm_off[c], comm_off[c+1]) form community c; rows >= comm_off[M]
  *   are the NONE pool (sparse contributions only, SPEC.md evaluator:205).
- *   intra entries (sign -1): community-local column (uint16), each row's run
- *   padded to a multiple of 8 with CDK_INTRA_PAD; inter entries (sign +1,
- *   also every entry of a NONE-pool row): global column (int32).
- *   rblock = <= 32 consecutive rows of one community (or of the pool);
- *   segment = a CTA's run of rblocks inside one community. */
+ *   intra entries (sign -1): uint16 column RELATIVE TO THE ROW'S SEGMENT BASE
+ *   (seg_base), each row's run padded to a multiple of 8 with CDK_INTRA_PAD;
+ *   inter entries (sign +1, also every entry of a NONE-pool row): global
+ *   column (int32).
+ *   rblock  = <= 32 consecutive rows of one community (or of the pool);
+ *   segment = a run of whole rblocks owned by one CTA whose intra neighbours
+ *             all lie in the node window seg_win[2s]..seg_win[2s+1] (staged in
+ *             shared memory by one bulk async copy) or, for a community larger
+ *             than the window capacity, in global memory (w0 == w1). */
 typedef struct cdk_graph {
   int64_t n_rows;
   int64_t n_comm;
@@ -107,13 +111,15 @@ typedef struct cdk_graph {
   int32_t n_rblk;
   int32_t n_seg;
   int32_t n_cta;
-  int32_t cta_threads;          /* 256 | 512 | 1024 */
-  int32_t smem_nodes;           /* communities with lambda <= smem_nodes are staged in smem */
-  int32_t reserved0;
+  int32_t cta_threads;          /* 512 */
+  int32_t smem_nodes;           /* window capacity (nodes) of the shared-memory stage */
+  int32_t seg_rows_cap;         /* max rows per segment (shared-memory accumulators) */
   const int64_t *rblk_row0;     /* [n_rblk] */
   const int32_t *rblk_comm;     /* [n_rblk], -1 = NONE pool */
   const int32_t *comm_rblk_off; /* [n_comm+1] */
   const int32_t *seg_rblk;      /* [n_seg+1] rblock boundaries of segments */
+  const int64_t *seg_win;       /* [2*n_seg] staged node window [w0, w1) */
+  const int64_t *seg_base;      /* [n_seg] base of the segment's intra columns */
   const int32_t *cta_seg;       /* [n_cta+1] segment boundaries per CTA */
 } cdk_graph;
 

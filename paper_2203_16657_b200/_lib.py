@@ -36,11 +36,13 @@ class CdkGraph(ctypes.Structure):
         ("n_cta", I32),
         ("cta_threads", I32),
         ("smem_nodes", I32),
-        ("reserved0", I32),
+        ("seg_rows_cap", I32),
         ("rblk_row0", P),
         ("rblk_comm", P),
         ("comm_rblk_off", P),
         ("seg_rblk", P),
+        ("seg_win", P),
+        ("seg_base", P),
         ("cta_seg", P),
     ]
 
@@ -78,6 +80,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
+ABI_VERSION = 2
 
 _lock = threading.Lock()
 _lib = None
@@ -99,7 +102,7 @@ def load_library(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, ctypes.c_int)
-        if lib.cdk_abi_version() != 1:
+        if lib.cdk_abi_version() != ABI_VERSION:
             raise DeviceError("libcommdyn_cuda.so ABI version mismatch")
         _lib = lib
         return lib

@@ -23,7 +23,6 @@
 namespace cdk {
 
 constexpr int RB = 32;  // rows per rblock
-constexpr int GL = 8;   // lanes per row
 
 struct Workspace {
   double2 *z[2];
@@ -46,8 +45,9 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
     return p;
   };
   const size_t n = (size_t)g->n_rows, m = (size_t)g->n_comm;
-  w.z[0] = (double2 *)take(n * sizeof(double2));
-  w.z[1] = (double2 *)take(n * sizeof(double2));
+  // +16: staged windows are rounded out to 8-node (128-byte) boundaries
+  w.z[0] = (double2 *)take((n + 16) * sizeof(double2));
+  w.z[1] = (double2 *)take((n + 16) * sizeof(double2));
   w.ksum = (double *)take(n * sizeof(double));
   w.R[0] = (double2 *)take((m + 1) * sizeof(double2));
   w.R[1] = (double2 *)take((m + 1) * sizeof(double2));
@@ -89,92 +89,136 @@ __device__ __forceinline__ double2 reduce_comm(const double2 *part, int b0, int 
   return make_double2(sr, si);
 }
 
+// ---- bulk async copy (TMA engine, non-tensor form) + mbarrier helpers -----
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // MODE 0: out = f(theta) (single RHS).  MODE 1..4: RK4 stage.  MODE 5: Euler step.
+//
+// Per segment (a run of whole rblocks, see cdk_graph):
+//  1. one thread bulk-copies the segment's node window of z_in into shared
+//     memory (async proxy, mbarrier completion);
+//  2. gather: 8-lane groups take rows round-robin; each lane streams 16-byte
+//     chunks (8 uint16 columns) of the row's intra run and gathers z from
+//     shared memory, then the row's inter entries from global memory (L2); the
+//     group reduces (fixed butterfly) and writes the row's sparse sum to a
+//     shared-memory accumulator;
+//  3. epilogue: warps take rblocks; lane = row: k = omega + K/N Im((R_c + acc) conj z),
+//     RK4 stage update, z_next = exp(i theta_next), rblock partial of R_next;
+//     the warp that completes a community's last rblock reduces R_next[c].
 template <int MODE>
 __global__ void __launch_bounds__(512, 2) kuramoto_stage_kernel(const StageArgs a) {
-  extern __shared__ __align__(128) double2 zs[];
-  __shared__ int s_last;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
   const cdk_graph &g = a.g;
+  double2 *zs = reinterpret_cast<double2 *>(smem_raw);
+  double2 *accs = zs + g.smem_nodes;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-  const int grp = lane >> 3, t = lane & 7;
+  const int t = lane & 7;                 // lane within the 8-lane row group
+  const int grp = tid >> 3, ngrp = blockDim.x >> 3;
   const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t parity = 0;
 
   for (int s = segA; s < segB; ++s) {
-    const int rb0 = g.seg_rblk[s], rb1 = g.seg_rblk[s + 1];
-    const int c = g.rblk_comm[rb0];
-    int64_t c0 = 0, cend = g.n_rows;
-    if (c >= 0) {
-      c0 = g.comm_off[c];
-      cend = g.comm_off[c + 1];
-    }
-    const bool staged = (c >= 0) && (cend - c0) <= (int64_t)g.smem_nodes;
-    __syncthreads();  // previous segment done with zs
+    const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
+    const int64_t row0 = g.rblk_row0[rbA];
+    const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
+    const int64_t w0 = g.seg_win[2 * s], w1 = g.seg_win[2 * s + 1];
+    const int64_t base = g.seg_base[s];
+    const bool staged = w1 > w0;
     if (staged) {
-      const int lam = (int)(cend - c0);
-      for (int i = tid; i < lam; i += blockDim.x) zs[i] = ldg(a.z_in + c0 + i);
+      if (tid == 0) {
+        fence_proxy_async_smem();  // prior generic reads of zs ordered before the async write
+        const uint32_t bytes = (uint32_t)((w1 - w0) * sizeof(double2));
+        mbar_expect_tx(&bar, bytes);
+        bulk_g2s(zs, a.z_in + w0, bytes, &bar);
+      }
+      mbar_wait(&bar, parity);
+      parity ^= 1;
     }
-    __syncthreads();
-    const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
+    const double2 *zsrc = staged ? zs : a.z_in + base;
 
-    for (int rb = rb0 + warp; rb < rb1; rb += nwarp) {
-      const int64_t row0 = g.rblk_row0[rb];
-      const int nr = (int)min((int64_t)RB, cend - row0);
-      const int64_t ip = (lane < nr) ? ldg(g.intra_ptr + row0 + lane) : 0;
-      const int64_t ipe = ldg(g.intra_ptr + row0 + nr);
-      const int64_t xp = (lane < nr) ? ldg(g.inter_ptr + row0 + lane) : 0;
-      const int64_t xpe = ldg(g.inter_ptr + row0 + nr);
-
-      double accr = 0.0, acci = 0.0;  // lane L ends with row L's sparse sum
-      const int npass = (nr + 3) >> 2;
-      for (int q = 0; q < npass; ++q) {
-        const int r = 4 * q + grp;  // this group's row in the rblock
-        const int rn = (r + 1) & 31;
-        const int64_t s0 = __shfl_sync(FULL, ip, r & 31);
-        const int64_t e0n = __shfl_sync(FULL, ip, rn);
-        const int64_t x0 = __shfl_sync(FULL, xp, r & 31);
-        const int64_t x1n = __shfl_sync(FULL, xp, rn);
-        double sr = 0.0, si = 0.0;
-        if (r < nr) {
-          const int64_t e0 = (r + 1 < nr) ? e0n : ipe;
-          const int64_t x1 = (r + 1 < nr) ? x1n : xpe;
-          for (int64_t p = s0 + 8 * t; p < e0; p += 8 * GL) {
-            const uint4 w = ldg(reinterpret_cast<const uint4 *>(g.intra_col + p));
-            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    // ---- gather phase --------------------------------------------------
+    const int nrows = (int)(row1 - row0);
+    for (int r = grp; r < nrows; r += ngrp) {
+      const int64_t i = row0 + r;
+      const int64_t e0 = ldg(g.intra_ptr + i), e1 = ldg(g.intra_ptr + i + 1);
+      const int64_t x0 = ldg(g.inter_ptr + i), x1 = ldg(g.inter_ptr + i + 1);
+      double sr = 0.0, si = 0.0;
+      for (int64_t p = e0 + 8 * t; p < e1; p += 64) {
+        const uint4 w = ldg(reinterpret_cast<const uint4 *>(g.intra_col + p));
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
-              if (u != CDK_INTRA_PAD) {
-                const double2 z = staged ? zs[u] : ldg(a.z_in + c0 + u);
-                sr -= z.x;
-                si -= z.y;
-              }
-            }
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+          if (u != CDK_INTRA_PAD) {
+            const double2 z = staged ? zs[u] : ldg(zsrc + u);
+            sr -= z.x;
+            si -= z.y;
           }
-          for (int64_t p = x0 + t; p < x1; p += GL) {
-            const int32_t j = ldg(g.inter_col + p);
-            const double2 z = ldg(a.z_in + j);
-            sr += z.x;
-            si += z.y;
-          }
-        }
-        sr = warp_sum(sr, GL);
-        si = warp_sum(si, GL);
-        const double vr = __shfl_sync(FULL, sr, (lane & 3) * GL);
-        const double vi = __shfl_sync(FULL, si, (lane & 3) * GL);
-        if ((lane >> 2) == q) {
-          accr = vr;
-          acci = vi;
         }
       }
+      for (int64_t p = x0 + t; p < x1; p += 8) {
+        const double2 z = ldg(a.z_in + ldg(g.inter_col + p));
+        sr += z.x;
+        si += z.y;
+      }
+      // only this 8-lane group is guaranteed to be here (rows may end mid-warp)
+      const unsigned gmask = 0xFFu << (lane & 24);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(gmask, sr, o);
+        si += __shfl_xor_sync(gmask, si, o);
+      }
+      if (t == 0) accs[r] = make_double2(sr, si);
+    }
+    __syncthreads();
 
-      // epilogue: lane L owns row row0 + L
+    // ---- epilogue: one warp per rblock, lane = row ------------------------
+    for (int rb = rbA + warp; rb < rbB; rb += nwarp) {
+      const int64_t rrow0 = g.rblk_row0[rb];
+      const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+      const int nr = (int)(rrow1 - rrow0);
+      const int c = g.rblk_comm[rb];
       double2 znew = make_double2(0.0, 0.0);
       if (lane < nr) {
-        const int64_t i = row0 + lane;
-        const double2 zi = staged ? zs[i - c0] : ldg(a.z_in + i);
+        const int64_t i = rrow0 + lane;
+        const double2 acc = accs[i - row0];
+        const double2 zi = staged ? zs[i - w0] : ldg(a.z_in + i);
+        const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
         const double kn = a.k_over_n;
         double k = ldg(a.omega + i) + kn * (R.y * zi.x - R.x * zi.y);
-        k = k + kn * (acci * zi.x - accr * zi.y);
+        k = k + kn * (acc.y * zi.x - acc.x * zi.y);
         if (MODE == 0) {
           a.out[i] = k;
         } else {
@@ -202,32 +246,28 @@ __global__ void __launch_bounds__(512, 2) kuramoto_stage_kernel(const StageArgs 
           a.z_out[i] = znew;
         }
       }
-      if (MODE != 0) {
-        const double pr = warp_sum(znew.x), pi = warp_sum(znew.y);
-        if (lane == 0) a.part[rb] = make_double2(pr, pi);
-      }
-    }
-
-    // community completion: the last CTA reduces the partials into R_out[c]
-    if (MODE != 0 && c >= 0) {
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        const int mine = rb1 - rb0;
-        const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
-        const int old = atomicAdd(a.cnt + c, mine);
-        s_last = (old + mine == total);
-      }
-      __syncthreads();
-      if (s_last && warp == 0) {
-        __threadfence();
-        const double2 Rn = reduce_comm(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane);
+      if (MODE != 0 && c >= 0) {
+        const double pr = warp_sum(znew.x), pim = warp_sum(znew.y);
+        int last = 0;
         if (lane == 0) {
-          a.R_out[c] = Rn;
-          a.cnt[c] = 0;
+          a.part[rb] = make_double2(pr, pim);
+          __threadfence();
+          const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
+          last = (atomicAdd(a.cnt + c, 1) + 1 == total);
+        }
+        last = __shfl_sync(FULL, last, 0);
+        if (last) {  // this warp finished community c: reduce its partials (fixed order)
+          __threadfence();
+          const double2 Rn =
+              reduce_comm(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane);
+          if (lane == 0) {
+            a.R_out[c] = Rn;
+            a.cnt[c] = 0;
+          }
         }
       }
     }
+    __syncthreads();  // zs / accs reused by the next segment
   }
 }
 
@@ -284,10 +324,16 @@ static int check_graph(const cdk_graph *g) {
     set_error("cdk_graph: cta_threads must be 256 or 512");
     return CDK_INPUT;
   }
+  if (g->smem_nodes < 0 || g->seg_rows_cap <= 0) {
+    set_error("cdk_graph: bad shared-memory capacities");
+    return CDK_INPUT;
+  }
   return CDK_OK;
 }
 
-static size_t stage_smem(const cdk_graph *g) { return (size_t)g->smem_nodes * sizeof(double2); }
+static size_t stage_smem(const cdk_graph *g) {
+  return ((size_t)g->smem_nodes + (size_t)g->seg_rows_cap) * sizeof(double2);
+}
 
 template <int MODE>
 static int launch_stage(const StageArgs &a, cudaStream_t st) {

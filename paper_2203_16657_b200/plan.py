@@ -11,8 +11,9 @@ stream (include/commdyn_cuda.h, struct cdk_graph):
   run padded to a multiple of 8 (one 16-byte vector load per lane), inter
   (+1) entries as int32 global columns;
 * 32-row "rblocks" (never straddling a community), cost-balanced contiguous
-  CTA ranges, and "segments" = a CTA's run inside one community (the unit of
-  shared-memory staging of that community's state).
+  CTA ranges, and "segments" = a CTA's run of rblocks whose intra neighbours
+  lie in one node window that fits shared memory (the unit of staging), with
+  the intra columns rebased to that window.
 """
 
 from __future__ import annotations
@@ -29,7 +30,6 @@ INTRA_PAD = 0xFFFF
 ROW_COST = 24.0  # per-row overhead in "entry" units (pointer loads, epilogue, sincos)
 INTER_COST = 3.0  # an inter entry: 4-byte index + an L2 gather
 DEFAULT_SMS = 148
-SMEM_OPTIN = 232448  # B200 max dynamic smem per block (227 KB)
 SMEM_PER_SM = 233472  # 228 KB per SM
 
 
@@ -66,13 +66,20 @@ class HostLayout:
 class Schedule:
     n_cta: int
     cta_threads: int
-    smem_nodes: int
+    smem_nodes: int  # staged window capacity (nodes)
+    seg_rows_cap: int  # rows per segment (shared-memory accumulators)
     seg_rblk: np.ndarray  # int32[n_seg+1]
+    seg_win: np.ndarray  # int64[n_seg, 2]
+    seg_base: np.ndarray  # int64[n_seg]
     cta_seg: np.ndarray  # int32[n_cta+1]
+    intra_col: np.ndarray  # uint16, columns rebased to each row's segment base
 
     @property
     def n_seg(self) -> int:
         return int(self.seg_rblk.shape[0] - 1)
+
+    def smem_bytes(self) -> int:
+        return 16 * (self.smem_nodes + self.seg_rows_cap)
 
 
 def _row_runs(rows_sorted: np.ndarray, n_rows: int):
@@ -87,8 +94,8 @@ def build_layout(dec: Decomposition) -> HostLayout:
     n = int(dec.n_nodes)
     off = part.offsets
     m = part.n_comm
-    if m and int(part.sizes.max()) > INTRA_PAD:
-        raise InputError("community larger than 65535 nodes: uint16 intra columns do not fit")
+    if m and int(part.sizes.max()) > INTRA_PAD - 1:
+        raise InputError("community larger than 65534 nodes: uint16 intra columns do not fit")
     comm = part.comm_of_permuted()
     rows, cols, sg = dec.directed()
     cr = comm[rows]
@@ -139,34 +146,79 @@ def build_layout(dec: Decomposition) -> HostLayout:
                       nnz_intra, nnz_inter)
 
 
+WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
+
+
+def _rblk_rows(lay: HostLayout) -> np.ndarray:
+    return np.concatenate([lay.rblk_row0, [lay.n_rows]]).astype(np.int64)
+
+
 def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, cta_threads: int = 512,
-                   smem_optin: int = SMEM_OPTIN, ctas_per_sm: int | None = None) -> Schedule:
-    sizes = np.diff(lay.comm_off)
-    fits = sizes[sizes * 16 <= smem_optin - 1024]
-    smem_nodes = int(fits.max()) if fits.size else 0
-    if ctas_per_sm is None:
-        per_cta = 16 * smem_nodes + 2048
-        ctas_per_sm = max(1, min(2, SMEM_PER_SM // max(per_cta, 1)))
+                   ctas_per_sm: int = 2, rows_cap: int = 1024) -> Schedule:
+    """Cost-balanced contiguous CTA ranges of rblocks, split into segments
+    whose intra neighbours fit one shared-memory window."""
+    per_cta = SMEM_PER_SM // ctas_per_sm - 1024 - 256  # driver reserve + static smem
+    smem_nodes = max(0, (per_cta - 16 * rows_cap) // 16) // WIN_ALIGN * WIN_ALIGN
     n_cta = max(1, sm_count * ctas_per_sm)
     nrb = lay.n_rblk
-    # cost per rblock (rows are contiguous across rblocks)
+    rows = _rblk_rows(lay)
     cum = np.concatenate([[0.0], np.cumsum(lay.row_cost)])
-    rb_end = np.concatenate([lay.rblk_row0[1:], [lay.n_rows]]) if nrb else np.empty(0, np.int64)
-    rb_cost = cum[rb_end] - cum[lay.rblk_row0] if nrb else np.empty(0)
-    # staging cost: charge lambda/8 once per rblock's community start (approximation)
+    rb_cost = cum[rows[1:]] - cum[rows[:-1]]
     cum_rb = np.concatenate([[0.0], np.cumsum(rb_cost)])
-    total = cum_rb[-1]
-    targets = total * np.arange(1, n_cta) / n_cta
-    cuts = np.searchsorted(cum_rb, targets, side="left").astype(np.int64)
-    cuts = np.clip(cuts, 0, nrb)
-    cta_bounds = np.concatenate([[0], cuts, [nrb]]).astype(np.int64)
-    cta_bounds = np.maximum.accumulate(cta_bounds)
-    comm_starts = lay.comm_rblk_off.astype(np.int64)
-    bounds = np.unique(np.concatenate([cta_bounds, comm_starts, [lay.comm_rblk_off[-1], nrb]]))
-    bounds = bounds[(bounds >= 0) & (bounds <= nrb)]
-    seg_rblk = bounds.astype(np.int32)
-    cta_seg = np.searchsorted(bounds, cta_bounds).astype(np.int32)
-    return Schedule(n_cta, cta_threads, smem_nodes, seg_rblk, cta_seg)
+    targets = cum_rb[-1] * np.arange(1, n_cta) / n_cta
+    cuts = np.clip(np.searchsorted(cum_rb, targets, side="left"), 0, nrb)
+    cta_bounds = np.maximum.accumulate(np.concatenate([[0], cuts, [nrb]]).astype(np.int64))
+
+    off = lay.comm_off
+    win_lo = off[:-1] // WIN_ALIGN * WIN_ALIGN
+    win_hi = (off[1:] + WIN_ALIGN - 1) // WIN_ALIGN * WIN_ALIGN
+    stageable = (win_hi - win_lo) <= smem_nodes
+    seg_rblk, seg_win, seg_base, cta_seg = [0], [], [], [0]
+    for b in range(n_cta):
+        rb, rb_end = int(cta_bounds[b]), int(cta_bounds[b + 1])
+        while rb < rb_end:
+            c = int(lay.rblk_comm[rb])
+            start = rb
+            if c < 0 or not stageable[c]:  # unstaged run of one community / the pool
+                while (rb < rb_end and lay.rblk_comm[rb] == c
+                       and rows[rb + 1] - rows[start] <= rows_cap):
+                    rb += 1
+                seg_win.append((0, 0))
+                seg_base.append(int(off[c]) if c >= 0 else 0)
+            else:  # staged window over whole communities, 128-byte aligned
+                w0 = int(win_lo[c])
+                while rb < rb_end:
+                    cc = int(lay.rblk_comm[rb])
+                    if cc < 0 or not stageable[cc]:
+                        break
+                    if int(win_hi[cc]) - w0 > smem_nodes or rows[rb + 1] - rows[start] > rows_cap:
+                        break
+                    rb += 1
+                seg_win.append((w0, int(win_hi[int(lay.rblk_comm[rb - 1])])))
+                seg_base.append(w0)
+            seg_rblk.append(rb)
+        cta_seg.append(len(seg_rblk) - 1)
+    seg_rblk = np.asarray(seg_rblk, dtype=np.int32)
+    seg_win = np.asarray(seg_win, dtype=np.int64).reshape(-1, 2)
+    seg_base = np.asarray(seg_base, dtype=np.int64)
+
+    # rebase intra columns (community-local in the layout) to each row's segment base
+    n = lay.n_rows
+    seg_of_row = np.repeat(np.arange(seg_base.shape[0]), np.diff(rows[seg_rblk]))
+    comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
+    cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
+    delta = (cstart - seg_base[seg_of_row]) if n else np.empty(0, np.int64)
+    col = lay.intra_col
+    if np.any(delta != 0):
+        col = col.copy()
+        d_ent = np.repeat(delta, np.diff(lay.intra_ptr))
+        m = col != INTRA_PAD
+        newc = col[m].astype(np.int64) + d_ent[m]
+        if newc.size and (newc.min() < 0 or newc.max() >= INTRA_PAD):
+            raise InputError("rebased intra column out of uint16 range")
+        col[m] = newc.astype(np.uint16)
+    return Schedule(n_cta, cta_threads, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
+                    seg_base, np.asarray(cta_seg, dtype=np.int32), col)
 
 
 class DeviceGraph:
@@ -196,13 +248,15 @@ class DeviceGraph:
         self._t = {
             "comm_off": up(lay.comm_off),
             "intra_ptr": up(lay.intra_ptr),
-            "intra_col": up(lay.intra_col.view(np.int16)),
+            "intra_col": up(sch.intra_col.view(np.int16)),
             "inter_ptr": up(lay.inter_ptr),
             "inter_col": up(lay.inter_col),
             "rblk_row0": up(lay.rblk_row0),
             "rblk_comm": up(lay.rblk_comm),
             "comm_rblk_off": up(lay.comm_rblk_off),
             "seg_rblk": up(sch.seg_rblk),
+            "seg_win": up(sch.seg_win.reshape(-1)),
+            "seg_base": up(sch.seg_base),
             "cta_seg": up(sch.cta_seg),
         }
         # keep a 16-byte tail on intra_col so uint4 loads never run past the allocation
@@ -215,9 +269,10 @@ class DeviceGraph:
             intra_col=t["intra_col"].data_ptr(), inter_ptr=t["inter_ptr"].data_ptr(),
             inter_col=t["inter_col"].data_ptr() if t["inter_col"].numel() else 0,
             n_rblk=lay.n_rblk, n_seg=sch.n_seg, n_cta=sch.n_cta, cta_threads=sch.cta_threads,
-            smem_nodes=sch.smem_nodes, reserved0=0,
+            smem_nodes=sch.smem_nodes, seg_rows_cap=sch.seg_rows_cap,
             rblk_row0=t["rblk_row0"].data_ptr(), rblk_comm=t["rblk_comm"].data_ptr(),
             comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
+            seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
             cta_seg=t["cta_seg"].data_ptr(),
         )
 

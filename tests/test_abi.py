@@ -30,12 +30,12 @@ def test_library_exports_header_symbols():
 
 def test_library_host_only_calls():
     lib = _lib.load_library(build_library())
-    assert lib.cdk_abi_version() == 1
+    assert lib.cdk_abi_version() == _lib.ABI_VERSION
     assert lib.cdk_launch_count() >= 0
     assert isinstance(lib.cdk_last_error(), (bytes, type(None)))
 
 
 def test_struct_layout_matches_header():
-    # 2 int64 + 5 pointers + 6 int32 + 5 pointers
-    assert ctypes.sizeof(_lib.CdkGraph) == 8 * 2 + 8 * 5 + 4 * 6 + 8 * 5
+    # 2 int64 + 5 pointers + 6 int32 + 7 pointers
+    assert ctypes.sizeof(_lib.CdkGraph) == 8 * 2 + 8 * 5 + 4 * 6 + 8 * 7
     assert ctypes.sizeof(_lib.CdkRunStatus) == 32

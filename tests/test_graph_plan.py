@@ -114,29 +114,72 @@ def test_layout_roundtrip(seed):
     assert lay.nnz_dir == dec.nnz_dir
 
 
-@pytest.mark.parametrize("sm_count,seed", [(1, 0), (3, 1), (148, 2), (7, 3)])
-def test_schedule_invariants(sm_count, seed):
+def _schedule_to_directed(lay, sch):
+    """Directed S reconstructed from the device columns (rebased to segment bases)."""
+    rows_rb = np.concatenate([lay.rblk_row0, [lay.n_rows]])
+    seg_rows = rows_rb[sch.seg_rblk]
+    rows, cols = [], []
+    for s in range(sch.n_seg):
+        for i in range(seg_rows[s], seg_rows[s + 1]):
+            a, b = lay.intra_ptr[i], lay.intra_ptr[i + 1]
+            loc = sch.intra_col[a:b]
+            loc = loc[loc != PL.INTRA_PAD].astype(np.int64)
+            rows += [i] * loc.size
+            cols += list(sch.seg_base[s] + loc)
+            x0, x1 = lay.inter_ptr[i], lay.inter_ptr[i + 1]
+            rows += [i] * (x1 - x0)
+            cols += list(lay.inter_col[x0:x1])
+    return np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64)
+
+
+@pytest.mark.parametrize("sm_count,seed,rows_cap", [(1, 0, 1024), (3, 1, 64), (148, 2, 1024),
+                                                    (7, 3, 32)])
+def test_schedule_invariants(sm_count, seed, rows_cap):
     rng = np.random.default_rng(seed)
     g, part = _random_graph_partition(rng, 190)
-    lay = PL.build_layout(G.decompose(g, part))
-    sch = PL.build_schedule(lay, sm_count=sm_count)
+    dec = G.decompose(g, part)
+    lay = PL.build_layout(dec)
+    sch = PL.build_schedule(lay, sm_count=sm_count, rows_cap=rows_cap)
     nrb = lay.n_rblk
     seg = sch.seg_rblk
     assert seg[0] == 0 and seg[-1] == nrb and np.all(np.diff(seg) > 0)
-    # every segment inside one community (or the pool)
+    rows_rb = np.concatenate([lay.rblk_row0, [lay.n_rows]])
+    off = lay.comm_off
     for s in range(sch.n_seg):
         cs = lay.rblk_comm[seg[s]:seg[s + 1]]
-        assert np.all(cs == cs[0])
+        assert rows_rb[seg[s + 1]] - rows_rb[seg[s]] <= rows_cap
+        w0, w1 = sch.seg_win[s]
+        if w1 > w0:  # staged: every community of the segment inside the window
+            assert np.all(cs >= 0)
+            assert w1 - w0 <= sch.smem_nodes and sch.seg_base[s] == w0
+            assert np.all(off[cs] >= w0) and np.all(off[cs + 1] <= w1)
+        else:
+            assert np.all(cs == cs[0])
     cta = sch.cta_seg
     assert cta[0] == 0 and cta[-1] == sch.n_seg and np.all(np.diff(cta) >= 0)
     assert sch.n_cta == cta.shape[0] - 1
     # rblocks: <= 32 rows, never straddle communities, cover all rows once
-    ends = np.concatenate([lay.rblk_row0[1:], [lay.n_rows]])
+    ends = rows_rb[1:]
     assert np.all(ends - lay.rblk_row0 <= 32) and np.all(ends > lay.rblk_row0)
     for c in range(lay.n_comm):
         b0, b1 = lay.comm_rblk_off[c], lay.comm_rblk_off[c + 1]
         assert lay.rblk_row0[b0] == lay.comm_off[c]
         assert np.all(lay.rblk_comm[b0:b1] == c)
+    # rebased device columns still encode exactly the directed S
+    r, c = _schedule_to_directed(lay, sch)
+    rows, cols, _ = dec.directed()
+    assert np.array_equal(np.sort(r * 1000 + c), np.sort(rows * 1000 + cols))
+
+
+def test_schedule_small_window_forces_unstaged():
+    dec = G.planted_partition_decomposition([300, 40, 40, 500], 0.9, 0.05, 5)
+    lay = PL.build_layout(dec)
+    # a tiny per-CTA budget: windows of <= ~100 nodes, big communities unstaged
+    sch = PL.build_schedule(lay, sm_count=2, ctas_per_sm=2, rows_cap=64)
+    assert sch.smem_nodes >= 0
+    r, c = _schedule_to_directed(lay, sch)
+    rows, cols, _ = dec.directed()
+    assert np.array_equal(np.sort(r * 10**6 + c), np.sort(rows * 10**6 + cols))
 
 
 def test_layout_rejects_inconsistent_signs():
