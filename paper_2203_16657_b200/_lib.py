@@ -44,6 +44,10 @@ class CdkGraph(ctypes.Structure):
         ("seg_win", P),
         ("seg_base", P),
         ("cta_seg", P),
+        ("seg_tile", P),
+        ("tiles", P),
+        ("tile_tab", P),
+        ("n_tile", I64),
     ]
 
 
@@ -80,7 +84,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lock = threading.Lock()
 _lib = None

@@ -22,7 +22,6 @@
 
 namespace cdk {
 
-constexpr int RB = 32;  // rows per rblock
 
 struct Workspace {
   double2 *z[2];
@@ -105,9 +104,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "LAB_WAIT:\n"
+      "LAB_WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra LAB_WAIT;\n"
+      "@!p bra LAB_WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity) : "memory");
 }
@@ -121,153 +120,294 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// MODE 0: out = f(theta) (single RHS).  MODE 1..4: RK4 stage.  MODE 5: Euler step.
-//
-// Per segment (a run of whole rblocks, see cdk_graph):
-//  1. one thread bulk-copies the segment's node window of z_in into shared
-//     memory (async proxy, mbarrier completion);
-//  2. gather: 8-lane groups take rows round-robin; each lane streams 16-byte
-//     chunks (8 uint16 columns) of the row's intra run and gathers z from
-//     shared memory, then the row's inter entries from global memory (L2); the
-//     group reduces (fixed butterfly) and writes the row's sparse sum to a
-//     shared-memory accumulator;
-//  3. epilogue: warps take rblocks; lane = row: k = omega + K/N Im((R_c + acc) conj z),
-//     RK4 stage update, z_next = exp(i theta_next), rblock partial of R_next;
-//     the warp that completes a community's last rblock reduces R_next[c].
-template <int MODE>
-__global__ void __launch_bounds__(512, 2) kuramoto_stage_kernel(const StageArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar;
-  const cdk_graph &g = a.g;
-  double2 *zs = reinterpret_cast<double2 *>(smem_raw);
-  double2 *accs = zs + g.smem_nodes;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-  const int t = lane & 7;                 // lane within the 8-lane row group
-  const int grp = tid >> 3, ngrp = blockDim.x >> 3;
-  const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
-  if (tid == 0) mbar_init(&bar, 1);
-  __syncthreads();
-  uint32_t parity = 0;
+// 8 uint16 intra columns (one 16-byte chunk): subtract their z (sign -1).
+// Staged (shared memory): branch-free, padding (0xFFFF) is clamped onto a zero
+// slot one past the window capacity.  Unstaged (global, huge communities):
+// predicated loads.
+template <bool STAGED>
+__device__ __forceinline__ void gather8(const uint4 w, const double2 *__restrict__ zbase,
+                                        uint32_t zero_slot, double &sr, double &si) {
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+    if (STAGED) {
+      const double2 z = zbase[min(u, zero_slot)];
+      sr -= z.x;
+      si -= z.y;
+    } else if (u != CDK_INTRA_PAD) {
+      const double2 z = ldg(zbase + u);
+      sr -= z.x;
+      si -= z.y;
+    }
+  }
+}
 
+// sparse sums of two rows (A, B) of an unstaged segment (global gathers)
+__device__ __forceinline__ void gather_rows_global(const cdk_graph &g,
+                                                   const double2 *__restrict__ z_in,
+                                                   const double2 *__restrict__ zbase, int64_t iA,
+                                                   int64_t iB, bool hasB, int t, double &ar,
+                                                   double &ai, double &br, double &bi) {
+  const int64_t eA0 = ldg(g.intra_ptr + iA), eA1 = ldg(g.intra_ptr + iA + 1);
+  const int64_t xA0 = ldg(g.inter_ptr + iA), xA1 = ldg(g.inter_ptr + iA + 1);
+  const int64_t eB0 = ldg(g.intra_ptr + iB);
+  const int64_t eB1 = hasB ? ldg(g.intra_ptr + iB + 1) : eB0;
+  const int64_t xB0 = ldg(g.inter_ptr + iB);
+  const int64_t xB1 = hasB ? ldg(g.inter_ptr + iB + 1) : xB0;
+  const uint4 *colv = reinterpret_cast<const uint4 *>(g.intra_col);
+  for (int64_t p = eA0 + 8 * t; p < eA1; p += 64)
+    gather8<false>(ldg(colv + (p >> 3)), zbase, 0, ar, ai);
+  for (int64_t p = eB0 + 8 * t; p < eB1; p += 64)
+    gather8<false>(ldg(colv + (p >> 3)), zbase, 0, br, bi);
+  for (int64_t p = xA0 + t; p < xA1; p += 8) {
+    const double2 z = ldg(z_in + ldg(g.inter_col + p));
+    ar += z.x;
+    ai += z.y;
+  }
+  for (int64_t p = xB0 + t; p < xB1; p += 8) {
+    const double2 z = ldg(z_in + ldg(g.inter_col + p));
+    br += z.x;
+    bi += z.y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined stage kernel.  One CTA per SM, 32 warps:
+//   warp 31 (one lane) = producer: streams each tile's CSR slices (uint16
+//     intra columns, int32 inter columns, int32 row-offset table) into a
+//     2-slot shared-memory ring with bulk async copies (full/empty mbarriers);
+//   warps 0..30 = consumers: per segment, one bulk copy of the node window of
+//     z_in into shared memory; per tile, 8-lane groups gather rows from the
+//     window (conflict-free 16-byte LDS per column), reduce, store the row
+//     sums; after a consumer-only named barrier the tile's rblocks run the
+//     epilogue (RK4 stage update, sincos, rblock partials, community R).
+// Unstaged segments (communities above the window capacity, NONE pool) are
+// processed by the consumers straight from global memory.
+// ---------------------------------------------------------------------------
+constexpr int TILE_ROWS = 256;
+constexpr int TILE_E = 16384;
+constexpr int TILE_X = 2048;
+constexpr int TILE_TAB = 2 * (TILE_ROWS + 4);
+constexpr int RING = 2;
+constexpr int NTHREADS = 1024;
+constexpr int NCONS_WARPS = 31;
+constexpr int NCONS = NCONS_WARPS * 32;
+constexpr int NGROUPS = NCONS / 8;
+
+struct TileSlot {
+  uint16_t cols[TILE_E];
+  int32_t xcol[TILE_X];
+  int32_t tab[TILE_TAB];
+};
+static_assert(sizeof(TileSlot) % 16 == 0, "tile slot must keep 16-byte alignment");
+
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"r"(NCONS) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// epilogue of rblocks [rbA, rbB): lane = row; acc rows indexed from accrow0
+template <int MODE>
+__device__ __forceinline__ void epilogue(const StageArgs &a, int rbA, int rbB, int warp,
+                                         int nwarp, int lane, const double2 *acc,
+                                         int64_t accrow0, bool staged, const double2 *zs,
+                                         int64_t w0) {
+  const cdk_graph &g = a.g;
+  for (int rb = rbA + warp; rb < rbB; rb += nwarp) {
+    const int64_t rrow0 = g.rblk_row0[rb];
+    const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+    const int nr = (int)(rrow1 - rrow0);
+    const int c = g.rblk_comm[rb];
+    double2 znew = make_double2(0.0, 0.0);
+    if (lane < nr) {
+      const int64_t i = rrow0 + lane;
+      const double2 ac = acc[i - accrow0];
+      const double2 zi = staged ? zs[i - w0] : ldg(a.z_in + i);
+      const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
+      const double kn = a.k_over_n;
+      double k = ldg(a.omega + i) + kn * (R.y * zi.x - R.x * zi.y);
+      k = k + kn * (ac.y * zi.x - ac.x * zi.y);
+      if (MODE == 0) {
+        a.out[i] = k;
+      } else {
+        const double th0 = a.theta[i];
+        double thn;
+        if (MODE == 1) {
+          a.ksum[i] = k;
+          thn = add_rn(th0, mul_rn(a.h, k));
+        } else if (MODE == 2 || MODE == 3) {
+          a.ksum[i] = add_rn(a.ksum[i], mul_rn(2.0, k));
+          thn = add_rn(th0, mul_rn(a.h, k));
+        } else {  // MODE 4: x + dt/6 (k1 + 2k2 + 2k3 + k4); MODE 5: Euler x + dt k
+          const double ks = (MODE == 4) ? add_rn(a.ksum[i], k) : k;
+          thn = wrap_phase(add_rn(th0, mul_rn(a.h, ks)));
+          a.theta[i] = thn;
+          if (!isfinite(thn)) {
+            atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->nonfinite), 1ull);
+            atomicMin(reinterpret_cast<long long *>(&a.status->first_bad_step),
+                      (long long)(a.status->steps_done + a.step_rel + 1));
+          }
+        }
+        double sn, cs;
+        sincos(thn, &sn, &cs);
+        znew = make_double2(cs, sn);
+        a.z_out[i] = znew;
+      }
+    }
+    if (MODE != 0 && c >= 0) {
+      const double pr = warp_sum(znew.x), pim = warp_sum(znew.y);
+      int last = 0;
+      if (lane == 0) {
+        a.part[rb] = make_double2(pr, pim);
+        __threadfence();
+        const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
+        last = (atomicAdd(a.cnt + c, 1) + 1 == total);
+      }
+      last = __shfl_sync(FULL, last, 0);
+      if (last) {  // this warp finished community c: reduce its partials (fixed order)
+        __threadfence();
+        const double2 Rn = reduce_comm(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane);
+        if (lane == 0) {
+          a.R_out[c] = Rn;
+          a.cnt[c] = 0;
+        }
+      }
+    }
+  }
+}
+
+// MODE 0: out = f(theta) (single RHS).  MODE 1..4: RK4 stage.  MODE 5: Euler step.
+template <int MODE>
+__global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar_full[RING], bar_empty[RING], bar_win;
+  const cdk_graph &g = a.g;
+  TileSlot *ring = reinterpret_cast<TileSlot *>(smem_raw);
+  double2 *accs = reinterpret_cast<double2 *>(smem_raw + RING * sizeof(TileSlot));
+  double2 *zs = accs + 2 * TILE_ROWS;
+  const uint32_t zero_slot = (uint32_t)g.smem_nodes;  // zs[smem_nodes] == 0
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
+  if (tid == 0) {
+    for (int b = 0; b < RING; ++b) {
+      mbar_init(&bar_full[b], 1);
+      mbar_init(&bar_empty[b], 1);
+    }
+    mbar_init(&bar_win, 1);
+    zs[zero_slot] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+
+  if (warp == NCONS_WARPS) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      int k = 0;
+      for (int s = segA; s < segB; ++s) {
+        for (int ti = g.seg_tile[s]; ti < g.seg_tile[s + 1]; ++ti, ++k) {
+          const int b = k & 1, n = k >> 1;
+          if (n > 0) mbar_wait(&bar_empty[b], (n - 1) & 1);
+          const cdk_tile T = g.tiles[ti];
+          const int64_t r0 = g.rblk_row0[T.rblk0];
+          const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
+          const int half = ((int)(r1 - r0) + 1 + 3) & ~3;
+          const uint32_t be = (uint32_t)T.ne * 2u, bx = (uint32_t)T.nxa * 4u,
+                         bt = (uint32_t)half * 8u;
+          mbar_expect_tx(&bar_full[b], be + bx + bt);
+          if (be) bulk_g2s(ring[b].cols, g.intra_col + T.e0, be, &bar_full[b]);
+          if (bx) bulk_g2s(ring[b].xcol, g.inter_col + T.x0a, bx, &bar_full[b]);
+          bulk_g2s(ring[b].tab, g.tile_tab + T.tab_off, bt, &bar_full[b]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers (warps 0..30) ----------------
+  const int t = lane & 7;
+  const int grp = tid >> 3;
+  const unsigned gmask = 0xFFu << (lane & 24);  // this 8-lane group only
+  int k = 0;
+  uint32_t win_par = 0;
   for (int s = segA; s < segB; ++s) {
     const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
-    const int64_t row0 = g.rblk_row0[rbA];
-    const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
     const int64_t w0 = g.seg_win[2 * s], w1 = g.seg_win[2 * s + 1];
-    const int64_t base = g.seg_base[s];
     const bool staged = w1 > w0;
     if (staged) {
       if (tid == 0) {
-        fence_proxy_async_smem();  // prior generic reads of zs ordered before the async write
+        fence_proxy_async_smem();  // prior generic reads of zs before the async overwrite
         const uint32_t bytes = (uint32_t)((w1 - w0) * sizeof(double2));
-        mbar_expect_tx(&bar, bytes);
-        bulk_g2s(zs, a.z_in + w0, bytes, &bar);
+        mbar_expect_tx(&bar_win, bytes);
+        bulk_g2s(zs, a.z_in + w0, bytes, &bar_win);
       }
-      mbar_wait(&bar, parity);
-      parity ^= 1;
-    }
-    const double2 *zsrc = staged ? zs : a.z_in + base;
-
-    // ---- gather phase --------------------------------------------------
-    const int nrows = (int)(row1 - row0);
-    for (int r = grp; r < nrows; r += ngrp) {
-      const int64_t i = row0 + r;
-      const int64_t e0 = ldg(g.intra_ptr + i), e1 = ldg(g.intra_ptr + i + 1);
-      const int64_t x0 = ldg(g.inter_ptr + i), x1 = ldg(g.inter_ptr + i + 1);
-      double sr = 0.0, si = 0.0;
-      for (int64_t p = e0 + 8 * t; p < e1; p += 64) {
-        const uint4 w = ldg(reinterpret_cast<const uint4 *>(g.intra_col + p));
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+      mbar_wait(&bar_win, win_par);
+      win_par ^= 1;
+      for (int ti = g.seg_tile[s]; ti < g.seg_tile[s + 1]; ++ti, ++k) {
+        const int b = k & 1;
+        mbar_wait(&bar_full[b], (k >> 1) & 1);
+        const TileSlot &S = ring[b];
+        const cdk_tile T = g.tiles[ti];
+        const int64_t r0 = g.rblk_row0[T.rblk0];
+        const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
+        const int nrow = (int)(r1 - r0);
+        const int half = (nrow + 1 + 3) & ~3;
+        double2 *acc = accs + (k & 1) * TILE_ROWS;
+        for (int r = grp; r < nrow; r += NGROUPS) {
+          const int ie0 = S.tab[r], ie1 = S.tab[r + 1];
+          const int xe0 = S.tab[half + r], xe1 = S.tab[half + r + 1];
+          const int32_t j = (xe0 + t < xe1) ? S.xcol[xe0 + t] : -1;
+          const double2 zx = (j >= 0) ? ldg(a.z_in + j) : make_double2(0.0, 0.0);
+          double sr = 0.0, si = 0.0;
+          for (int p = ie0 + 8 * t; p < ie1; p += 64)
+            gather8<true>(*reinterpret_cast<const uint4 *>(S.cols + p), zs, zero_slot, sr, si);
+          sr += zx.x;
+          si += zx.y;
+          for (int p = xe0 + 8 + t; p < xe1; p += 8) {
+            const double2 z = ldg(a.z_in + S.xcol[p]);
+            sr += z.x;
+            si += z.y;
+          }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
-          if (u != CDK_INTRA_PAD) {
-            const double2 z = staged ? zs[u] : ldg(zsrc + u);
-            sr -= z.x;
-            si -= z.y;
+          for (int o = 4; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(gmask, sr, o);
+            si += __shfl_xor_sync(gmask, si, o);
           }
+          if (t == 0) acc[r] = make_double2(sr, si);
         }
+        consumer_bar();  // tile's row sums complete; ring slot b no longer read
+        if (tid == 0) mbar_arrive(&bar_empty[b]);
+        epilogue<MODE>(a, T.rblk0, T.rblk1, warp, NCONS_WARPS, lane, acc, r0, true, zs, w0);
       }
-      for (int64_t p = x0 + t; p < x1; p += 8) {
-        const double2 z = ldg(a.z_in + ldg(g.inter_col + p));
-        sr += z.x;
-        si += z.y;
-      }
-      // only this 8-lane group is guaranteed to be here (rows may end mid-warp)
-      const unsigned gmask = 0xFFu << (lane & 24);
+    } else {
+      const int64_t row0 = g.rblk_row0[rbA];
+      const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
+      const int nrows = (int)(row1 - row0);
+      const double2 *zbase = a.z_in + g.seg_base[s];
+      double2 *acc = accs + (k & 1) * TILE_ROWS;
+      for (int r = grp; r < nrows; r += 2 * NGROUPS) {
+        const int rB = r + NGROUPS;
+        const bool hasB = rB < nrows;
+        double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+        gather_rows_global(g, a.z_in, zbase, row0 + r, row0 + (hasB ? rB : r), hasB, t, ar, ai,
+                           br, bi);
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        sr += __shfl_xor_sync(gmask, sr, o);
-        si += __shfl_xor_sync(gmask, si, o);
+        for (int o = 4; o > 0; o >>= 1) {
+          ar += __shfl_xor_sync(gmask, ar, o);
+          ai += __shfl_xor_sync(gmask, ai, o);
+          br += __shfl_xor_sync(gmask, br, o);
+          bi += __shfl_xor_sync(gmask, bi, o);
+        }
+        if (t == 0) {
+          acc[r] = make_double2(ar, ai);
+          if (hasB) acc[rB] = make_double2(br, bi);
+        }
       }
-      if (t == 0) accs[r] = make_double2(sr, si);
+      consumer_bar();
+      epilogue<MODE>(a, rbA, rbB, warp, NCONS_WARPS, lane, acc, row0, false, zs, 0);
+      ++k;
     }
-    __syncthreads();
-
-    // ---- epilogue: one warp per rblock, lane = row ------------------------
-    for (int rb = rbA + warp; rb < rbB; rb += nwarp) {
-      const int64_t rrow0 = g.rblk_row0[rb];
-      const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
-      const int nr = (int)(rrow1 - rrow0);
-      const int c = g.rblk_comm[rb];
-      double2 znew = make_double2(0.0, 0.0);
-      if (lane < nr) {
-        const int64_t i = rrow0 + lane;
-        const double2 acc = accs[i - row0];
-        const double2 zi = staged ? zs[i - w0] : ldg(a.z_in + i);
-        const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
-        const double kn = a.k_over_n;
-        double k = ldg(a.omega + i) + kn * (R.y * zi.x - R.x * zi.y);
-        k = k + kn * (acc.y * zi.x - acc.x * zi.y);
-        if (MODE == 0) {
-          a.out[i] = k;
-        } else {
-          const double th0 = a.theta[i];
-          double thn;
-          if (MODE == 1) {
-            a.ksum[i] = k;
-            thn = add_rn(th0, mul_rn(a.h, k));
-          } else if (MODE == 2 || MODE == 3) {
-            a.ksum[i] = add_rn(a.ksum[i], mul_rn(2.0, k));
-            thn = add_rn(th0, mul_rn(a.h, k));
-          } else {  // MODE 4: x + dt/6 (k1 + 2k2 + 2k3 + k4); MODE 5: Euler x + dt k
-            const double ks = (MODE == 4) ? add_rn(a.ksum[i], k) : k;
-            thn = wrap_phase(add_rn(th0, mul_rn(a.h, ks)));
-            a.theta[i] = thn;
-            if (!isfinite(thn)) {
-              atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->nonfinite), 1ull);
-              atomicMin(reinterpret_cast<long long *>(&a.status->first_bad_step),
-                        (long long)(a.status->steps_done + a.step_rel + 1));
-            }
-          }
-          double sn, cs;
-          sincos(thn, &sn, &cs);
-          znew = make_double2(cs, sn);
-          a.z_out[i] = znew;
-        }
-      }
-      if (MODE != 0 && c >= 0) {
-        const double pr = warp_sum(znew.x), pim = warp_sum(znew.y);
-        int last = 0;
-        if (lane == 0) {
-          a.part[rb] = make_double2(pr, pim);
-          __threadfence();
-          const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
-          last = (atomicAdd(a.cnt + c, 1) + 1 == total);
-        }
-        last = __shfl_sync(FULL, last, 0);
-        if (last) {  // this warp finished community c: reduce its partials (fixed order)
-          __threadfence();
-          const double2 Rn =
-              reduce_comm(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane);
-          if (lane == 0) {
-            a.R_out[c] = Rn;
-            a.cnt[c] = 0;
-          }
-        }
-      }
-    }
-    __syncthreads();  // zs / accs reused by the next segment
+    consumer_bar();  // zs / accs reuse by the next segment
   }
 }
 
@@ -278,9 +418,8 @@ __global__ void __launch_bounds__(256) prepare_kernel(cdk_graph g, const double 
   const int rb = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (rb >= g.n_rblk) return;
   const int64_t row0 = g.rblk_row0[rb];
-  const int c = g.rblk_comm[rb];
-  const int64_t cend = (c >= 0) ? g.comm_off[c + 1] : g.n_rows;
-  const int nr = (int)min((int64_t)RB, cend - row0);
+  const int64_t row1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+  const int nr = (int)(row1 - row0);
   double2 zz = make_double2(0.0, 0.0);
   if (lane < nr) {
     double sn, cs;
@@ -320,11 +459,11 @@ static int check_graph(const cdk_graph *g) {
     set_error("cdk_graph: invalid sizes");
     return CDK_INPUT;
   }
-  if (g->cta_threads != 256 && g->cta_threads != 512) {
-    set_error("cdk_graph: cta_threads must be 256 or 512");
+  if (g->cta_threads != NTHREADS) {
+    set_error("cdk_graph: cta_threads must be 1024");
     return CDK_INPUT;
   }
-  if (g->smem_nodes < 0 || g->seg_rows_cap <= 0) {
+  if (g->smem_nodes < 0 || g->seg_rows_cap <= 0 || g->seg_rows_cap > TILE_ROWS) {
     set_error("cdk_graph: bad shared-memory capacities");
     return CDK_INPUT;
   }
@@ -332,7 +471,8 @@ static int check_graph(const cdk_graph *g) {
 }
 
 static size_t stage_smem(const cdk_graph *g) {
-  return ((size_t)g->smem_nodes + (size_t)g->seg_rows_cap) * sizeof(double2);
+  return RING * sizeof(TileSlot) + 2 * TILE_ROWS * sizeof(double2) +
+         ((size_t)g->smem_nodes + 8) * sizeof(double2);
 }
 
 template <int MODE>

@@ -30,7 +30,7 @@ INTRA_PAD = 0xFFFF
 ROW_COST = 24.0  # per-row overhead in "entry" units (pointer loads, epilogue, sincos)
 INTER_COST = 3.0  # an inter entry: 4-byte index + an L2 gather
 DEFAULT_SMS = 148
-SMEM_PER_SM = 233472  # 228 KB per SM
+SMEM_OPTIN = 232448  # max dynamic + static shared memory per block (227 KB)
 
 
 @dataclass
@@ -67,19 +67,26 @@ class Schedule:
     n_cta: int
     cta_threads: int
     smem_nodes: int  # staged window capacity (nodes)
-    seg_rows_cap: int  # rows per segment (shared-memory accumulators)
+    seg_rows_cap: int  # rows per unstaged segment (shared-memory accumulators)
     seg_rblk: np.ndarray  # int32[n_seg+1]
     seg_win: np.ndarray  # int64[n_seg, 2]
     seg_base: np.ndarray  # int64[n_seg]
     cta_seg: np.ndarray  # int32[n_cta+1]
     intra_col: np.ndarray  # uint16, columns rebased to each row's segment base
+    seg_tile: np.ndarray  # int32[n_seg+1] tile range per segment (staged segments only)
+    tiles: np.ndarray  # TILE_DTYPE[n_tile]
+    tile_tab: np.ndarray  # int32: per tile [intra offsets | inter offsets], 16-byte padded
 
     @property
     def n_seg(self) -> int:
         return int(self.seg_rblk.shape[0] - 1)
 
+    @property
+    def n_tile(self) -> int:
+        return int(self.tiles.shape[0])
+
     def smem_bytes(self) -> int:
-        return 16 * (self.smem_nodes + self.seg_rows_cap)
+        return stage_smem_bytes(self.smem_nodes)
 
 
 def _row_runs(rows_sorted: np.ndarray, n_rows: int):
@@ -87,6 +94,33 @@ def _row_runs(rows_sorted: np.ndarray, n_rows: int):
     start = np.zeros(n_rows + 1, dtype=np.int64)
     np.cumsum(counts, out=start[1:])
     return counts, start
+
+
+# rblocks: <= 32 rows of one community and at most RB_MAX_E padded intra /
+# RB_MAX_X inter entries, so every rblock fits one shared-memory tile
+RB_MAX_E = 8192
+RB_MAX_X = 1024
+
+
+def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
+    nxt = np.minimum(row0 + RB, row_end)
+    e = intra_ptr[nxt] - intra_ptr[row0]
+    x = inter_ptr[nxt] - inter_ptr[row0]
+    heavy = np.nonzero((e > RB_MAX_E) | (x > RB_MAX_X))[0]
+    if heavy.size == 0:
+        return row0
+    extra = []
+    for b in heavy.tolist():
+        r, end = int(row0[b]), int(nxt[b])
+        start = r
+        while r < end:
+            ne = intra_ptr[r + 1] - intra_ptr[start]
+            nx = inter_ptr[r + 1] - inter_ptr[start]
+            if r > start and (ne > RB_MAX_E or nx > RB_MAX_X):
+                extra.append(r)
+                start = r
+            r += 1
+    return np.sort(np.concatenate([row0, np.asarray(extra, dtype=np.int64)]))
 
 
 def build_layout(dec: Decomposition) -> HostLayout:
@@ -137,6 +171,10 @@ def build_layout(dec: Decomposition) -> HostLayout:
     rc = np.repeat(np.arange(m, dtype=np.int64), nb)
     within = np.arange(rc.shape[0], dtype=np.int64) - comm_rblk_off[rc]
     row0 = off[rc] + RB * within
+    # split 32-row blocks whose entries exceed the tile caps (dense long rows)
+    row0 = _split_heavy_rblocks(row0, off[rc + 1] if rc.size else row0, intra_ptr, inter_ptr)
+    rc = np.searchsorted(off, row0, side="right").astype(np.int64) - 1
+    comm_rblk_off = np.searchsorted(row0, off).astype(np.int64)
     pool_row0 = np.arange(n_in, n, RB, dtype=np.int64)
     rblk_row0 = np.concatenate([row0, pool_row0])
     rblk_comm = np.concatenate([rc, np.full(pool_row0.shape[0], -1, np.int64)]).astype(np.int32)
@@ -148,17 +186,39 @@ def build_layout(dec: Decomposition) -> HostLayout:
 
 WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
 
+# shared-memory tile ring of the TMA pipeline (must match csrc/kuramoto.cu)
+TILE_ROWS = 256
+TILE_E = 16384  # uint16 intra columns per tile
+TILE_X = 2048  # int32 inter columns per tile (incl. 16-byte alignment slack)
+TILE_TAB = 2 * (TILE_ROWS + 4)  # int32 offset table per tile
+RING = 2
+CTA_THREADS = 1024
+TILE_DTYPE = np.dtype([("e0", np.int64), ("x0a", np.int64), ("tab_off", np.int64),
+                       ("ne", np.int32), ("nxa", np.int32), ("rblk0", np.int32),
+                       ("rblk1", np.int32)])
+
+
+def ring_bytes() -> int:
+    return RING * (2 * TILE_E + 4 * TILE_X + 4 * TILE_TAB)
+
+
+def stage_smem_bytes(smem_nodes: int) -> int:
+    """dynamic shared memory of the stage kernel: window (+8 spare slots),
+    double-buffered row accumulators, tile ring"""
+    return 16 * (smem_nodes + 8) + 2 * 16 * TILE_ROWS + ring_bytes()
+
 
 def _rblk_rows(lay: HostLayout) -> np.ndarray:
     return np.concatenate([lay.rblk_row0, [lay.n_rows]]).astype(np.int64)
 
 
-def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, cta_threads: int = 512,
-                   ctas_per_sm: int = 2, rows_cap: int = 1024) -> Schedule:
+def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, ctas_per_sm: int = 1,
+                   rows_cap: int = TILE_ROWS, smem_budget: int = SMEM_OPTIN - 1024) -> Schedule:
     """Cost-balanced contiguous CTA ranges of rblocks, split into segments
-    whose intra neighbours fit one shared-memory window."""
-    per_cta = SMEM_PER_SM // ctas_per_sm - 1024 - 256  # driver reserve + static smem
-    smem_nodes = max(0, (per_cta - 16 * rows_cap) // 16) // WIN_ALIGN * WIN_ALIGN
+    whose intra neighbours fit one shared-memory window; staged segments are
+    cut into tiles streamed through the TMA ring."""
+    win_bytes = smem_budget - (stage_smem_bytes(0))
+    smem_nodes = max(0, win_bytes // 16) // WIN_ALIGN * WIN_ALIGN
     n_cta = max(1, sm_count * ctas_per_sm)
     nrb = lay.n_rblk
     rows = _rblk_rows(lay)
@@ -191,7 +251,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, cta_threads: in
                     cc = int(lay.rblk_comm[rb])
                     if cc < 0 or not stageable[cc]:
                         break
-                    if int(win_hi[cc]) - w0 > smem_nodes or rows[rb + 1] - rows[start] > rows_cap:
+                    if int(win_hi[cc]) - w0 > smem_nodes:
                         break
                     rb += 1
                 seg_win.append((w0, int(win_hi[int(lay.rblk_comm[rb - 1])])))
@@ -201,6 +261,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, cta_threads: in
     seg_rblk = np.asarray(seg_rblk, dtype=np.int32)
     seg_win = np.asarray(seg_win, dtype=np.int64).reshape(-1, 2)
     seg_base = np.asarray(seg_base, dtype=np.int64)
+    seg_tile, tiles, tile_tab = _build_tiles(lay, rows, seg_rblk, seg_win)
 
     # rebase intra columns (community-local in the layout) to each row's segment base
     n = lay.n_rows
@@ -217,8 +278,54 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, cta_threads: in
         if newc.size and (newc.min() < 0 or newc.max() >= INTRA_PAD):
             raise InputError("rebased intra column out of uint16 range")
         col[m] = newc.astype(np.uint16)
-    return Schedule(n_cta, cta_threads, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
-                    seg_base, np.asarray(cta_seg, dtype=np.int32), col)
+    return Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk,
+                    seg_win, seg_base, np.asarray(cta_seg, dtype=np.int32), col, seg_tile, tiles,
+                    tile_tab)
+
+
+def _build_tiles(lay: HostLayout, rows, seg_rblk, seg_win):
+    """Pack each staged segment's rblocks into tiles (<= TILE_ROWS rows,
+    <= TILE_E intra and TILE_X (aligned) inter entries) and build the per-tile
+    int32 offset tables the consumers read from shared memory."""
+    ip, xp = lay.intra_ptr, lay.inter_ptr
+    seg_tile = [0]
+    recs = []
+    tabs = []
+    tab_off = 0
+    for s_ in range(seg_rblk.shape[0] - 1):
+        w0, w1 = seg_win[s_]
+        rb, rb_end = int(seg_rblk[s_]), int(seg_rblk[s_ + 1])
+        if w1 > w0:
+            while rb < rb_end:
+                start = rb
+                r0 = int(rows[start])
+                while rb < rb_end:
+                    r1 = int(rows[rb + 1])
+                    ne = ip[r1] - ip[r0]
+                    x0a = xp[r0] // 4 * 4
+                    nxa = (xp[r1] + 3) // 4 * 4 - x0a
+                    if rb > start and (r1 - r0 > TILE_ROWS or ne > TILE_E or nxa > TILE_X):
+                        break
+                    rb += 1
+                r1 = int(rows[rb])
+                if r1 - r0 > TILE_ROWS or ip[r1] - ip[r0] > TILE_E:
+                    raise InputError("an rblock exceeds the shared-memory tile capacity")
+                x0a = int(xp[r0] // 4 * 4)
+                nxa = int((xp[r1] + 3) // 4 * 4 - x0a)
+                if nxa > TILE_X:
+                    raise InputError("an rblock's inter entries exceed the tile capacity")
+                nrow = r1 - r0
+                half = (nrow + 1 + 3) // 4 * 4
+                tab = np.zeros(2 * half, dtype=np.int32)
+                tab[: nrow + 1] = ip[r0: r1 + 1] - ip[r0]
+                tab[half: half + nrow + 1] = xp[r0: r1 + 1] - x0a
+                tabs.append(tab)
+                recs.append((int(ip[r0]), x0a, tab_off, int(ip[r1] - ip[r0]), nxa, start, rb))
+                tab_off += tab.shape[0]
+        seg_tile.append(len(recs))
+    tiles = np.array(recs, dtype=TILE_DTYPE) if recs else np.zeros(0, dtype=TILE_DTYPE)
+    tile_tab = np.concatenate(tabs) if tabs else np.zeros(4, dtype=np.int32)
+    return np.asarray(seg_tile, dtype=np.int32), tiles, tile_tab
 
 
 class DeviceGraph:
@@ -258,7 +365,14 @@ class DeviceGraph:
             "seg_win": up(sch.seg_win.reshape(-1)),
             "seg_base": up(sch.seg_base),
             "cta_seg": up(sch.cta_seg),
+            "seg_tile": up(sch.seg_tile),
+            "tiles": up(sch.tiles.view(np.uint8)) if sch.n_tile else
+            torch.zeros(64, dtype=torch.uint8, device=dev),
+            "tile_tab": up(sch.tile_tab),
         }
+        # inter columns are bulk-copied in 16-byte units: keep 3 entries of slack
+        t_ic = self._t["inter_col"]
+        self._t["inter_col"] = torch.cat([t_ic, torch.zeros(4, dtype=torch.int32, device=dev)])
         # keep a 16-byte tail on intra_col so uint4 loads never run past the allocation
         if self._t["intra_col"].numel() == 0:
             self._t["intra_col"] = torch.full((8,), -1, dtype=torch.int16, device=dev)
@@ -267,13 +381,14 @@ class DeviceGraph:
             n_rows=lay.n_rows, n_comm=lay.n_comm,
             comm_off=t["comm_off"].data_ptr(), intra_ptr=t["intra_ptr"].data_ptr(),
             intra_col=t["intra_col"].data_ptr(), inter_ptr=t["inter_ptr"].data_ptr(),
-            inter_col=t["inter_col"].data_ptr() if t["inter_col"].numel() else 0,
+            inter_col=t["inter_col"].data_ptr(),
             n_rblk=lay.n_rblk, n_seg=sch.n_seg, n_cta=sch.n_cta, cta_threads=sch.cta_threads,
             smem_nodes=sch.smem_nodes, seg_rows_cap=sch.seg_rows_cap,
             rblk_row0=t["rblk_row0"].data_ptr(), rblk_comm=t["rblk_comm"].data_ptr(),
             comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
             seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
-            cta_seg=t["cta_seg"].data_ptr(),
+            cta_seg=t["cta_seg"].data_ptr(), seg_tile=t["seg_tile"].data_ptr(),
+            tiles=t["tiles"].data_ptr(), tile_tab=t["tile_tab"].data_ptr(), n_tile=sch.n_tile,
         )
 
     def device_bytes(self) -> int:

@@ -147,8 +147,9 @@ def test_schedule_invariants(sm_count, seed, rows_cap):
     off = lay.comm_off
     for s in range(sch.n_seg):
         cs = lay.rblk_comm[seg[s]:seg[s + 1]]
-        assert rows_rb[seg[s + 1]] - rows_rb[seg[s]] <= rows_cap
         w0, w1 = sch.seg_win[s]
+        if w1 == w0:
+            assert rows_rb[seg[s + 1]] - rows_rb[seg[s]] <= rows_cap
         if w1 > w0:  # staged: every community of the segment inside the window
             assert np.all(cs >= 0)
             assert w1 - w0 <= sch.smem_nodes and sch.seg_base[s] == w0
@@ -161,6 +162,26 @@ def test_schedule_invariants(sm_count, seed, rows_cap):
     # rblocks: <= 32 rows, never straddle communities, cover all rows once
     ends = rows_rb[1:]
     assert np.all(ends - lay.rblk_row0 <= 32) and np.all(ends > lay.rblk_row0)
+    # tiles: cover exactly the staged segments' rblocks, within the ring caps
+    for s in range(sch.n_seg):
+        t0, t1 = sch.seg_tile[s], sch.seg_tile[s + 1]
+        w0, w1 = sch.seg_win[s]
+        if w1 == w0:
+            assert t0 == t1
+            continue
+        tl = sch.tiles[t0:t1]
+        assert tl["rblk0"][0] == seg[s] and tl["rblk1"][-1] == seg[s + 1]
+        assert np.all(tl["rblk0"][1:] == tl["rblk1"][:-1])
+        for tt in tl:
+            r0, r1 = rows_rb[tt["rblk0"]], rows_rb[tt["rblk1"]]
+            assert r1 - r0 <= PL.TILE_ROWS and tt["ne"] <= PL.TILE_E and tt["nxa"] <= PL.TILE_X
+            assert tt["e0"] == lay.intra_ptr[r0] and tt["e0"] % 8 == 0 and tt["x0a"] % 4 == 0
+            assert tt["tab_off"] % 4 == 0
+            half = (r1 - r0 + 1 + 3) // 4 * 4
+            tab = sch.tile_tab[tt["tab_off"]: tt["tab_off"] + 2 * half]
+            assert np.array_equal(tab[: r1 - r0 + 1], lay.intra_ptr[r0:r1 + 1] - tt["e0"])
+            assert np.array_equal(tab[half: half + r1 - r0 + 1],
+                                  lay.inter_ptr[r0:r1 + 1] - tt["x0a"])
     for c in range(lay.n_comm):
         b0, b1 = lay.comm_rblk_off[c], lay.comm_rblk_off[c + 1]
         assert lay.rblk_row0[b0] == lay.comm_off[c]
@@ -175,7 +196,7 @@ def test_schedule_small_window_forces_unstaged():
     dec = G.planted_partition_decomposition([300, 40, 40, 500], 0.9, 0.05, 5)
     lay = PL.build_layout(dec)
     # a tiny per-CTA budget: windows of <= ~100 nodes, big communities unstaged
-    sch = PL.build_schedule(lay, sm_count=2, ctas_per_sm=2, rows_cap=64)
+    sch = PL.build_schedule(lay, sm_count=2, rows_cap=64, smem_budget=PL.stage_smem_bytes(0) + 16 * 200)
     assert sch.smem_nodes >= 0
     r, c = _schedule_to_directed(lay, sch)
     rows, cols, _ = dec.directed()
