@@ -75,16 +75,23 @@ struct StageArgs {
   int64_t step_rel;
 };
 
-// Sum of rblock partials of community c, fixed order (lane-strided, butterfly).
-__device__ __forceinline__ double2 reduce_comm(const double2 *part, int b0, int b1, int lane) {
+// Canonical community sum R_c of the rblock partials: 8 lanes, lane t sums
+// partials b0+t, b0+t+8, ... in order, then a fixed xor butterfly (4, 2, 1).
+// Used by every producer of R (prepare and all stage kernels) so R is
+// bitwise independent of which CTA/GPU reduces it.
+__device__ __forceinline__ double2 reduce_comm8(const double2 *part, int b0, int b1, int t,
+                                                unsigned mask) {
   double sr = 0.0, si = 0.0;
-  for (int b = b0 + lane; b < b1; b += 32) {
+  for (int b = b0 + t; b < b1; b += 8) {
     double2 v = ldcg2(part + b);
     sr += v.x;
     si += v.y;
   }
-  sr = warp_sum(sr);
-  si = warp_sum(si);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    sr += __shfl_xor_sync(mask, sr, o);
+    si += __shfl_xor_sync(mask, si, o);
+  }
   return make_double2(sr, si);
 }
 
@@ -173,27 +180,33 @@ __device__ __forceinline__ void gather_rows_global(const cdk_graph &g,
 }
 
 // ---------------------------------------------------------------------------
-// TMA-pipelined stage kernel.  One CTA per SM, 32 warps:
+// TMA-pipelined, barrier-free stage kernel.  One CTA per SM, 32 warps:
 //   warp 31 (one lane) = producer: streams each tile's CSR slices (uint16
-//     intra columns, int32 inter columns, int32 row-offset table) into a
-//     2-slot shared-memory ring with bulk async copies (full/empty mbarriers);
-//   warps 0..30 = consumers: per segment, one bulk copy of the node window of
-//     z_in into shared memory; per tile, 8-lane groups gather rows from the
-//     window (conflict-free 16-byte LDS per column), reduce, store the row
-//     sums; after a consumer-only named barrier the tile's rblocks run the
-//     epilogue (RK4 stage update, sincos, rblock partials, community R).
+//     intra columns, int32 inter columns, int32 row table) into a 2-slot
+//     shared-memory ring with bulk async copies (full/empty mbarriers);
+//   warps 0..30 = 124 consumer groups of 8 lanes.  Per segment, one bulk copy
+//     stages the node window of z_in in shared memory.  Per tile, groups claim
+//     rows from a shared counter (dynamic balance, no CTA barrier), gather
+//     the row from the window, store the row sum, and count the row into its
+//     rblock; the group that completes an rblock runs its epilogue (RK4 stage
+//     update, sincos, canonical rblock partial, community completion).  The
+//     slot is refilled once every group has left the tile and the tile's last
+//     epilogue is done (empty barrier expects NGROUPS + 1 arrivals).
 // Unstaged segments (communities above the window capacity, NONE pool) are
-// processed by the consumers straight from global memory.
+// processed from global memory with CTA barriers (rare path).
+// All reductions have a fixed shape => bitwise deterministic and independent
+// of the schedule (and so of the GPU count).
 // ---------------------------------------------------------------------------
 constexpr int TILE_ROWS = 256;
 constexpr int TILE_E = 16384;
 constexpr int TILE_X = 2048;
-constexpr int TILE_TAB = 2 * (TILE_ROWS + 4);
+constexpr int TILE_TAB = 2 * (TILE_ROWS + 4) + TILE_ROWS;
 constexpr int RING = 2;
 constexpr int NTHREADS = 1024;
 constexpr int NCONS_WARPS = 31;
 constexpr int NCONS = NCONS_WARPS * 32;
 constexpr int NGROUPS = NCONS / 8;
+constexpr int CNT_STRIDE = TILE_ROWS + 4;
 
 struct TileSlot {
   uint16_t cols[TILE_E];
@@ -209,25 +222,28 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// epilogue of rblocks [rbA, rbB): lane = row; acc rows indexed from accrow0
+// Epilogue of one rblock by an 8-lane group: lane t owns rows t, t+8, t+16,
+// t+24 of the rblock.  Canonical rblock partial: per-lane sum in row order,
+// then the 8-lane butterfly.  The group that completes community c reduces R.
 template <int MODE>
-__device__ __forceinline__ void epilogue(const StageArgs &a, int rbA, int rbB, int warp,
-                                         int nwarp, int lane, const double2 *acc,
-                                         int64_t accrow0, bool staged, const double2 *zs,
-                                         int64_t w0) {
+__device__ __forceinline__ void epilogue_group(const StageArgs &a, int rb, int t, unsigned gmask,
+                                               const double2 *acc, int64_t accrow0, bool staged,
+                                               const double2 *zs, int64_t w0) {
   const cdk_graph &g = a.g;
-  for (int rb = rbA + warp; rb < rbB; rb += nwarp) {
-    const int64_t rrow0 = g.rblk_row0[rb];
-    const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
-    const int nr = (int)(rrow1 - rrow0);
-    const int c = g.rblk_comm[rb];
-    double2 znew = make_double2(0.0, 0.0);
-    if (lane < nr) {
-      const int64_t i = rrow0 + lane;
+  const int64_t rrow0 = g.rblk_row0[rb];
+  const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+  const int nr = (int)(rrow1 - rrow0);
+  const int c = g.rblk_comm[rb];
+  const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
+  const double kn = a.k_over_n;
+  double pr = 0.0, pim = 0.0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int l = t + 8 * m;
+    if (l < nr) {
+      const int64_t i = rrow0 + l;
       const double2 ac = acc[i - accrow0];
       const double2 zi = staged ? zs[i - w0] : ldg(a.z_in + i);
-      const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
-      const double kn = a.k_over_n;
       double k = ldg(a.omega + i) + kn * (R.y * zi.x - R.x * zi.y);
       k = k + kn * (ac.y * zi.x - ac.x * zi.y);
       if (MODE == 0) {
@@ -253,27 +269,34 @@ __device__ __forceinline__ void epilogue(const StageArgs &a, int rbA, int rbB, i
         }
         double sn, cs;
         sincos(thn, &sn, &cs);
-        znew = make_double2(cs, sn);
-        a.z_out[i] = znew;
+        a.z_out[i] = make_double2(cs, sn);
+        pr += cs;
+        pim += sn;
       }
     }
-    if (MODE != 0 && c >= 0) {
-      const double pr = warp_sum(znew.x), pim = warp_sum(znew.y);
-      int last = 0;
-      if (lane == 0) {
-        a.part[rb] = make_double2(pr, pim);
-        __threadfence();
-        const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
-        last = (atomicAdd(a.cnt + c, 1) + 1 == total);
-      }
-      last = __shfl_sync(FULL, last, 0);
-      if (last) {  // this warp finished community c: reduce its partials (fixed order)
-        __threadfence();
-        const double2 Rn = reduce_comm(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane);
-        if (lane == 0) {
-          a.R_out[c] = Rn;
-          a.cnt[c] = 0;
-        }
+  }
+  if (MODE != 0 && c >= 0) {
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      pr += __shfl_xor_sync(gmask, pr, o);
+      pim += __shfl_xor_sync(gmask, pim, o);
+    }
+    const int leader = (threadIdx.x & 31) & 24;
+    int last = 0;
+    if (t == 0) {
+      a.part[rb] = make_double2(pr, pim);
+      __threadfence();
+      const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
+      last = (atomicAdd(a.cnt + c, 1) + 1 == total);
+    }
+    last = __shfl_sync(gmask, last, leader);
+    if (last) {  // this group finished community c: reduce its partials
+      __threadfence();
+      const double2 Rn =
+          reduce_comm8(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], t, gmask);
+      if (t == 0) {
+        a.R_out[c] = Rn;
+        a.cnt[c] = 0;
       }
     }
   }
@@ -284,17 +307,22 @@ template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar_full[RING], bar_empty[RING], bar_win;
+  __shared__ int s_next[RING], s_rbdone[RING];
   const cdk_graph &g = a.g;
   TileSlot *ring = reinterpret_cast<TileSlot *>(smem_raw);
   double2 *accs = reinterpret_cast<double2 *>(smem_raw + RING * sizeof(TileSlot));
-  double2 *zs = accs + 2 * TILE_ROWS;
+  int *cnt_rb = reinterpret_cast<int *>(accs + RING * TILE_ROWS);
+  double2 *zs = reinterpret_cast<double2 *>(cnt_rb + RING * CNT_STRIDE);
   const uint32_t zero_slot = (uint32_t)g.smem_nodes;  // zs[smem_nodes] == 0
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
+  for (int i = tid; i < RING * CNT_STRIDE; i += NTHREADS) cnt_rb[i] = 0;
   if (tid == 0) {
     for (int b = 0; b < RING; ++b) {
       mbar_init(&bar_full[b], 1);
-      mbar_init(&bar_empty[b], 1);
+      mbar_init(&bar_empty[b], NGROUPS + 1);
+      s_next[b] = 0;
+      s_rbdone[b] = 0;
     }
     mbar_init(&bar_win, 1);
     zs[zero_slot] = make_double2(0.0, 0.0);
@@ -307,13 +335,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       for (int s = segA; s < segB; ++s) {
         for (int ti = g.seg_tile[s]; ti < g.seg_tile[s + 1]; ++ti, ++k) {
           const int b = k & 1, n = k >> 1;
-          if (n > 0) mbar_wait(&bar_empty[b], (n - 1) & 1);
+          if (n > 0) {
+            mbar_wait(&bar_empty[b], (n - 1) & 1);
+            // every consumer left the slot: reset its claim/completion counters
+            s_next[b] = 0;
+            s_rbdone[b] = 0;
+            for (int i = 0; i < CNT_STRIDE; ++i) cnt_rb[b * CNT_STRIDE + i] = 0;
+            fence_proxy_async_smem();
+          }
           const cdk_tile T = g.tiles[ti];
           const int64_t r0 = g.rblk_row0[T.rblk0];
           const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
-          const int half = ((int)(r1 - r0) + 1 + 3) & ~3;
+          const int nrow = (int)(r1 - r0);
+          const int half = (nrow + 1 + 3) & ~3;
           const uint32_t be = (uint32_t)T.ne * 2u, bx = (uint32_t)T.nxa * 4u,
-                         bt = (uint32_t)half * 8u;
+                         bt = (uint32_t)(2 * half + ((nrow + 3) & ~3)) * 4u;
           mbar_expect_tx(&bar_full[b], be + bx + bt);
           if (be) bulk_g2s(ring[b].cols, g.intra_col + T.e0, be, &bar_full[b]);
           if (bx) bulk_g2s(ring[b].xcol, g.inter_col + T.x0a, bx, &bar_full[b]);
@@ -327,7 +363,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
   // ---------------- consumers (warps 0..30) ----------------
   const int t = lane & 7;
   const int grp = tid >> 3;
-  const unsigned gmask = 0xFFu << (lane & 24);  // this 8-lane group only
+  const int leader = lane & 24;
+  const unsigned gmask = 0xFFu << leader;  // this 8-lane group only
   int k = 0;
   uint32_t win_par = 0;
   for (int s = segA; s < segB; ++s) {
@@ -352,8 +389,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
         const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
         const int nrow = (int)(r1 - r0);
         const int half = (nrow + 1 + 3) & ~3;
-        double2 *acc = accs + (k & 1) * TILE_ROWS;
-        for (int r = grp; r < nrow; r += NGROUPS) {
+        const int nrb = T.rblk1 - T.rblk0;
+        double2 *acc = accs + b * TILE_ROWS;
+        int *cnt = cnt_rb + b * CNT_STRIDE;
+        while (true) {
+          int r = 0;
+          if (t == 0) r = atomicAdd(&s_next[b], 1);
+          r = __shfl_sync(gmask, r, leader);
+          if (r >= nrow) break;
           const int ie0 = S.tab[r], ie1 = S.tab[r + 1];
           const int xe0 = S.tab[half + r], xe1 = S.tab[half + r + 1];
           const int32_t j = (xe0 + t < xe1) ? S.xcol[xe0 + t] : -1;
@@ -373,18 +416,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
             sr += __shfl_xor_sync(gmask, sr, o);
             si += __shfl_xor_sync(gmask, si, o);
           }
-          if (t == 0) acc[r] = make_double2(sr, si);
+          int last = 0, lrb = 0;
+          if (t == 0) {
+            acc[r] = make_double2(sr, si);
+            __threadfence_block();
+            lrb = S.tab[2 * half + r];
+            const int rb = T.rblk0 + lrb;
+            const int64_t e = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+            last = (atomicAdd(&cnt[lrb], 1) + 1 == (int)(e - g.rblk_row0[rb]));
+          }
+          last = __shfl_sync(gmask, last, leader);
+          if (last) {
+            lrb = __shfl_sync(gmask, lrb, leader);
+            __threadfence_block();
+            epilogue_group<MODE>(a, T.rblk0 + lrb, t, gmask, acc, r0, true, zs, w0);
+            if (t == 0 && atomicAdd(&s_rbdone[b], 1) + 1 == nrb) mbar_arrive(&bar_empty[b]);
+          }
         }
-        consumer_bar();  // tile's row sums complete; ring slot b no longer read
-        if (tid == 0) mbar_arrive(&bar_empty[b]);
-        epilogue<MODE>(a, T.rblk0, T.rblk1, warp, NCONS_WARPS, lane, acc, r0, true, zs, w0);
+        if (t == 0) mbar_arrive(&bar_empty[b]);  // this group is done with the tile
       }
     } else {
       const int64_t row0 = g.rblk_row0[rbA];
       const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
       const int nrows = (int)(row1 - row0);
       const double2 *zbase = a.z_in + g.seg_base[s];
-      double2 *acc = accs + (k & 1) * TILE_ROWS;
+      double2 *acc = accs;  // ring slots are idle on this path only after a barrier
+      consumer_bar();
       for (int r = grp; r < nrows; r += 2 * NGROUPS) {
         const int rB = r + NGROUPS;
         const bool hasB = rB < nrows;
@@ -404,39 +461,51 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
         }
       }
       consumer_bar();
-      epilogue<MODE>(a, rbA, rbB, warp, NCONS_WARPS, lane, acc, row0, false, zs, 0);
-      ++k;
+      for (int rb = rbA + grp; rb < rbB; rb += NGROUPS)
+        epilogue_group<MODE>(a, rb, t, gmask, acc, row0, false, zs, 0);
     }
     consumer_bar();  // zs / accs reuse by the next segment
   }
 }
 
-// z = exp(i theta) per rblock and the rblock partials (prepare).
+// z = exp(i theta) and the canonical rblock partials (prepare).  One 8-lane
+// group per rblock, lane t owns rows t, t+8, t+16, t+24 (same shape as the
+// stage epilogue).
 __global__ void __launch_bounds__(256) prepare_kernel(cdk_graph g, const double *theta,
                                                       double2 *z, double2 *part) {
-  const int lane = threadIdx.x & 31;
-  const int rb = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (rb >= g.n_rblk) return;
+  const int t = threadIdx.x & 7;
+  const int rb = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  if (rb >= g.n_rblk) return;  // whole 8-lane groups exit together
+  const unsigned gmask = 0xFFu << (threadIdx.x & 24);
   const int64_t row0 = g.rblk_row0[rb];
   const int64_t row1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
   const int nr = (int)(row1 - row0);
-  double2 zz = make_double2(0.0, 0.0);
-  if (lane < nr) {
-    double sn, cs;
-    sincos(theta[row0 + lane], &sn, &cs);
-    zz = make_double2(cs, sn);
-    z[row0 + lane] = zz;
+  double pr = 0.0, pim = 0.0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int l = t + 8 * m;
+    if (l < nr) {
+      double sn, cs;
+      sincos(theta[row0 + l], &sn, &cs);
+      z[row0 + l] = make_double2(cs, sn);
+      pr += cs;
+      pim += sn;
+    }
   }
-  const double pr = warp_sum(zz.x), pi = warp_sum(zz.y);
-  if (lane == 0) part[rb] = make_double2(pr, pi);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    pr += __shfl_xor_sync(gmask, pr, o);
+    pim += __shfl_xor_sync(gmask, pim, o);
+  }
+  if (t == 0) part[rb] = make_double2(pr, pim);
 }
 
 __global__ void comm_reduce_kernel(cdk_graph g, const double2 *part, double2 *R, int32_t *cnt,
                                    cdk_run_status *st) {
   const int c = blockIdx.x;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x;  // blockDim.x == 8
   if (c < g.n_comm) {
-    const double2 Rc = reduce_comm(part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane);
+    const double2 Rc = reduce_comm8(part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane, 0xFFu);
     if (lane == 0) {
       R[c] = Rc;
       cnt[c] = 0;
@@ -471,8 +540,8 @@ static int check_graph(const cdk_graph *g) {
 }
 
 static size_t stage_smem(const cdk_graph *g) {
-  return RING * sizeof(TileSlot) + 2 * TILE_ROWS * sizeof(double2) +
-         ((size_t)g->smem_nodes + 8) * sizeof(double2);
+  return RING * sizeof(TileSlot) + RING * TILE_ROWS * sizeof(double2) +
+         RING * CNT_STRIDE * sizeof(int) + ((size_t)g->smem_nodes + 8) * sizeof(double2);
 }
 
 template <int MODE>
@@ -500,12 +569,12 @@ static int launch_stage(const StageArgs &a, cudaStream_t st) {
 
 static int prepare(const cdk_graph *g, const double *theta, const Workspace &w, cudaStream_t st) {
   if (g->n_rblk > 0) {
-    const int wpb = 8;
-    prepare_kernel<<<(g->n_rblk + wpb - 1) / wpb, 32 * wpb, 0, st>>>(*g, theta, w.z[0], w.part);
+    const int gpb = 32;  // 8-lane groups per block
+    prepare_kernel<<<(g->n_rblk + gpb - 1) / gpb, 8 * gpb, 0, st>>>(*g, theta, w.z[0], w.part);
     CDK_CHECK_LAUNCH("prepare_kernel");
   }
   const int m = (int)g->n_comm;
-  comm_reduce_kernel<<<m > 0 ? m : 1, 32, 0, st>>>(*g, w.part, w.R[0], w.cnt, w.status);
+  comm_reduce_kernel<<<m > 0 ? m : 1, 8, 0, st>>>(*g, w.part, w.R[0], w.cnt, w.status);
   CDK_CHECK_LAUNCH("comm_reduce_kernel");
   return CDK_OK;
 }

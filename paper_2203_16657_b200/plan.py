@@ -190,7 +190,7 @@ WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-
 TILE_ROWS = 256
 TILE_E = 16384  # uint16 intra columns per tile
 TILE_X = 2048  # int32 inter columns per tile (incl. 16-byte alignment slack)
-TILE_TAB = 2 * (TILE_ROWS + 4)  # int32 offset table per tile
+TILE_TAB = 2 * (TILE_ROWS + 4) + TILE_ROWS  # int32 offset table per tile
 RING = 2
 CTA_THREADS = 1024
 TILE_DTYPE = np.dtype([("e0", np.int64), ("x0a", np.int64), ("tab_off", np.int64),
@@ -205,7 +205,8 @@ def ring_bytes() -> int:
 def stage_smem_bytes(smem_nodes: int) -> int:
     """dynamic shared memory of the stage kernel: window (+8 spare slots),
     double-buffered row accumulators, tile ring"""
-    return 16 * (smem_nodes + 8) + 2 * 16 * TILE_ROWS + ring_bytes()
+    return (16 * (smem_nodes + 8) + 2 * 16 * TILE_ROWS + ring_bytes()
+            + 4 * RING * (TILE_ROWS + 4))  # per-slot rblock counters
 
 
 def _rblk_rows(lay: HostLayout) -> np.ndarray:
@@ -316,9 +317,12 @@ def _build_tiles(lay: HostLayout, rows, seg_rblk, seg_win):
                     raise InputError("an rblock's inter entries exceed the tile capacity")
                 nrow = r1 - r0
                 half = (nrow + 1 + 3) // 4 * 4
-                tab = np.zeros(2 * half, dtype=np.int32)
+                tab = np.zeros(2 * half + (nrow + 3) // 4 * 4, dtype=np.int32)
                 tab[: nrow + 1] = ip[r0: r1 + 1] - ip[r0]
                 tab[half: half + nrow + 1] = xp[r0: r1 + 1] - x0a
+                # local rblock index of every row of the tile
+                tab[2 * half: 2 * half + nrow] = np.repeat(
+                    np.arange(rb - start, dtype=np.int32), np.diff(rows[start: rb + 1]))
                 tabs.append(tab)
                 recs.append((int(ip[r0]), x0a, tab_off, int(ip[r1] - ip[r0]), nxa, start, rb))
                 tab_off += tab.shape[0]

@@ -182,6 +182,10 @@ def test_schedule_invariants(sm_count, seed, rows_cap):
             assert np.array_equal(tab[: r1 - r0 + 1], lay.intra_ptr[r0:r1 + 1] - tt["e0"])
             assert np.array_equal(tab[half: half + r1 - r0 + 1],
                                   lay.inter_ptr[r0:r1 + 1] - tt["x0a"])
+            rbl = sch.tile_tab[tt["tab_off"] + 2 * half: tt["tab_off"] + 2 * half + r1 - r0]
+            for lr, rr in enumerate(range(r0, r1)):
+                grb = tt["rblk0"] + rbl[lr]
+                assert rows_rb[grb] <= rr < rows_rb[grb + 1]
     for c in range(lay.n_comm):
         b0, b1 = lay.comm_rblk_off[c], lay.comm_rblk_off[c + 1]
         assert lay.rblk_row0[b0] == lay.comm_off[c]
