@@ -13,7 +13,7 @@ import threading
 from .errors import CDK_CUDA, CDK_INPUT, CDK_NUMERIC, CDK_OK, DeviceError, InputError, NumericError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_build", "libcommdyn_cuda.so")
+LIB_PATH = os.environ.get("CDK_LIB") or os.path.join(_PKG, "_build", "libcommdyn_cuda.so")
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

@@ -48,12 +48,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> str:
-    if not force and not _stale():
+def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False,
+                  debug: bool = False) -> str:
+    out = LIB if not debug else LIB.replace(".so", "_debug.so")
+    if not debug and not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-o", tmp, *sources()]
+    if debug:
+        cmd.insert(1, "-DCDK_DEBUG")
     if ptxas_verbose:
         cmd.insert(1, "-Xptxas=-v")
     if verbose:
@@ -63,9 +67,10 @@ def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: boo
         raise RuntimeError(f"nvcc failed:\n{res.stderr}")
     if ptxas_verbose or verbose:
         print(res.stderr, file=sys.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build_library(force=True, verbose=True, ptxas_verbose="-v" in sys.argv))
+    print(build_library(force=True, verbose=True, ptxas_verbose="-v" in sys.argv,
+                        debug="--debug" in sys.argv))

@@ -22,6 +22,21 @@
 
 namespace cdk {
 
+#ifdef CDK_DEBUG
+#define DBG_CHECK(cond, fmt, ...)                                                  \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      printf("CDK_DEBUG %s:%d block %d thread %d: " fmt "\n", __FILE__, __LINE__, \
+             blockIdx.x, threadIdx.x, __VA_ARGS__);                                \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define DBG_CHECK(cond, fmt, ...) \
+  do {                            \
+  } while (0)
+#endif
+
 
 struct Workspace {
   double2 *z[2];
@@ -197,11 +212,11 @@ __device__ __forceinline__ void gather_rows_global(const cdk_graph &g,
 // All reductions have a fixed shape => bitwise deterministic and independent
 // of the schedule (and so of the GPU count).
 // ---------------------------------------------------------------------------
-constexpr int TILE_ROWS = 256;
-constexpr int TILE_E = 16384;
-constexpr int TILE_X = 2048;
+constexpr int TILE_ROWS = 128;
+constexpr int TILE_E = 8192;
+constexpr int TILE_X = 1024;
 constexpr int TILE_TAB = 2 * (TILE_ROWS + 4) + TILE_ROWS;
-constexpr int RING = 2;
+constexpr int RING = 4;
 constexpr int NTHREADS = 1024;
 constexpr int NCONS_WARPS = 31;
 constexpr int NCONS = NCONS_WARPS * 32;
@@ -306,8 +321,15 @@ __device__ __forceinline__ void epilogue_group(const StageArgs &a, int rb, int t
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  // full: tile data landed (TMA tx); empty: all rows of the tile gathered
+  // (slot reusable).  A group only waits for tiles it has rows in, so it may
+  // skip fills: s_slot_tag[b] names the tile currently filling/filled in slot
+  // b (set by the producer before the copies) and is checked before the
+  // parity wait; s_acc_owner[b] names the tile allowed to use accumulator
+  // slot b (advanced by the tile's last epilogue).
   __shared__ __align__(8) uint64_t bar_full[RING], bar_empty[RING], bar_win;
-  __shared__ int s_next[RING], s_rbdone[RING];
+  __shared__ int s_rows_done[RING], s_rb_done[RING];
+  __shared__ volatile int s_slot_tag[RING], s_acc_owner[RING];
   const cdk_graph &g = a.g;
   TileSlot *ring = reinterpret_cast<TileSlot *>(smem_raw);
   double2 *accs = reinterpret_cast<double2 *>(smem_raw + RING * sizeof(TileSlot));
@@ -320,9 +342,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
   if (tid == 0) {
     for (int b = 0; b < RING; ++b) {
       mbar_init(&bar_full[b], 1);
-      mbar_init(&bar_empty[b], NGROUPS + 1);
-      s_next[b] = 0;
-      s_rbdone[b] = 0;
+      mbar_init(&bar_empty[b], 1);
+      s_rows_done[b] = 0;
+      s_rb_done[b] = 0;
+      s_slot_tag[b] = -1;
+      s_acc_owner[b] = b;
     }
     mbar_init(&bar_win, 1);
     zs[zero_slot] = make_double2(0.0, 0.0);
@@ -334,15 +358,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       int k = 0;
       for (int s = segA; s < segB; ++s) {
         for (int ti = g.seg_tile[s]; ti < g.seg_tile[s + 1]; ++ti, ++k) {
-          const int b = k & 1, n = k >> 1;
-          if (n > 0) {
-            mbar_wait(&bar_empty[b], (n - 1) & 1);
-            // every consumer left the slot: reset its claim/completion counters
-            s_next[b] = 0;
-            s_rbdone[b] = 0;
-            for (int i = 0; i < CNT_STRIDE; ++i) cnt_rb[b * CNT_STRIDE + i] = 0;
-            fence_proxy_async_smem();
-          }
+          const int b = k % RING, n = k / RING;
+          if (n > 0) mbar_wait(&bar_empty[b], (n - 1) & 1);
+          s_slot_tag[b] = k;
           const cdk_tile T = g.tiles[ti];
           const int64_t r0 = g.rblk_row0[T.rblk0];
           const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
@@ -365,7 +383,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
   const int grp = tid >> 3;
   const int leader = lane & 24;
   const unsigned gmask = 0xFFu << leader;  // this 8-lane group only
+  const double2 *__restrict__ z_in = a.z_in;
   int k = 0;
+  int rot = 0;  // rows of the CTA's earlier tiles, mod NGROUPS (rotating row assignment)
   uint32_t win_par = 0;
   for (int s = segA; s < segB; ++s) {
     const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
@@ -376,38 +396,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
         fence_proxy_async_smem();  // prior generic reads of zs before the async overwrite
         const uint32_t bytes = (uint32_t)((w1 - w0) * sizeof(double2));
         mbar_expect_tx(&bar_win, bytes);
-        bulk_g2s(zs, a.z_in + w0, bytes, &bar_win);
+        bulk_g2s(zs, z_in + w0, bytes, &bar_win);
       }
       mbar_wait(&bar_win, win_par);
       win_par ^= 1;
       for (int ti = g.seg_tile[s]; ti < g.seg_tile[s + 1]; ++ti, ++k) {
-        const int b = k & 1;
-        mbar_wait(&bar_full[b], (k >> 1) & 1);
-        const TileSlot &S = ring[b];
         const cdk_tile T = g.tiles[ti];
         const int64_t r0 = g.rblk_row0[T.rblk0];
         const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
         const int nrow = (int)(r1 - r0);
+        int r = grp - rot;
+        if (r < 0) r += NGROUPS;
+        rot += nrow;
+        rot %= NGROUPS;
+        if (r >= nrow) continue;  // no row of this tile for this group
+        const int b = k % RING, n = k / RING;
+        while (s_slot_tag[b] != k) __nanosleep(32);
+        mbar_wait(&bar_full[b], n & 1);
+        while (s_acc_owner[b] != k) __nanosleep(32);
+        __threadfence_block();
+        const TileSlot &S = ring[b];
         const int half = (nrow + 1 + 3) & ~3;
         const int nrb = T.rblk1 - T.rblk0;
         double2 *acc = accs + b * TILE_ROWS;
         int *cnt = cnt_rb + b * CNT_STRIDE;
-        while (true) {
-          int r = 0;
-          if (t == 0) r = atomicAdd(&s_next[b], 1);
-          r = __shfl_sync(gmask, r, leader);
-          if (r >= nrow) break;
+        for (; r < nrow; r += NGROUPS) {
           const int ie0 = S.tab[r], ie1 = S.tab[r + 1];
           const int xe0 = S.tab[half + r], xe1 = S.tab[half + r + 1];
+          const int lrb = S.tab[2 * half + r];
+          DBG_CHECK(ie0 >= 0 && ie0 <= ie1 && ie1 <= T.ne && xe0 >= 0 && xe0 <= xe1 &&
+                        xe1 <= T.nxa && lrb >= 0 && lrb < nrb,
+                    "tab r=%d nrow=%d ie %d %d xe %d %d lrb %d k=%d ti=%d", r, nrow, ie0, ie1, xe0,
+                    xe1, lrb, k, ti);
           const int32_t j = (xe0 + t < xe1) ? S.xcol[xe0 + t] : -1;
-          const double2 zx = (j >= 0) ? ldg(a.z_in + j) : make_double2(0.0, 0.0);
+          DBG_CHECK(j < (int32_t)g.n_rows, "inter col %d r=%d k=%d ti=%d", j, r, k, ti);
+          const double2 zx = (j >= 0) ? ldg(z_in + j) : make_double2(0.0, 0.0);
           double sr = 0.0, si = 0.0;
           for (int p = ie0 + 8 * t; p < ie1; p += 64)
             gather8<true>(*reinterpret_cast<const uint4 *>(S.cols + p), zs, zero_slot, sr, si);
           sr += zx.x;
           si += zx.y;
           for (int p = xe0 + 8 + t; p < xe1; p += 8) {
-            const double2 z = ldg(a.z_in + S.xcol[p]);
+            const double2 z = ldg(z_in + S.xcol[p]);
             sr += z.x;
             si += z.y;
           }
@@ -416,38 +446,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
             sr += __shfl_xor_sync(gmask, sr, o);
             si += __shfl_xor_sync(gmask, si, o);
           }
-          int last = 0, lrb = 0;
+          int last = 0;
           if (t == 0) {
             acc[r] = make_double2(sr, si);
             __threadfence_block();
-            lrb = S.tab[2 * half + r];
             const int rb = T.rblk0 + lrb;
             const int64_t e = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
             last = (atomicAdd(&cnt[lrb], 1) + 1 == (int)(e - g.rblk_row0[rb]));
+            DBG_CHECK(cnt[lrb] <= 32, "rblock counter overflow %d", cnt[lrb]);
+            if (atomicAdd(&s_rows_done[b], 1) + 1 == nrow) {  // slot data fully consumed
+              s_rows_done[b] = 0;
+              mbar_arrive(&bar_empty[b]);
+            }
           }
           last = __shfl_sync(gmask, last, leader);
           if (last) {
-            lrb = __shfl_sync(gmask, lrb, leader);
             __threadfence_block();
             epilogue_group<MODE>(a, T.rblk0 + lrb, t, gmask, acc, r0, true, zs, w0);
-            if (t == 0 && atomicAdd(&s_rbdone[b], 1) + 1 == nrb) mbar_arrive(&bar_empty[b]);
+            if (t == 0 && atomicAdd(&s_rb_done[b], 1) + 1 == nrb) {  // accumulators free
+              for (int i = 0; i < nrb; ++i) cnt[i] = 0;
+              s_rb_done[b] = 0;
+              __threadfence_block();
+              s_acc_owner[b] = k + RING;
+            }
           }
         }
-        if (t == 0) mbar_arrive(&bar_empty[b]);  // this group is done with the tile
       }
     } else {
       const int64_t row0 = g.rblk_row0[rbA];
       const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
       const int nrows = (int)(row1 - row0);
-      const double2 *zbase = a.z_in + g.seg_base[s];
-      double2 *acc = accs;  // ring slots are idle on this path only after a barrier
-      consumer_bar();
+      const double2 *zbase = z_in + g.seg_base[s];
+      double2 *acc = accs;  // all staged tiles' epilogues finished (segment barrier)
       for (int r = grp; r < nrows; r += 2 * NGROUPS) {
         const int rB = r + NGROUPS;
         const bool hasB = rB < nrows;
         double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-        gather_rows_global(g, a.z_in, zbase, row0 + r, row0 + (hasB ? rB : r), hasB, t, ar, ai,
-                           br, bi);
+        gather_rows_global(g, z_in, zbase, row0 + r, row0 + (hasB ? rB : r), hasB, t, ar, ai, br,
+                           bi);
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) {
           ar += __shfl_xor_sync(gmask, ar, o);
@@ -540,7 +576,7 @@ static int check_graph(const cdk_graph *g) {
 }
 
 static size_t stage_smem(const cdk_graph *g) {
-  return RING * sizeof(TileSlot) + RING * TILE_ROWS * sizeof(double2) +
+  return RING * sizeof(TileSlot) + (size_t)RING * TILE_ROWS * sizeof(double2) +
          RING * CNT_STRIDE * sizeof(int) + ((size_t)g->smem_nodes + 8) * sizeof(double2);
 }
 

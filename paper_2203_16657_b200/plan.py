@@ -98,8 +98,8 @@ def _row_runs(rows_sorted: np.ndarray, n_rows: int):
 
 # rblocks: <= 32 rows of one community and at most RB_MAX_E padded intra /
 # RB_MAX_X inter entries, so every rblock fits one shared-memory tile
-RB_MAX_E = 8192
-RB_MAX_X = 1024
+RB_MAX_E = 8192  # == TILE_E
+RB_MAX_X = 1016  # aligned span <= RB_MAX_X + 6 <= TILE_X
 
 
 def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
@@ -187,11 +187,11 @@ def build_layout(dec: Decomposition) -> HostLayout:
 WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
 
 # shared-memory tile ring of the TMA pipeline (must match csrc/kuramoto.cu)
-TILE_ROWS = 256
-TILE_E = 16384  # uint16 intra columns per tile
-TILE_X = 2048  # int32 inter columns per tile (incl. 16-byte alignment slack)
+TILE_ROWS = 128
+TILE_E = 8192  # uint16 intra columns per tile
+TILE_X = 1024  # int32 inter columns per tile (incl. 16-byte alignment slack)
 TILE_TAB = 2 * (TILE_ROWS + 4) + TILE_ROWS  # int32 offset table per tile
-RING = 2
+RING = 4
 CTA_THREADS = 1024
 TILE_DTYPE = np.dtype([("e0", np.int64), ("x0a", np.int64), ("tab_off", np.int64),
                        ("ne", np.int32), ("nxa", np.int32), ("rblk0", np.int32),
@@ -204,8 +204,8 @@ def ring_bytes() -> int:
 
 def stage_smem_bytes(smem_nodes: int) -> int:
     """dynamic shared memory of the stage kernel: window (+8 spare slots),
-    double-buffered row accumulators, tile ring"""
-    return (16 * (smem_nodes + 8) + 2 * 16 * TILE_ROWS + ring_bytes()
+    per-slot row accumulators, tile ring, per-slot rblock counters"""
+    return (16 * (smem_nodes + 8) + RING * 16 * TILE_ROWS + ring_bytes()
             + 4 * RING * (TILE_ROWS + 4))  # per-slot rblock counters
 
 
