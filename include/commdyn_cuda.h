@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 3
+#define CDK_ABI_VERSION 4
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -86,51 +86,37 @@ CDK_API int cdk_dense_poly(const double *x, const int64_t *offsets, int64_t m_co
 /* Fused CIA path: Kuramoto RHS (E1 + E2) inside RK4 stages.                */
 /* ------------------------------------------------------------------------ */
 
-/* One tile of a staged segment: whole rblocks whose CSR slices are streamed
- * into a shared-memory ring slot by bulk async copies (TMA engine). */
-typedef struct cdk_tile {
-  int64_t e0;      /* first intra entry (multiple of 8) */
-  int64_t x0a;     /* first inter entry, rounded down to a multiple of 4 */
-  int64_t tab_off; /* offset of this tile's table in tile_tab (multiple of 4) */
-  int32_t ne;      /* intra entries (multiple of 8) */
-  int32_t nxa;     /* inter entries from x0a (multiple of 4) */
-  int32_t rblk0;   /* rblock range [rblk0, rblk1) */
-  int32_t rblk1;
-} cdk_tile;
-
 /* Device form of a Decomposition as a directed CSR without
  * the diagonal, rows in permuted (community-contiguous) order, plus the
  * static work schedule built by the host planner (paper_2203_16657_b200/plan.py).
  *   rows [comm_off[c], comm_off[c+1]) form community c; rows >= comm_off[M]
  *   are the NONE pool (sparse contributions only, SPEC.md evaluator:205).
  *   intra entries (sign -1): uint16 column RELATIVE TO THE ROW'S SEGMENT BASE
- *   (seg_base), each row's run padded to a multiple of 8 with CDK_INTRA_PAD;
- *   inter entries (sign +1, also every entry of a NONE-pool row): global
- *   column (int32).
- *   rblock  = <= 32 consecutive rows of one community (or of the pool), at
- *             most 8192 intra / 1024 inter entries;
- *   segment = a run of whole rblocks owned by one CTA whose intra neighbours
- *             all lie in the node window seg_win[2s]..seg_win[2s+1] (staged in
- *             shared memory by one bulk async copy) or, for a community larger
- *             than the window capacity, in global memory (w0 == w1; such a
- *             segment has <= seg_rows_cap rows and no tiles);
- *   tile    = see cdk_tile; tile_tab holds per tile the int32 offsets
- *             intra_ptr[r] - e0 for its rows r0..r1, padded to a multiple of
- *             4, followed by inter_ptr[r] - x0a, padded likewise. */
+ *   (seg_base), each row's run padded to a multiple of 8 with CDK_INTRA_PAD
+ *   and ordered by cdk_host_bank_order; inter entries (sign +1, also every
+ *   entry of a NONE-pool row): global column (int32).
+ *   rblock  = <= 32 consecutive rows of one community (or of the pool);
+ *   segment = a run of whole rblocks owned by one CTA, <= seg_rows_cap rows,
+ *             whose intra neighbours all lie in the node window
+ *             seg_win[2s]..seg_win[2s+1] (staged in shared memory by one bulk
+ *             async copy) or, for a community larger than the window
+ *             capacity (and the NONE pool), in global memory (w0 == w1).
+ * Padding contract (bulk copies move 16-byte units): intra_ptr / inter_ptr
+ * readable up to index n_rows + 3, theta / omega up to n_rows + 1. */
 typedef struct cdk_graph {
   int64_t n_rows;
   int64_t n_comm;
   const int64_t *comm_off;      /* [n_comm+1] */
-  const int64_t *intra_ptr;     /* [n_rows+1], multiples of 8 */
+  const int64_t *intra_ptr;     /* [n_rows+1 (+3 pad)], multiples of 8 */
   const uint16_t *intra_col;    /* [intra_ptr[n_rows]] */
-  const int64_t *inter_ptr;     /* [n_rows+1] */
-  const int32_t *inter_col;     /* [inter_ptr[n_rows]] (+3 readable slack) */
+  const int64_t *inter_ptr;     /* [n_rows+1 (+3 pad)] */
+  const int32_t *inter_col;     /* [inter_ptr[n_rows]] */
   int32_t n_rblk;
   int32_t n_seg;
   int32_t n_cta;
   int32_t cta_threads;          /* 1024 */
-  int32_t smem_nodes;           /* window capacity (nodes) of the shared-memory stage */
-  int32_t seg_rows_cap;         /* max rows per unstaged segment */
+  int32_t smem_nodes;           /* window capacity (nodes, multiple of 8) */
+  int32_t seg_rows_cap;         /* max rows per segment (multiple of 8) */
   const int64_t *rblk_row0;     /* [n_rblk] */
   const int32_t *rblk_comm;     /* [n_rblk], -1 = NONE pool */
   const int32_t *comm_rblk_off; /* [n_comm+1] */
@@ -138,10 +124,6 @@ typedef struct cdk_graph {
   const int64_t *seg_win;       /* [2*n_seg] staged node window [w0, w1) */
   const int64_t *seg_base;      /* [n_seg] base of the segment's intra columns */
   const int32_t *cta_seg;       /* [n_cta+1] segment boundaries per CTA */
-  const int32_t *seg_tile;      /* [n_seg+1] tile range per segment */
-  const cdk_tile *tiles;        /* [n_tile] */
-  const int32_t *tile_tab;      /* per-tile offset tables */
-  int64_t n_tile;
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */
@@ -161,7 +143,8 @@ CDK_API int cdk_kuramoto_prepare(const cdk_graph *g, const double *theta, void *
 
 /* One CIA right-hand side (eval_rhs_cia + kuramoto_rhs):
  *   out[i] = omega[i] + k_over_n * Im( (R_c(i) + sum_j s_ij z_j) * conj(z_i) )
- * with k_over_n = K / N (h = K sin, global 1/N).  Runs prepare internally. */
+ * with k_over_n = K / N (h = K sin, global 1/N).  Runs prepare internally.
+ * theta / omega: see the padding contract of cdk_graph. */
 CDK_API int cdk_kuramoto_rhs(const cdk_graph *g, const double *theta, const double *omega,
                      double k_over_n, double *out, void *workspace, void *stream);
 
@@ -186,6 +169,16 @@ CDK_API int cdk_kuramoto_euler(const cdk_graph *g, double *theta, const double *
 /* copy the workspace's run status to [host] *out (synchronises `stream`). */
 CDK_API int cdk_kuramoto_status(const cdk_graph *g, const void *workspace, cdk_run_status *out,
                         void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* host-side planning (no device needed)                                    */
+/* ------------------------------------------------------------------------ */
+
+/* [host] reorder each row's intra run (ptr[r]..ptr[r+1], multiples of 8) so
+ * the 16-byte shared-memory gathers of one 8-lane row group hit distinct bank
+ * groups (column mod 8); pads (pad_value) count as bank pad_bank. */
+CDK_API int cdk_host_bank_order(uint16_t *cols, const int64_t *ptr, int64_t n_rows,
+                                int32_t pad_value, int32_t pad_bank);
 
 /* ------------------------------------------------------------------------ */
 /* misc                                                                      */

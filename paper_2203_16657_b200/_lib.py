@@ -44,10 +44,6 @@ class CdkGraph(ctypes.Structure):
         ("seg_win", P),
         ("seg_base", P),
         ("cta_seg", P),
-        ("seg_tile", P),
-        ("tiles", P),
-        ("tile_tab", P),
-        ("n_tile", I64),
     ]
 
 
@@ -72,6 +68,7 @@ _SIGS = {
     "cdk_kuramoto_rk4_stage": [ctypes.POINTER(CdkGraph), P, P, D, D, I, P, P],
     "cdk_kuramoto_euler": [ctypes.POINTER(CdkGraph), P, P, D, D, I64, P, P],
     "cdk_kuramoto_status": [ctypes.POINTER(CdkGraph), P, ctypes.POINTER(CdkRunStatus), P],
+    "cdk_host_bank_order": [P, P, I64, I32, I32],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],
@@ -84,7 +81,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _lock = threading.Lock()
 _lib = None

@@ -1,0 +1,52 @@
+// Host-side planning helpers (native, O(nnz)) exported through the C ABI.
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/commdyn_cuda.h"
+
+// Reorder every row's intra run so that the 16-byte shared-memory gathers one
+// 8-lane row group issues together (lane t reads entries 8t..8t+7 of each
+// 64-entry block; instruction k touches entry 8t+k of every lane, i.e. one
+// quarter-warp phase per (block, k)) hit distinct bank groups (column mod 8).
+// Entries are counting-sorted by bank group and dealt round-robin over the
+// row's phases, so equal bank groups land in different phases.  The sum a row
+// produces is unchanged up to floating-point reassociation; the order is a
+// deterministic function of the row.
+extern "C" CDK_API int cdk_host_bank_order(uint16_t *cols, const int64_t *ptr, int64_t n_rows,
+                                           int32_t pad_value, int32_t pad_bank) {
+  if (!cols || !ptr || n_rows < 0) return CDK_INPUT;
+  std::vector<uint16_t> vals, out;
+  std::vector<int> cap, fill;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    const int64_t a = ptr[r], b = ptr[r + 1];
+    const int64_t L = b - a;
+    if (L <= 8) continue;  // a single lane-chunk: one entry per phase already
+    if (L % 8) return CDK_INPUT;
+    vals.assign(cols + a, cols + b);
+    // counting sort by bank group (pads carry the zero slot's bank)
+    int cnt[9] = {0};
+    for (uint16_t v : vals) cnt[(v == pad_value ? pad_bank : (v & 7)) + 1]++;
+    for (int i = 0; i < 8; ++i) cnt[i + 1] += cnt[i];
+    out.resize(L);
+    for (uint16_t v : vals) out[cnt[v == pad_value ? pad_bank : (v & 7)]++] = v;
+    // phases: block m (64 entries), instruction k -> lanes t < T_m
+    const int64_t nblk = (L + 63) / 64;
+    const int64_t P = 8 * nblk;
+    cap.assign(P, 0);
+    fill.assign(P, 0);
+    for (int64_t m = 0; m < nblk; ++m) {
+      const int64_t Lm = std::min<int64_t>(64, L - 64 * m);
+      for (int k = 0; k < 8; ++k) cap[8 * m + k] = (int)(Lm / 8);
+    }
+    int64_t j = 0;
+    for (int64_t s = 0; s < L; ++s) {
+      while (fill[j] == cap[j]) j = (j + 1) % P;
+      const int64_t m = j / 8, k = j % 8, t = fill[j]++;
+      cols[a + 64 * m + 8 * t + k] = out[s];
+      j = (j + 1) % P;
+    }
+  }
+  return CDK_OK;
+}

@@ -62,7 +62,7 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
   // +16: staged windows are rounded out to 8-node (128-byte) boundaries
   w.z[0] = (double2 *)take((n + 16) * sizeof(double2));
   w.z[1] = (double2 *)take((n + 16) * sizeof(double2));
-  w.ksum = (double *)take(n * sizeof(double));
+  w.ksum = (double *)take((n + 4) * sizeof(double));  // bulk copies read 16-byte units
   w.R[0] = (double2 *)take((m + 1) * sizeof(double2));
   w.R[1] = (double2 *)take((m + 1) * sizeof(double2));
   w.part = (double2 *)take(((size_t)g->n_rblk + 1) * sizeof(double2));
@@ -165,342 +165,249 @@ __device__ __forceinline__ void gather8(const uint4 w, const double2 *__restrict
   }
 }
 
-// sparse sums of two rows (A, B) of an unstaged segment (global gathers)
-__device__ __forceinline__ void gather_rows_global(const cdk_graph &g,
-                                                   const double2 *__restrict__ z_in,
-                                                   const double2 *__restrict__ zbase, int64_t iA,
-                                                   int64_t iB, bool hasB, int t, double &ar,
-                                                   double &ai, double &br, double &bi) {
-  const int64_t eA0 = ldg(g.intra_ptr + iA), eA1 = ldg(g.intra_ptr + iA + 1);
-  const int64_t xA0 = ldg(g.inter_ptr + iA), xA1 = ldg(g.inter_ptr + iA + 1);
-  const int64_t eB0 = ldg(g.intra_ptr + iB);
-  const int64_t eB1 = hasB ? ldg(g.intra_ptr + iB + 1) : eB0;
-  const int64_t xB0 = ldg(g.inter_ptr + iB);
-  const int64_t xB1 = hasB ? ldg(g.inter_ptr + iB + 1) : xB0;
-  const uint4 *colv = reinterpret_cast<const uint4 *>(g.intra_col);
-  for (int64_t p = eA0 + 8 * t; p < eA1; p += 64)
-    gather8<false>(ldg(colv + (p >> 3)), zbase, 0, ar, ai);
-  for (int64_t p = eB0 + 8 * t; p < eB1; p += 64)
-    gather8<false>(ldg(colv + (p >> 3)), zbase, 0, br, bi);
-  for (int64_t p = xA0 + t; p < xA1; p += 8) {
-    const double2 z = ldg(z_in + ldg(g.inter_col + p));
-    ar += z.x;
-    ai += z.y;
-  }
-  for (int64_t p = xB0 + t; p < xB1; p += 8) {
-    const double2 z = ldg(z_in + ldg(g.inter_col + p));
-    br += z.x;
-    bi += z.y;
-  }
-}
-
 // ---------------------------------------------------------------------------
-// TMA-pipelined, barrier-free stage kernel.  One CTA per SM, 32 warps:
-//   warp 31 (one lane) = producer: streams each tile's CSR slices (uint16
-//     intra columns, int32 inter columns, int32 row table) into a 2-slot
-//     shared-memory ring with bulk async copies (full/empty mbarriers);
-//   warps 0..30 = 124 consumer groups of 8 lanes.  Per segment, one bulk copy
-//     stages the node window of z_in in shared memory.  Per tile, groups claim
-//     rows from a shared counter (dynamic balance, no CTA barrier), gather
-//     the row from the window, store the row sum, and count the row into its
-//     rblock; the group that completes an rblock runs its epilogue (RK4 stage
-//     update, sincos, canonical rblock partial, community completion).  The
-//     slot is refilled once every group has left the tile and the tile's last
-//     epilogue is done (empty barrier expects NGROUPS + 1 arrivals).
-// Unstaged segments (communities above the window capacity, NONE pool) are
-// processed from global memory with CTA barriers (rare path).
-// All reductions have a fixed shape => bitwise deterministic and independent
-// of the schedule (and so of the GPU count).
+// Stage kernel.  One CTA (1024 threads = 128 groups of 8 lanes) per SM,
+// persistent over its cost-balanced segments.  Per segment:
+//  1. one thread issues bulk async copies (TMA engine) of the segment's node
+//     window of z_in, its row-pointer slices and the epilogue inputs (theta,
+//     omega, ksum) into shared memory, all completing on one mbarrier;
+//  2. gather: groups claim rows from a shared counter (dynamic balance); each
+//     lane streams 16-byte chunks (8 uint16 columns) of the row's intra run
+//     with the next row's chunks already in flight (1-row-ahead prefetch) and
+//     gathers z from the window (bank-conflict-free entry order, host-side);
+//     inter entries gather z from global memory (L2); the group reduces (fixed
+//     butterfly) into a shared row accumulator;
+//  3. epilogue (after a CTA barrier): warps take rblocks, lane = row:
+//     k = omega + K/N Im((R_c + acc) conj z), RK4 stage update, z_next =
+//     exp(i theta_next), canonical rblock partial; the warp that completes a
+//     community's last rblock reduces R_next[c].
+// Communities above the window capacity (and the NONE pool) gather intra
+// neighbours from global memory; everything else is identical.
 // ---------------------------------------------------------------------------
-constexpr int TILE_ROWS = 128;
-constexpr int TILE_E = 8192;
-constexpr int TILE_X = 1024;
-constexpr int TILE_TAB = 2 * (TILE_ROWS + 4) + TILE_ROWS;
-constexpr int RING = 4;
 constexpr int NTHREADS = 1024;
-constexpr int NCONS_WARPS = 31;
-constexpr int NCONS = NCONS_WARPS * 32;
-constexpr int NGROUPS = NCONS / 8;
-constexpr int CNT_STRIDE = TILE_ROWS + 4;
+constexpr int NWARPS = NTHREADS / 32;
+constexpr int NGROUPS = NTHREADS / 8;
 
-struct TileSlot {
-  uint16_t cols[TILE_E];
-  int32_t xcol[TILE_X];
-  int32_t tab[TILE_TAB];
+struct SegSmem {  // carve-up of dynamic shared memory (all 16-byte aligned)
+  double2 *acc;     // [cap4]   row sums, index i - row0
+  int64_t *sip;     // [cap4]   intra_ptr[row0a ..]
+  int64_t *sxp;     // [cap4]   inter_ptr[row0a ..]
+  double *sth;      // [cap4]   theta[row0a ..]
+  double *som;      // [cap4]   omega[row0a ..]
+  double *sks;      // [cap4]   ksum[row0a ..]
+  double2 *zs;      // [smem_nodes + 8] window + zero slot
 };
-static_assert(sizeof(TileSlot) % 16 == 0, "tile slot must keep 16-byte alignment");
 
-__device__ __forceinline__ void consumer_bar() {
-  asm volatile("bar.sync 1, %0;" ::"r"(NCONS) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__host__ __device__ inline size_t cap4_of(int cap) { return (size_t)cap + 4; }
+
+__host__ __device__ inline size_t stage_smem_bytes(int cap, int smem_nodes) {
+  return cap4_of(cap) * (16 + 5 * 8) + ((size_t)smem_nodes + 8) * 16;
 }
 
-// Epilogue of one rblock by an 8-lane group: lane t owns rows t, t+8, t+16,
-// t+24 of the rblock.  Canonical rblock partial: per-lane sum in row order,
-// then the 8-lane butterfly.  The group that completes community c reduces R.
-template <int MODE>
-__device__ __forceinline__ void epilogue_group(const StageArgs &a, int rb, int t, unsigned gmask,
-                                               const double2 *acc, int64_t accrow0, bool staged,
-                                               const double2 *zs, int64_t w0) {
-  const cdk_graph &g = a.g;
-  const int64_t rrow0 = g.rblk_row0[rb];
-  const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
-  const int nr = (int)(rrow1 - rrow0);
-  const int c = g.rblk_comm[rb];
-  const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
-  const double kn = a.k_over_n;
-  double pr = 0.0, pim = 0.0;
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const int l = t + 8 * m;
-    if (l < nr) {
-      const int64_t i = rrow0 + l;
-      const double2 ac = acc[i - accrow0];
-      const double2 zi = staged ? zs[i - w0] : ldg(a.z_in + i);
-      double k = ldg(a.omega + i) + kn * (R.y * zi.x - R.x * zi.y);
-      k = k + kn * (ac.y * zi.x - ac.x * zi.y);
-      if (MODE == 0) {
-        a.out[i] = k;
-      } else {
-        const double th0 = a.theta[i];
-        double thn;
-        if (MODE == 1) {
-          a.ksum[i] = k;
-          thn = add_rn(th0, mul_rn(a.h, k));
-        } else if (MODE == 2 || MODE == 3) {
-          a.ksum[i] = add_rn(a.ksum[i], mul_rn(2.0, k));
-          thn = add_rn(th0, mul_rn(a.h, k));
-        } else {  // MODE 4: x + dt/6 (k1 + 2k2 + 2k3 + k4); MODE 5: Euler x + dt k
-          const double ks = (MODE == 4) ? add_rn(a.ksum[i], k) : k;
-          thn = wrap_phase(add_rn(th0, mul_rn(a.h, ks)));
-          a.theta[i] = thn;
-          if (!isfinite(thn)) {
-            atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->nonfinite), 1ull);
-            atomicMin(reinterpret_cast<long long *>(&a.status->first_bad_step),
-                      (long long)(a.status->steps_done + a.step_rel + 1));
-          }
-        }
-        double sn, cs;
-        sincos(thn, &sn, &cs);
-        a.z_out[i] = make_double2(cs, sn);
-        pr += cs;
-        pim += sn;
-      }
-    }
-  }
-  if (MODE != 0 && c >= 0) {
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      pr += __shfl_xor_sync(gmask, pr, o);
-      pim += __shfl_xor_sync(gmask, pim, o);
-    }
-    const int leader = (threadIdx.x & 31) & 24;
-    int last = 0;
-    if (t == 0) {
-      a.part[rb] = make_double2(pr, pim);
-      __threadfence();
-      const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
-      last = (atomicAdd(a.cnt + c, 1) + 1 == total);
-    }
-    last = __shfl_sync(gmask, last, leader);
-    if (last) {  // this group finished community c: reduce its partials
-      __threadfence();
-      const double2 Rn =
-          reduce_comm8(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], t, gmask);
-      if (t == 0) {
-        a.R_out[c] = Rn;
-        a.cnt[c] = 0;
-      }
-    }
-  }
+__device__ __forceinline__ SegSmem carve_smem(unsigned char *base, int cap, int smem_nodes) {
+  SegSmem m;
+  const size_t c4 = cap4_of(cap);
+  m.acc = reinterpret_cast<double2 *>(base);
+  m.sip = reinterpret_cast<int64_t *>(m.acc + c4);
+  m.sxp = m.sip + c4;
+  m.sth = reinterpret_cast<double *>(m.sxp + c4);
+  m.som = m.sth + c4;
+  m.sks = m.som + c4;
+  m.zs = reinterpret_cast<double2 *>(m.sks + c4);
+  return m;
 }
 
-// MODE 0: out = f(theta) (single RHS).  MODE 1..4: RK4 stage.  MODE 5: Euler step.
+struct RowLoads {
+  int64_t e1, x0, x1;
+  int64_t p;  // first chunk position of this lane
+  uint4 c0, c1;
+  int32_t j;
+};
+
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // full: tile data landed (TMA tx); empty: all rows of the tile gathered
-  // (slot reusable).  A group only waits for tiles it has rows in, so it may
-  // skip fills: s_slot_tag[b] names the tile currently filling/filled in slot
-  // b (set by the producer before the copies) and is checked before the
-  // parity wait; s_acc_owner[b] names the tile allowed to use accumulator
-  // slot b (advanced by the tile's last epilogue).
-  __shared__ __align__(8) uint64_t bar_full[RING], bar_empty[RING], bar_win;
-  __shared__ int s_rows_done[RING], s_rb_done[RING];
-  __shared__ volatile int s_slot_tag[RING], s_acc_owner[RING];
+  __shared__ __align__(8) uint64_t bar_seg;
+  __shared__ int s_claim;
   const cdk_graph &g = a.g;
-  TileSlot *ring = reinterpret_cast<TileSlot *>(smem_raw);
-  double2 *accs = reinterpret_cast<double2 *>(smem_raw + RING * sizeof(TileSlot));
-  int *cnt_rb = reinterpret_cast<int *>(accs + RING * TILE_ROWS);
-  double2 *zs = reinterpret_cast<double2 *>(cnt_rb + RING * CNT_STRIDE);
+  const SegSmem sm = carve_smem(smem_raw, g.seg_rows_cap, g.smem_nodes);
   const uint32_t zero_slot = (uint32_t)g.smem_nodes;  // zs[smem_nodes] == 0
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
-  for (int i = tid; i < RING * CNT_STRIDE; i += NTHREADS) cnt_rb[i] = 0;
-  if (tid == 0) {
-    for (int b = 0; b < RING; ++b) {
-      mbar_init(&bar_full[b], 1);
-      mbar_init(&bar_empty[b], 1);
-      s_rows_done[b] = 0;
-      s_rb_done[b] = 0;
-      s_slot_tag[b] = -1;
-      s_acc_owner[b] = b;
-    }
-    mbar_init(&bar_win, 1);
-    zs[zero_slot] = make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-
-  if (warp == NCONS_WARPS) {  // ---------------- producer ----------------
-    if (lane == 0) {
-      int k = 0;
-      for (int s = segA; s < segB; ++s) {
-        for (int ti = g.seg_tile[s]; ti < g.seg_tile[s + 1]; ++ti, ++k) {
-          const int b = k % RING, n = k / RING;
-          if (n > 0) mbar_wait(&bar_empty[b], (n - 1) & 1);
-          s_slot_tag[b] = k;
-          const cdk_tile T = g.tiles[ti];
-          const int64_t r0 = g.rblk_row0[T.rblk0];
-          const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
-          const int nrow = (int)(r1 - r0);
-          const int half = (nrow + 1 + 3) & ~3;
-          const uint32_t be = (uint32_t)T.ne * 2u, bx = (uint32_t)T.nxa * 4u,
-                         bt = (uint32_t)(2 * half + ((nrow + 3) & ~3)) * 4u;
-          mbar_expect_tx(&bar_full[b], be + bx + bt);
-          if (be) bulk_g2s(ring[b].cols, g.intra_col + T.e0, be, &bar_full[b]);
-          if (bx) bulk_g2s(ring[b].xcol, g.inter_col + T.x0a, bx, &bar_full[b]);
-          bulk_g2s(ring[b].tab, g.tile_tab + T.tab_off, bt, &bar_full[b]);
-        }
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers (warps 0..30) ----------------
   const int t = lane & 7;
-  const int grp = tid >> 3;
   const int leader = lane & 24;
   const unsigned gmask = 0xFFu << leader;  // this 8-lane group only
+  const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
   const double2 *__restrict__ z_in = a.z_in;
-  int k = 0;
-  int rot = 0;  // rows of the CTA's earlier tiles, mod NGROUPS (rotating row assignment)
-  uint32_t win_par = 0;
+  const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col);
+  const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
+  if (tid == 0) {
+    mbar_init(&bar_seg, 1);
+    sm.zs[zero_slot] = make_double2(0.0, 0.0);
+    s_claim = 0;
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+
   for (int s = segA; s < segB; ++s) {
     const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
+    const int64_t row0 = g.rblk_row0[rbA];
+    const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
+    const int64_t row0a = row0 & ~(int64_t)1;
     const int64_t w0 = g.seg_win[2 * s], w1 = g.seg_win[2 * s + 1];
     const bool staged = w1 > w0;
-    if (staged) {
-      if (tid == 0) {
-        fence_proxy_async_smem();  // prior generic reads of zs before the async overwrite
-        const uint32_t bytes = (uint32_t)((w1 - w0) * sizeof(double2));
-        mbar_expect_tx(&bar_win, bytes);
-        bulk_g2s(zs, z_in + w0, bytes, &bar_win);
+    const int nrows = (int)(row1 - row0);
+
+    // ---- 1. stage window, pointer slices, epilogue inputs ------------------
+    if (tid == 0) {
+      fence_proxy_async_smem();  // earlier generic accesses before the async overwrite
+      const uint32_t bw = staged ? (uint32_t)((w1 - w0) * 16) : 0u;
+      const uint32_t bp = (uint32_t)((((row1 + 2) & ~(int64_t)1) - row0a) * 8);
+      const uint32_t br = (uint32_t)((((row1 + 1) & ~(int64_t)1) - row0a) * 8);
+      const int nr_in = (MODE == 0 || MODE == 5 || MODE == 1) ? ((MODE == 0) ? 1 : 2) : 3;
+      mbar_expect_tx(&bar_seg, bw + 2 * bp + (uint32_t)nr_in * br);
+      if (bw) bulk_g2s(sm.zs, z_in + w0, bw, &bar_seg);
+      bulk_g2s(sm.sip, g.intra_ptr + row0a, bp, &bar_seg);
+      bulk_g2s(sm.sxp, g.inter_ptr + row0a, bp, &bar_seg);
+      bulk_g2s(sm.som, a.omega + row0a, br, &bar_seg);
+      if (MODE != 0) bulk_g2s(sm.sth, a.theta + row0a, br, &bar_seg);
+      if (MODE >= 2 && MODE <= 4) bulk_g2s(sm.sks, a.ksum + row0a, br, &bar_seg);
+    }
+    mbar_wait(&bar_seg, parity);
+    parity ^= 1;
+    const double2 *zwin = staged ? sm.zs : z_in + g.seg_base[s];
+
+    // ---- 2. gather: dynamic row claims, 1-row-ahead prefetch ---------------
+    auto claim = [&]() {
+      int r = 0;
+      if (t == 0) r = atomicAdd(&s_claim, 1);
+      return __shfl_sync(gmask, r, leader);
+    };
+    auto issue = [&](int r, RowLoads &L) {
+      if (r < nrows) {
+        const int64_t li = row0 + r - row0a;
+        const int64_t e0 = sm.sip[li];
+        L.e1 = sm.sip[li + 1];
+        L.x0 = sm.sxp[li];
+        L.x1 = sm.sxp[li + 1];
+        L.p = e0 + 8 * t;
+        L.c0 = (L.p < L.e1) ? ldg(colv + (L.p >> 3)) : padv;
+        L.c1 = (L.p + 64 < L.e1) ? ldg(colv + ((L.p + 64) >> 3)) : padv;
+        L.j = (L.x0 + t < L.x1) ? ldg(g.inter_col + L.x0 + t) : -1;
       }
-      mbar_wait(&bar_win, win_par);
-      win_par ^= 1;
-      for (int ti = g.seg_tile[s]; ti < g.seg_tile[s + 1]; ++ti, ++k) {
-        const cdk_tile T = g.tiles[ti];
-        const int64_t r0 = g.rblk_row0[T.rblk0];
-        const int64_t r1 = (T.rblk1 < g.n_rblk) ? g.rblk_row0[T.rblk1] : g.n_rows;
-        const int nrow = (int)(r1 - r0);
-        int r = grp - rot;
-        if (r < 0) r += NGROUPS;
-        rot += nrow;
-        rot %= NGROUPS;
-        if (r >= nrow) continue;  // no row of this tile for this group
-        const int b = k % RING, n = k / RING;
-        while (s_slot_tag[b] != k) __nanosleep(32);
-        mbar_wait(&bar_full[b], n & 1);
-        while (s_acc_owner[b] != k) __nanosleep(32);
-        __threadfence_block();
-        const TileSlot &S = ring[b];
-        const int half = (nrow + 1 + 3) & ~3;
-        const int nrb = T.rblk1 - T.rblk0;
-        double2 *acc = accs + b * TILE_ROWS;
-        int *cnt = cnt_rb + b * CNT_STRIDE;
-        for (; r < nrow; r += NGROUPS) {
-          const int ie0 = S.tab[r], ie1 = S.tab[r + 1];
-          const int xe0 = S.tab[half + r], xe1 = S.tab[half + r + 1];
-          const int lrb = S.tab[2 * half + r];
-          DBG_CHECK(ie0 >= 0 && ie0 <= ie1 && ie1 <= T.ne && xe0 >= 0 && xe0 <= xe1 &&
-                        xe1 <= T.nxa && lrb >= 0 && lrb < nrb,
-                    "tab r=%d nrow=%d ie %d %d xe %d %d lrb %d k=%d ti=%d", r, nrow, ie0, ie1, xe0,
-                    xe1, lrb, k, ti);
-          const int32_t j = (xe0 + t < xe1) ? S.xcol[xe0 + t] : -1;
-          DBG_CHECK(j < (int32_t)g.n_rows, "inter col %d r=%d k=%d ti=%d", j, r, k, ti);
-          const double2 zx = (j >= 0) ? ldg(z_in + j) : make_double2(0.0, 0.0);
-          double sr = 0.0, si = 0.0;
-          for (int p = ie0 + 8 * t; p < ie1; p += 64)
-            gather8<true>(*reinterpret_cast<const uint4 *>(S.cols + p), zs, zero_slot, sr, si);
-          sr += zx.x;
-          si += zx.y;
-          for (int p = xe0 + 8 + t; p < xe1; p += 8) {
-            const double2 z = ldg(z_in + S.xcol[p]);
-            sr += z.x;
-            si += z.y;
-          }
+    };
+    int r = claim();
+    RowLoads cur{}, nxt{};
+    issue(r, cur);
+    while (r < nrows) {
+      const int rn = claim();
+      issue(rn, nxt);
+      const double2 zx = (cur.j >= 0) ? ldg(z_in + cur.j) : make_double2(0.0, 0.0);
+      double sr = 0.0, si = 0.0;
+      if (staged) {
+        gather8<true>(cur.c0, zwin, zero_slot, sr, si);
+        gather8<true>(cur.c1, zwin, zero_slot, sr, si);
+        for (int64_t p = cur.p + 128; p < cur.e1; p += 64)
+          gather8<true>(ldg(colv + (p >> 3)), zwin, zero_slot, sr, si);
+      } else {
+        gather8<false>(cur.c0, zwin, 0, sr, si);
+        gather8<false>(cur.c1, zwin, 0, sr, si);
+        for (int64_t p = cur.p + 128; p < cur.e1; p += 64)
+          gather8<false>(ldg(colv + (p >> 3)), zwin, 0, sr, si);
+      }
+      sr += zx.x;
+      si += zx.y;
+      for (int64_t p = cur.x0 + 8 + t; p < cur.x1; p += 8) {
+        const double2 z = ldg(z_in + ldg(g.inter_col + p));
+        sr += z.x;
+        si += z.y;
+      }
 #pragma unroll
-          for (int o = 4; o > 0; o >>= 1) {
-            sr += __shfl_xor_sync(gmask, sr, o);
-            si += __shfl_xor_sync(gmask, si, o);
-          }
-          int last = 0;
-          if (t == 0) {
-            acc[r] = make_double2(sr, si);
-            __threadfence_block();
-            const int rb = T.rblk0 + lrb;
-            const int64_t e = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
-            last = (atomicAdd(&cnt[lrb], 1) + 1 == (int)(e - g.rblk_row0[rb]));
-            DBG_CHECK(cnt[lrb] <= 32, "rblock counter overflow %d", cnt[lrb]);
-            if (atomicAdd(&s_rows_done[b], 1) + 1 == nrow) {  // slot data fully consumed
-              s_rows_done[b] = 0;
-              mbar_arrive(&bar_empty[b]);
+      for (int o = 4; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(gmask, sr, o);
+        si += __shfl_xor_sync(gmask, si, o);
+      }
+      if (t == 0) sm.acc[r] = make_double2(sr, si);
+      r = rn;
+      cur = nxt;
+    }
+    __syncthreads();
+    if (tid == 0) s_claim = 0;  // next segment's claims start after the end barrier
+
+    // ---- 3. epilogue: warp per rblock, lane = row ---------------------------
+    const double kn = a.k_over_n;
+    for (int rb = rbA + warp; rb < rbB; rb += NWARPS) {
+      const int64_t rrow0 = g.rblk_row0[rb];
+      const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+      const int nr = (int)(rrow1 - rrow0);
+      const int c = g.rblk_comm[rb];
+      double zr = 0.0, zim = 0.0;
+      if (lane < nr) {
+        const int64_t i = rrow0 + lane;
+        const int64_t li = i - row0a;
+        const double2 ac = sm.acc[i - row0];
+        const double2 zi = staged ? sm.zs[i - w0] : ldg(z_in + i);
+        const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
+        double k = sm.som[li] + kn * (R.y * zi.x - R.x * zi.y);
+        k = k + kn * (ac.y * zi.x - ac.x * zi.y);
+        if (MODE == 0) {
+          a.out[i] = k;
+        } else {
+          const double th0 = sm.sth[li];
+          double thn;
+          if (MODE == 1) {
+            a.ksum[i] = k;
+            thn = add_rn(th0, mul_rn(a.h, k));
+          } else if (MODE == 2 || MODE == 3) {
+            a.ksum[i] = add_rn(sm.sks[li], mul_rn(2.0, k));
+            thn = add_rn(th0, mul_rn(a.h, k));
+          } else {  // MODE 4: x + dt/6 (k1 + 2k2 + 2k3 + k4); MODE 5: Euler x + dt k
+            const double ks = (MODE == 4) ? add_rn(sm.sks[li], k) : k;
+            thn = wrap_phase(add_rn(th0, mul_rn(a.h, ks)));
+            a.theta[i] = thn;
+            if (!isfinite(thn)) {
+              atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->nonfinite), 1ull);
+              atomicMin(reinterpret_cast<long long *>(&a.status->first_bad_step),
+                        (long long)(a.status->steps_done + a.step_rel + 1));
             }
           }
-          last = __shfl_sync(gmask, last, leader);
-          if (last) {
-            __threadfence_block();
-            epilogue_group<MODE>(a, T.rblk0 + lrb, t, gmask, acc, r0, true, zs, w0);
-            if (t == 0 && atomicAdd(&s_rb_done[b], 1) + 1 == nrb) {  // accumulators free
-              for (int i = 0; i < nrb; ++i) cnt[i] = 0;
-              s_rb_done[b] = 0;
-              __threadfence_block();
-              s_acc_owner[b] = k + RING;
-            }
-          }
+          sincos(thn, &zim, &zr);
+          a.z_out[i] = make_double2(zr, zim);
         }
       }
-    } else {
-      const int64_t row0 = g.rblk_row0[rbA];
-      const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
-      const int nrows = (int)(row1 - row0);
-      const double2 *zbase = z_in + g.seg_base[s];
-      double2 *acc = accs;  // all staged tiles' epilogues finished (segment barrier)
-      for (int r = grp; r < nrows; r += 2 * NGROUPS) {
-        const int rB = r + NGROUPS;
-        const bool hasB = rB < nrows;
-        double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-        gather_rows_global(g, z_in, zbase, row0 + r, row0 + (hasB ? rB : r), hasB, t, ar, ai, br,
-                           bi);
+      if (MODE != 0 && c >= 0) {
+        // canonical rblock partial: lane t < 8 sums rows t, t+8, t+16, t+24 in
+        // order (absent rows = +0), then the 8-lane xor butterfly
+        const double r8 = __shfl_down_sync(FULL, zr, 8), i8 = __shfl_down_sync(FULL, zim, 8);
+        const double r16 = __shfl_down_sync(FULL, zr, 16), i16 = __shfl_down_sync(FULL, zim, 16);
+        const double r24 = __shfl_down_sync(FULL, zr, 24), i24 = __shfl_down_sync(FULL, zim, 24);
+        double pr = ((zr + r8) + r16) + r24, pim = ((zim + i8) + i16) + i24;
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) {
-          ar += __shfl_xor_sync(gmask, ar, o);
-          ai += __shfl_xor_sync(gmask, ai, o);
-          br += __shfl_xor_sync(gmask, br, o);
-          bi += __shfl_xor_sync(gmask, bi, o);
+          pr += __shfl_xor_sync(FULL, pr, o);
+          pim += __shfl_xor_sync(FULL, pim, o);
         }
-        if (t == 0) {
-          acc[r] = make_double2(ar, ai);
-          if (hasB) acc[rB] = make_double2(br, bi);
+        int last = 0;
+        if (lane == 0) {
+          a.part[rb] = make_double2(pr, pim);
+          __threadfence();
+          const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
+          last = (atomicAdd(a.cnt + c, 1) + 1 == total);
+        }
+        last = __shfl_sync(FULL, last, 0);
+        if (last) {  // this warp finished community c: reduce its partials
+          __threadfence();
+          if (lane < 8) {
+            const double2 Rn =
+                reduce_comm8(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane, 0xFFu);
+            if (lane == 0) {
+              a.R_out[c] = Rn;
+              a.cnt[c] = 0;
+            }
+          }
         }
       }
-      consumer_bar();
-      for (int rb = rbA + grp; rb < rbB; rb += NGROUPS)
-        epilogue_group<MODE>(a, rb, t, gmask, acc, row0, false, zs, 0);
     }
-    consumer_bar();  // zs / accs reuse by the next segment
+    __syncthreads();  // shared segment buffers reused by the next segment
   }
 }
 
@@ -516,18 +423,18 @@ __global__ void __launch_bounds__(256) prepare_kernel(cdk_graph g, const double 
   const int64_t row0 = g.rblk_row0[rb];
   const int64_t row1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
   const int nr = (int)(row1 - row0);
-  double pr = 0.0, pim = 0.0;
+  double zr[4], zi[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
     const int l = t + 8 * m;
+    zr[m] = 0.0;
+    zi[m] = 0.0;
     if (l < nr) {
-      double sn, cs;
-      sincos(theta[row0 + l], &sn, &cs);
-      z[row0 + l] = make_double2(cs, sn);
-      pr += cs;
-      pim += sn;
+      sincos(theta[row0 + l], &zi[m], &zr[m]);
+      z[row0 + l] = make_double2(zr[m], zi[m]);
     }
   }
+  double pr = ((zr[0] + zr[1]) + zr[2]) + zr[3], pim = ((zi[0] + zi[1]) + zi[2]) + zi[3];
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) {
     pr += __shfl_xor_sync(gmask, pr, o);
@@ -568,7 +475,7 @@ static int check_graph(const cdk_graph *g) {
     set_error("cdk_graph: cta_threads must be 1024");
     return CDK_INPUT;
   }
-  if (g->smem_nodes < 0 || g->seg_rows_cap <= 0 || g->seg_rows_cap > TILE_ROWS) {
+  if (g->smem_nodes < 0 || (g->smem_nodes & 7) || g->seg_rows_cap <= 0) {
     set_error("cdk_graph: bad shared-memory capacities");
     return CDK_INPUT;
   }
@@ -576,8 +483,7 @@ static int check_graph(const cdk_graph *g) {
 }
 
 static size_t stage_smem(const cdk_graph *g) {
-  return RING * sizeof(TileSlot) + (size_t)RING * TILE_ROWS * sizeof(double2) +
-         RING * CNT_STRIDE * sizeof(int) + ((size_t)g->smem_nodes + 8) * sizeof(double2);
+  return stage_smem_bytes(g->seg_rows_cap, g->smem_nodes);
 }
 
 template <int MODE>

@@ -39,8 +39,13 @@ class KuramotoEngine:
                                 else omega, dtype=torch.float64)
         if omega.shape != (n,):
             raise InputError(f"omega must have shape ({n},)")
-        self.omega = omega.to(self.device).contiguous()
-        self.theta = torch.zeros(n, dtype=torch.float64, device=self.device)
+        # bulk copies read theta/omega in 16-byte units: keep a 4-element tail
+        self._omega_buf = torch.zeros(n + 4, dtype=torch.float64, device=self.device)
+        self._omega_buf[:n].copy_(omega)
+        self.omega = self._omega_buf[:n]
+        self._theta_buf = torch.zeros(n + 4, dtype=torch.float64, device=self.device)
+        self.theta = self._theta_buf[:n]
+        self._rhs_theta = None
         nbytes = int(self.lib.cdk_kuramoto_workspace_bytes(ctypes.byref(self.graph.struct)))
         self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         self._gp = ctypes.byref(self.graph.struct)
@@ -67,8 +72,13 @@ class KuramotoEngine:
         """One CIA RHS at ``theta`` (default: current state).  Returns a device tensor."""
         import torch
 
-        th = self.theta if theta is None else torch.as_tensor(theta, dtype=torch.float64,
-                                                              device=self.device).contiguous()
+        if theta is None:
+            th = self.theta
+        else:
+            if self._rhs_theta is None:
+                self._rhs_theta = torch.zeros(self.n + 4, dtype=torch.float64, device=self.device)
+            th = self._rhs_theta[: self.n]
+            th.copy_(torch.as_tensor(theta, dtype=torch.float64).to(self.device))
         if out is None:
             out = torch.empty(self.n, dtype=torch.float64, device=self.device)
         if self._rhs_ws is None:  # separate workspace: never disturbs a running trajectory

@@ -67,26 +67,19 @@ class Schedule:
     n_cta: int
     cta_threads: int
     smem_nodes: int  # staged window capacity (nodes)
-    seg_rows_cap: int  # rows per unstaged segment (shared-memory accumulators)
+    seg_rows_cap: int  # rows per segment (shared-memory row buffers)
     seg_rblk: np.ndarray  # int32[n_seg+1]
     seg_win: np.ndarray  # int64[n_seg, 2]
     seg_base: np.ndarray  # int64[n_seg]
     cta_seg: np.ndarray  # int32[n_cta+1]
-    intra_col: np.ndarray  # uint16, columns rebased to each row's segment base
-    seg_tile: np.ndarray  # int32[n_seg+1] tile range per segment (staged segments only)
-    tiles: np.ndarray  # TILE_DTYPE[n_tile]
-    tile_tab: np.ndarray  # int32: per tile [intra offsets | inter offsets], 16-byte padded
+    intra_col: np.ndarray  # uint16, rebased to each row's segment base, bank-ordered
 
     @property
     def n_seg(self) -> int:
         return int(self.seg_rblk.shape[0] - 1)
 
-    @property
-    def n_tile(self) -> int:
-        return int(self.tiles.shape[0])
-
     def smem_bytes(self) -> int:
-        return stage_smem_bytes(self.smem_nodes)
+        return stage_smem_bytes(self.smem_nodes, self.seg_rows_cap)
 
 
 def _row_runs(rows_sorted: np.ndarray, n_rows: int):
@@ -97,9 +90,9 @@ def _row_runs(rows_sorted: np.ndarray, n_rows: int):
 
 
 # rblocks: <= 32 rows of one community and at most RB_MAX_E padded intra /
-# RB_MAX_X inter entries, so every rblock fits one shared-memory tile
-RB_MAX_E = 8192  # == TILE_E
-RB_MAX_X = 1016  # aligned span <= RB_MAX_X + 6 <= TILE_X
+# RB_MAX_X inter entries (bounds the work of one warp-level epilogue unit)
+RB_MAX_E = 8192
+RB_MAX_X = 1016
 
 
 def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
@@ -171,7 +164,7 @@ def build_layout(dec: Decomposition) -> HostLayout:
     rc = np.repeat(np.arange(m, dtype=np.int64), nb)
     within = np.arange(rc.shape[0], dtype=np.int64) - comm_rblk_off[rc]
     row0 = off[rc] + RB * within
-    # split 32-row blocks whose entries exceed the tile caps (dense long rows)
+    # split 32-row blocks whose entries exceed the caps (dense long rows)
     row0 = _split_heavy_rblocks(row0, off[rc + 1] if rc.size else row0, intra_ptr, inter_ptr)
     rc = np.searchsorted(off, row0, side="right").astype(np.int64) - 1
     comm_rblk_off = np.searchsorted(row0, off).astype(np.int64)
@@ -185,42 +178,29 @@ def build_layout(dec: Decomposition) -> HostLayout:
 
 
 WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
-
-# shared-memory tile ring of the TMA pipeline (must match csrc/kuramoto.cu)
-TILE_ROWS = 128
-TILE_E = 8192  # uint16 intra columns per tile
-TILE_X = 1024  # int32 inter columns per tile (incl. 16-byte alignment slack)
-TILE_TAB = 2 * (TILE_ROWS + 4) + TILE_ROWS  # int32 offset table per tile
-RING = 4
 CTA_THREADS = 1024
-TILE_DTYPE = np.dtype([("e0", np.int64), ("x0a", np.int64), ("tab_off", np.int64),
-                       ("ne", np.int32), ("nxa", np.int32), ("rblk0", np.int32),
-                       ("rblk1", np.int32)])
+ROWS_CAP = 1536  # rows per segment (shared-memory row buffers; multiple of 8)
 
 
-def ring_bytes() -> int:
-    return RING * (2 * TILE_E + 4 * TILE_X + 4 * TILE_TAB)
-
-
-def stage_smem_bytes(smem_nodes: int) -> int:
-    """dynamic shared memory of the stage kernel: window (+8 spare slots),
-    per-slot row accumulators, tile ring, per-slot rblock counters"""
-    return (16 * (smem_nodes + 8) + RING * 16 * TILE_ROWS + ring_bytes()
-            + 4 * RING * (TILE_ROWS + 4))  # per-slot rblock counters
+def stage_smem_bytes(smem_nodes: int, rows_cap: int = ROWS_CAP) -> int:
+    """dynamic shared memory of the stage kernel (csrc/kuramoto.cu:stage_smem_bytes):
+    row accumulators + pointer slices + epilogue inputs + window (+8 spare)"""
+    return (rows_cap + 4) * (16 + 5 * 8) + 16 * (smem_nodes + 8)
 
 
 def _rblk_rows(lay: HostLayout) -> np.ndarray:
     return np.concatenate([lay.rblk_row0, [lay.n_rows]]).astype(np.int64)
 
 
-def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, ctas_per_sm: int = 1,
-                   rows_cap: int = TILE_ROWS, smem_budget: int = SMEM_OPTIN - 1024) -> Schedule:
-    """Cost-balanced contiguous CTA ranges of rblocks, split into segments
-    whose intra neighbours fit one shared-memory window; staged segments are
-    cut into tiles streamed through the TMA ring."""
-    win_bytes = smem_budget - (stage_smem_bytes(0))
-    smem_nodes = max(0, win_bytes // 16) // WIN_ALIGN * WIN_ALIGN
-    n_cta = max(1, sm_count * ctas_per_sm)
+def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int = ROWS_CAP,
+                   smem_budget: int = SMEM_OPTIN - 1024) -> Schedule:
+    """Cost-balanced contiguous CTA ranges of rblocks (one CTA per SM), split
+    into segments of <= rows_cap rows whose intra neighbours fit one
+    shared-memory window (or, for communities above the window capacity and
+    the NONE pool, gather from global memory)."""
+    rows_cap = int(rows_cap) // 8 * 8
+    smem_nodes = max(0, (smem_budget - stage_smem_bytes(0, rows_cap)) // 16) // WIN_ALIGN * WIN_ALIGN
+    n_cta = max(1, int(sm_count))
     nrb = lay.n_rblk
     rows = _rblk_rows(lay)
     cum = np.concatenate([[0.0], np.cumsum(lay.row_cost)])
@@ -252,7 +232,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, ctas_per_sm: in
                     cc = int(lay.rblk_comm[rb])
                     if cc < 0 or not stageable[cc]:
                         break
-                    if int(win_hi[cc]) - w0 > smem_nodes:
+                    if int(win_hi[cc]) - w0 > smem_nodes or rows[rb + 1] - rows[start] > rows_cap:
                         break
                     rb += 1
                 seg_win.append((w0, int(win_hi[int(lay.rblk_comm[rb - 1])])))
@@ -262,7 +242,6 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, ctas_per_sm: in
     seg_rblk = np.asarray(seg_rblk, dtype=np.int32)
     seg_win = np.asarray(seg_win, dtype=np.int64).reshape(-1, 2)
     seg_base = np.asarray(seg_base, dtype=np.int64)
-    seg_tile, tiles, tile_tab = _build_tiles(lay, rows, seg_rblk, seg_win)
 
     # rebase intra columns (community-local in the layout) to each row's segment base
     n = lay.n_rows
@@ -270,66 +249,35 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, ctas_per_sm: in
     comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
     cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
     delta = (cstart - seg_base[seg_of_row]) if n else np.empty(0, np.int64)
-    col = lay.intra_col
+    col = lay.intra_col.copy()
     if np.any(delta != 0):
-        col = col.copy()
         d_ent = np.repeat(delta, np.diff(lay.intra_ptr))
         m = col != INTRA_PAD
         newc = col[m].astype(np.int64) + d_ent[m]
         if newc.size and (newc.min() < 0 or newc.max() >= INTRA_PAD):
             raise InputError("rebased intra column out of uint16 range")
         col[m] = newc.astype(np.uint16)
-    return Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk,
-                    seg_win, seg_base, np.asarray(cta_seg, dtype=np.int32), col, seg_tile, tiles,
-                    tile_tab)
+    _bank_order(col, lay.intra_ptr, smem_nodes)
+    return Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
+                    seg_base, np.asarray(cta_seg, dtype=np.int32), col)
 
 
-def _build_tiles(lay: HostLayout, rows, seg_rblk, seg_win):
-    """Pack each staged segment's rblocks into tiles (<= TILE_ROWS rows,
-    <= TILE_E intra and TILE_X (aligned) inter entries) and build the per-tile
-    int32 offset tables the consumers read from shared memory."""
-    ip, xp = lay.intra_ptr, lay.inter_ptr
-    seg_tile = [0]
-    recs = []
-    tabs = []
-    tab_off = 0
-    for s_ in range(seg_rblk.shape[0] - 1):
-        w0, w1 = seg_win[s_]
-        rb, rb_end = int(seg_rblk[s_]), int(seg_rblk[s_ + 1])
-        if w1 > w0:
-            while rb < rb_end:
-                start = rb
-                r0 = int(rows[start])
-                while rb < rb_end:
-                    r1 = int(rows[rb + 1])
-                    ne = ip[r1] - ip[r0]
-                    x0a = xp[r0] // 4 * 4
-                    nxa = (xp[r1] + 3) // 4 * 4 - x0a
-                    if rb > start and (r1 - r0 > TILE_ROWS or ne > TILE_E or nxa > TILE_X):
-                        break
-                    rb += 1
-                r1 = int(rows[rb])
-                if r1 - r0 > TILE_ROWS or ip[r1] - ip[r0] > TILE_E:
-                    raise InputError("an rblock exceeds the shared-memory tile capacity")
-                x0a = int(xp[r0] // 4 * 4)
-                nxa = int((xp[r1] + 3) // 4 * 4 - x0a)
-                if nxa > TILE_X:
-                    raise InputError("an rblock's inter entries exceed the tile capacity")
-                nrow = r1 - r0
-                half = (nrow + 1 + 3) // 4 * 4
-                tab = np.zeros(2 * half + (nrow + 3) // 4 * 4, dtype=np.int32)
-                tab[: nrow + 1] = ip[r0: r1 + 1] - ip[r0]
-                tab[half: half + nrow + 1] = xp[r0: r1 + 1] - x0a
-                # local rblock index of every row of the tile
-                tab[2 * half: 2 * half + nrow] = np.repeat(
-                    np.arange(rb - start, dtype=np.int32), np.diff(rows[start: rb + 1]))
-                tabs.append(tab)
-                recs.append((int(ip[r0]), x0a, tab_off, int(ip[r1] - ip[r0]), nxa, start, rb))
-                tab_off += tab.shape[0]
-        seg_tile.append(len(recs))
-    tiles = np.array(recs, dtype=TILE_DTYPE) if recs else np.zeros(0, dtype=TILE_DTYPE)
-    tile_tab = np.concatenate(tabs) if tabs else np.zeros(4, dtype=np.int32)
-    return np.asarray(seg_tile, dtype=np.int32), tiles, tile_tab
+def _bank_order(col: np.ndarray, ptr: np.ndarray, smem_nodes: int) -> None:
+    """Native in-place bank-conflict-free ordering of every row's intra run."""
+    import ctypes
+
+    from ._lib import load_library
+
+    if col.size == 0:
+        return
+    lib = load_library()
+    col = np.ascontiguousarray(col)
+    ptr = np.ascontiguousarray(ptr, dtype=np.int64)
+    rc = lib.cdk_host_bank_order(col.ctypes.data_as(ctypes.c_void_p),
+                                 ptr.ctypes.data_as(ctypes.c_void_p), ptr.shape[0] - 1,
+                                 INTRA_PAD, int(smem_nodes) & 7)
+    if rc != 0:
+        raise InputError("cdk_host_bank_order failed")
 
 
 class DeviceGraph:
@@ -356,11 +304,13 @@ class DeviceGraph:
             return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
         # uint16 has no torch dtype with from_numpy in older builds: ship as int16 bits
+        pad = np.zeros(4, dtype=np.int64)
         self._t = {
             "comm_off": up(lay.comm_off),
-            "intra_ptr": up(lay.intra_ptr),
+            # bulk copies read the pointer slices in 16-byte units: 4 entries of slack
+            "intra_ptr": up(np.concatenate([lay.intra_ptr, pad + lay.intra_ptr[-1]])),
             "intra_col": up(sch.intra_col.view(np.int16)),
-            "inter_ptr": up(lay.inter_ptr),
+            "inter_ptr": up(np.concatenate([lay.inter_ptr, pad + lay.inter_ptr[-1]])),
             "inter_col": up(lay.inter_col),
             "rblk_row0": up(lay.rblk_row0),
             "rblk_comm": up(lay.rblk_comm),
@@ -369,17 +319,12 @@ class DeviceGraph:
             "seg_win": up(sch.seg_win.reshape(-1)),
             "seg_base": up(sch.seg_base),
             "cta_seg": up(sch.cta_seg),
-            "seg_tile": up(sch.seg_tile),
-            "tiles": up(sch.tiles.view(np.uint8)) if sch.n_tile else
-            torch.zeros(64, dtype=torch.uint8, device=dev),
-            "tile_tab": up(sch.tile_tab),
         }
-        # inter columns are bulk-copied in 16-byte units: keep 3 entries of slack
-        t_ic = self._t["inter_col"]
-        self._t["inter_col"] = torch.cat([t_ic, torch.zeros(4, dtype=torch.int32, device=dev)])
         # keep a 16-byte tail on intra_col so uint4 loads never run past the allocation
         if self._t["intra_col"].numel() == 0:
             self._t["intra_col"] = torch.full((8,), -1, dtype=torch.int16, device=dev)
+        if self._t["inter_col"].numel() == 0:
+            self._t["inter_col"] = torch.zeros(4, dtype=torch.int32, device=dev)
         t = self._t
         self.struct = CdkGraph(
             n_rows=lay.n_rows, n_comm=lay.n_comm,
@@ -391,8 +336,7 @@ class DeviceGraph:
             rblk_row0=t["rblk_row0"].data_ptr(), rblk_comm=t["rblk_comm"].data_ptr(),
             comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
             seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
-            cta_seg=t["cta_seg"].data_ptr(), seg_tile=t["seg_tile"].data_ptr(),
-            tiles=t["tiles"].data_ptr(), tile_tab=t["tile_tab"].data_ptr(), n_tile=sch.n_tile,
+            cta_seg=t["cta_seg"].data_ptr(),
         )
 
     def device_bytes(self) -> int:
