@@ -187,6 +187,9 @@ CDK_API int cdk_abi_version(void);
 CDK_API const char *cdk_last_error(void);
 /* number of kernel launches issued by this library since load (for the bench's gpu_launches) */
 CDK_API int64_t cdk_launch_count(void);
+/* profiling builds (-DCDK_PROFILE) only: per-CTA phase cycles of the latest
+ * stage launch go to prof (device, 4 * n_cta uint64); no-op otherwise */
+CDK_API void cdk_debug_set_profile_buffer(void *prof);
 /* max dynamic shared memory per block (opt-in) on the current device */
 CDK_API int cdk_max_smem_optin(void);
 

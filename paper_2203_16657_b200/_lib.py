@@ -69,6 +69,7 @@ _SIGS = {
     "cdk_kuramoto_euler": [ctypes.POINTER(CdkGraph), P, P, D, D, I64, P, P],
     "cdk_kuramoto_status": [ctypes.POINTER(CdkGraph), P, ctypes.POINTER(CdkRunStatus), P],
     "cdk_host_bank_order": [P, P, I64, I32, I32],
+    "cdk_debug_set_profile_buffer": [P],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],
@@ -78,6 +79,7 @@ _RESTYPES = {
     "cdk_kuramoto_workspace_bytes": ctypes.c_size_t,
     "cdk_last_error": ctypes.c_char_p,
     "cdk_launch_count": I64,
+    "cdk_debug_set_profile_buffer": None,
 }
 
 EXPORTED = tuple(_SIGS)

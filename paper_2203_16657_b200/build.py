@@ -50,13 +50,16 @@ def _stale() -> bool:
 
 def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False,
                   debug: bool = False) -> str:
-    out = LIB if not debug else LIB.replace(".so", "_debug.so")
+    out = LIB if not debug else LIB.replace(".so", "_profile.so" if debug == "profile"
+                                            else "_debug.so")
     if not debug and not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     tmp = out + ".tmp"
     cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-o", tmp, *sources()]
-    if debug:
+    if debug == "profile":
+        cmd.insert(1, "-DCDK_PROFILE")
+    elif debug:
         cmd.insert(1, "-DCDK_DEBUG")
     if ptxas_verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -73,4 +76,4 @@ def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: boo
 
 if __name__ == "__main__":
     print(build_library(force=True, verbose=True, ptxas_verbose="-v" in sys.argv,
-                        debug="--debug" in sys.argv))
+                        debug="profile" if "--profile" in sys.argv else ("--debug" in sys.argv)))

@@ -88,6 +88,7 @@ struct StageArgs {
   double k_over_n;
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
+  unsigned long long *prof;  // CDK_PROFILE builds: per-CTA phase cycles
 };
 
 // Canonical community sum R_c of the rblock partials: 8 lanes, lane t sums
@@ -247,6 +248,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
   }
   __syncthreads();
   uint32_t parity = 0;
+#ifdef CDK_PROFILE
+  unsigned long long t_stage = 0, t_gather = 0, t_epi = 0, t_mark = clock64();
+  const unsigned long long t_begin = t_mark;
+#define PROF_MARK(acc)                        \
+  do {                                        \
+    const unsigned long long _n = clock64();  \
+    acc += _n - t_mark;                       \
+    t_mark = _n;                              \
+  } while (0)
+#else
+#define PROF_MARK(acc) \
+  do {                 \
+  } while (0)
+#endif
 
   for (int s = segA; s < segB; ++s) {
     const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
@@ -274,6 +289,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
     }
     mbar_wait(&bar_seg, parity);
     parity ^= 1;
+    PROF_MARK(t_stage);
     const double2 *zwin = staged ? sm.zs : z_in + g.seg_base[s];
 
     // ---- 2. gather: dynamic row claims, 1-row-ahead prefetch ---------------
@@ -331,6 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       cur = nxt;
     }
     __syncthreads();
+    PROF_MARK(t_gather);
     if (tid == 0) s_claim = 0;  // next segment's claims start after the end barrier
 
     // ---- 3. epilogue: warp per rblock, lane = row ---------------------------
@@ -408,7 +425,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       }
     }
     __syncthreads();  // shared segment buffers reused by the next segment
+    PROF_MARK(t_epi);
   }
+#ifdef CDK_PROFILE
+  if (tid == 0 && a.prof) {
+    unsigned long long *p = a.prof + 4 * blockIdx.x;
+    p[0] = clock64() - t_begin;
+    p[1] = t_stage;
+    p[2] = t_gather;
+    p[3] = t_epi;
+  }
+#endif
 }
 
 // z = exp(i theta) and the canonical rblock partials (prepare).  One 8-lane
@@ -521,9 +548,12 @@ static int prepare(const cdk_graph *g, const double *theta, const Workspace &w, 
   return CDK_OK;
 }
 
+static unsigned long long *g_prof = nullptr;
+
 static StageArgs base_args(const cdk_graph *g, const Workspace &w, double *theta,
                            const double *omega, double k_over_n) {
   StageArgs a{};
+  a.prof = g_prof;
   a.g = *g;
   a.part = w.part;
   a.cnt = w.cnt;
@@ -667,4 +697,10 @@ extern "C" int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const d
     case 3: a.h = dt; return launch_stage<3>(a, st);
     default: a.h = dt / 6.0; return launch_stage<4>(a, st);
   }
+}
+
+// CDK_PROFILE builds only: per-CTA phase cycles [total, staging, gather, epilogue]
+// of the most recent stage launch are written to prof (device, 4*n_cta u64).
+extern "C" CDK_API void cdk_debug_set_profile_buffer(void *prof) {
+  g_prof = reinterpret_cast<unsigned long long *>(prof);
 }

@@ -1,0 +1,41 @@
+"""Per-CTA phase timing of the stage kernel (needs the CDK_PROFILE build)."""
+import os, sys
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+os.environ.setdefault("CDK_LIB", os.path.join(REPO, "paper_2203_16657_b200/_build/libcommdyn_cuda_profile.so"))
+import numpy as np, torch
+from paper_2203_16657_b200 import configs
+from paper_2203_16657_b200.engine import KuramotoEngine
+c = configs.config2(); dec = c.decomposition(); omega, theta0 = c.state()
+eng = KuramotoEngine(dec, omega, coupling=c.coupling, norm=c.n)
+sch = eng.graph.schedule; lay = eng.graph.layout
+prof = torch.zeros(4 * sch.n_cta, dtype=torch.int64, device="cuda")
+eng.lib.cdk_debug_set_profile_buffer(prof.data_ptr())
+eng.set_state(theta0)
+for it in range(3):
+    eng.rk4_stage(c.dt, 1)
+torch.cuda.synchronize()
+P = prof.view(-1, 4).cpu().numpy().astype(np.float64)
+rows = np.concatenate([lay.rblk_row0, [lay.n_rows]])
+seg_rows = rows[sch.seg_rblk]
+feat = []
+for b in range(sch.n_cta):
+    s0, s1 = sch.cta_seg[b], sch.cta_seg[b + 1]
+    r0, r1 = seg_rows[s0], seg_rows[s1]
+    ent = lay.intra_ptr[r1] - lay.intra_ptr[r0]
+    xen = lay.inter_ptr[r1] - lay.inter_ptr[r0]
+    win = sum(int(sch.seg_win[s][1] - sch.seg_win[s][0]) for s in range(s0, s1))
+    feat.append((r1 - r0, ent, xen, s1 - s0, win))
+F = np.array(feat, dtype=np.float64)
+np.set_printoptions(linewidth=150)
+print("cycles total/stage/gather/epi: mean", P.mean(0).astype(int), "max", P.max(0).astype(int), "min", P.min(0).astype(int))
+print("rows/entries/inter/segs/window: mean", F.mean(0).astype(int), "max", F.max(0).astype(int), "min", F.min(0).astype(int))
+X = np.column_stack([F[:, :5], np.ones(len(F))])
+for j, name in enumerate(["total", "stage", "gather", "epi"]):
+    coef, *_ = np.linalg.lstsq(X, P[:, j], rcond=None)
+    pred = X @ coef
+    print(name, "fit rows/ent/inter/segs/win/const", np.round(coef, 3), "R2", round(1 - ((P[:, j] - pred) ** 2).sum() / ((P[:, j] - P[:, j].mean()) ** 2).sum(), 3))
+order = np.argsort(-P[:, 0])[:8]
+for b in order: print("slow cta", b, P[b].astype(int), F[b].astype(int))
+order = np.argsort(P[:, 0])[:4]
+for b in order: print("fast cta", b, P[b].astype(int), F[b].astype(int))
