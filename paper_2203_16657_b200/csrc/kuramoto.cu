@@ -41,9 +41,7 @@ namespace cdk {
 struct Workspace {
   double2 *z[2];
   double *ksum;
-  double2 *R[2];
-  double2 *part;
-  int32_t *cnt;
+  double2 *part[2];  // canonical rblock partials of z (ping-pong with z)
   cdk_run_status *status;
 };
 
@@ -58,15 +56,13 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
     off = align_up(off + bytes, 256);
     return p;
   };
-  const size_t n = (size_t)g->n_rows, m = (size_t)g->n_comm;
+  const size_t n = (size_t)g->n_rows;
   // +16: staged windows are rounded out to 8-node (128-byte) boundaries
   w.z[0] = (double2 *)take((n + 16) * sizeof(double2));
   w.z[1] = (double2 *)take((n + 16) * sizeof(double2));
   w.ksum = (double *)take((n + 4) * sizeof(double));  // bulk copies read 16-byte units
-  w.R[0] = (double2 *)take((m + 1) * sizeof(double2));
-  w.R[1] = (double2 *)take((m + 1) * sizeof(double2));
-  w.part = (double2 *)take(((size_t)g->n_rblk + 1) * sizeof(double2));
-  w.cnt = (int32_t *)take((m + 1) * sizeof(int32_t));
+  w.part[0] = (double2 *)take(((size_t)g->n_rblk + 1) * sizeof(double2));
+  w.part[1] = (double2 *)take(((size_t)g->n_rblk + 1) * sizeof(double2));
   w.status = (cdk_run_status *)take(sizeof(cdk_run_status));
   if (total) *total = off;
   return w;
@@ -76,10 +72,8 @@ struct StageArgs {
   cdk_graph g;
   const double2 *z_in;
   double2 *z_out;
-  const double2 *R_in;
-  double2 *R_out;
-  double2 *part;
-  int32_t *cnt;
+  const double2 *part_in;  // rblock partials of z_in (community sums are reduced in-kernel)
+  double2 *part_out;       // rblock partials of z_out
   cdk_run_status *status;
   double *theta;
   const double *omega;
@@ -143,22 +137,35 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+__device__ __forceinline__ double2 lds_d2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 // 8 uint16 intra columns (one 16-byte chunk): subtract their z (sign -1).
-// Staged (shared memory): branch-free, padding (0xFFFF) is clamped onto a zero
-// slot one past the window capacity.  Unstaged (global, huge communities):
-// predicated loads.
-template <bool STAGED>
-__device__ __forceinline__ void gather8(const uint4 w, const double2 *__restrict__ zbase,
-                                        uint32_t zero_slot, double &sr, double &si) {
+// Staged: explicit ld.shared from the window (32-bit shared address),
+// branch-free, padding (0xFFFF) clamped onto a zero slot one past the window
+// capacity.  Unstaged (global, huge communities / NONE pool): predicated loads.
+__device__ __forceinline__ void gather8_smem(const uint4 w, uint32_t zs_addr, uint32_t zero_slot,
+                                             double &sr, double &si) {
   const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
-    if (STAGED) {
-      const double2 z = zbase[min(u, zero_slot)];
-      sr -= z.x;
-      si -= z.y;
-    } else if (u != CDK_INTRA_PAD) {
+    const double2 z = lds_d2(zs_addr + (min(u, zero_slot) << 4));
+    sr -= z.x;
+    si -= z.y;
+  }
+}
+
+__device__ __forceinline__ void gather8_global(const uint4 w, const double2 *__restrict__ zbase,
+                                               double &sr, double &si) {
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+    if (u != CDK_INTRA_PAD) {
       const double2 z = ldg(zbase + u);
       sr -= z.x;
       si -= z.y;
@@ -218,33 +225,36 @@ __device__ __forceinline__ SegSmem carve_smem(unsigned char *base, int cap, int 
   return m;
 }
 
-struct RowLoads {
-  int64_t e1, x0, x1;
-  int64_t p;  // first chunk position of this lane
-  uint4 c0, c1;
-  int32_t j;
+constexpr int SEG_MAX_COMM = 64;  // communities per segment (planner cap)
+
+// one row of the group's software pipeline (offsets relative to the segment)
+struct RowPipe {
+  int e1, p;    // intra run end, this lane's first chunk position
+  int x0, x1;   // inter run
+  int j;        // this lane's first inter column (or -1)
+  uint4 c0, c1; // this lane's first two 16-byte column chunks
+  double2 z;    // z of column j
 };
 
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar_seg;
-  __shared__ int s_claim;
+  __shared__ double2 sR[SEG_MAX_COMM];
   const cdk_graph &g = a.g;
   const SegSmem sm = carve_smem(smem_raw, g.seg_rows_cap, g.smem_nodes);
   const uint32_t zero_slot = (uint32_t)g.smem_nodes;  // zs[smem_nodes] == 0
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = lane & 7;
+  const int grp = tid >> 3;
   const int leader = lane & 24;
   const unsigned gmask = 0xFFu << leader;  // this 8-lane group only
   const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
   const double2 *__restrict__ z_in = a.z_in;
-  const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col);
   const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
   if (tid == 0) {
     mbar_init(&bar_seg, 1);
     sm.zs[zero_slot] = make_double2(0.0, 0.0);
-    s_claim = 0;
   }
   __syncthreads();
   uint32_t parity = 0;
@@ -271,14 +281,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
     const int64_t w0 = g.seg_win[2 * s], w1 = g.seg_win[2 * s + 1];
     const bool staged = w1 > w0;
     const int nrows = (int)(row1 - row0);
+    const int cA = g.rblk_comm[rbA];
 
-    // ---- 1. stage window, pointer slices, epilogue inputs ------------------
+    // ---- 1. stage window, pointer slices, epilogue inputs (async) ----------
     if (tid == 0) {
       fence_proxy_async_smem();  // earlier generic accesses before the async overwrite
       const uint32_t bw = staged ? (uint32_t)((w1 - w0) * 16) : 0u;
       const uint32_t bp = (uint32_t)((((row1 + 2) & ~(int64_t)1) - row0a) * 8);
       const uint32_t br = (uint32_t)((((row1 + 1) & ~(int64_t)1) - row0a) * 8);
-      const int nr_in = (MODE == 0 || MODE == 5 || MODE == 1) ? ((MODE == 0) ? 1 : 2) : 3;
+      const int nr_in = (MODE == 0) ? 1 : ((MODE == 1 || MODE == 5) ? 2 : 3);
       mbar_expect_tx(&bar_seg, bw + 2 * bp + (uint32_t)nr_in * br);
       if (bw) bulk_g2s(sm.zs, z_in + w0, bw, &bar_seg);
       bulk_g2s(sm.sip, g.intra_ptr + row0a, bp, &bar_seg);
@@ -287,53 +298,100 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       if (MODE != 0) bulk_g2s(sm.sth, a.theta + row0a, br, &bar_seg);
       if (MODE >= 2 && MODE <= 4) bulk_g2s(sm.sks, a.ksum + row0a, br, &bar_seg);
     }
+    // community observables R_c of the segment's communities, reduced (in the
+    // canonical 8-lane order) from the previous stage's rblock partials while
+    // the copies fly: all threads load the partials into the (still unused)
+    // accumulator buffer at once, then one 8-lane group per community reduces.
+    if (cA >= 0) {
+      const int cB = g.rblk_comm[rbB - 1];
+      const int cLast = cB >= 0 ? cB : (int)g.n_comm - 1;
+      const int ncomm = cLast - cA + 1;
+      const int pb0 = g.comm_rblk_off[cA], pb1 = g.comm_rblk_off[cLast + 1];
+      const int np = pb1 - pb0;
+      const bool fits = np <= (int)cap4_of(g.seg_rows_cap);
+      if (fits) {
+        for (int q = tid; q < np; q += NTHREADS) sm.acc[q] = ldcg2(a.part_in + pb0 + q);
+        __syncthreads();
+      }
+      for (int q = grp; q < ncomm; q += NGROUPS) {
+        const int c = cA + q;
+        const int b0 = g.comm_rblk_off[c], b1 = g.comm_rblk_off[c + 1];
+        double2 Rc;
+        if (fits) {
+          double sr = 0.0, si = 0.0;
+          for (int b = b0 + t; b < b1; b += 8) {
+            const double2 v = sm.acc[b - pb0];
+            sr += v.x;
+            si += v.y;
+          }
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(gmask, sr, o);
+            si += __shfl_xor_sync(gmask, si, o);
+          }
+          Rc = make_double2(sr, si);
+        } else {
+          Rc = reduce_comm8(a.part_in, b0, b1, t, gmask);
+        }
+        if (t == 0) sR[q] = Rc;
+      }
+      __syncthreads();  // accumulator buffer free for the gather phase
+    }
     mbar_wait(&bar_seg, parity);
     parity ^= 1;
     PROF_MARK(t_stage);
-    const double2 *zwin = staged ? sm.zs : z_in + g.seg_base[s];
+    const uint32_t zs_addr = smem_u32(sm.zs);
+    const double2 *__restrict__ zglob = z_in + g.seg_base[s];
+    const int64_t ebase = sm.sip[row0 - row0a], xbase = sm.sxp[row0 - row0a];
+    const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col + ebase);
+    const int32_t *__restrict__ xcol = g.inter_col + xbase;
 
-    // ---- 2. gather: dynamic row claims, 1-row-ahead prefetch ---------------
-    auto claim = [&]() {
-      int r = 0;
-      if (t == 0) r = atomicAdd(&s_claim, 1);
-      return __shfl_sync(gmask, r, leader);
-    };
-    auto issue = [&](int r, RowLoads &L) {
+    // ---- 2. gather: static rows grp, grp+NGROUPS, ...; 3-deep pipeline ----
+    //   C: pointers + first inter column (2 rows ahead)
+    //   B: first two column chunks + z of the inter column (1 row ahead)
+    //   A: gathers, tails, reduction
+    auto stage_ptr = [&](int r, RowPipe &R) {
       if (r < nrows) {
         const int64_t li = row0 + r - row0a;
-        const int64_t e0 = sm.sip[li];
-        L.e1 = sm.sip[li + 1];
-        L.x0 = sm.sxp[li];
-        L.x1 = sm.sxp[li + 1];
-        L.p = e0 + 8 * t;
-        L.c0 = (L.p < L.e1) ? ldg(colv + (L.p >> 3)) : padv;
-        L.c1 = (L.p + 64 < L.e1) ? ldg(colv + ((L.p + 64) >> 3)) : padv;
-        L.j = (L.x0 + t < L.x1) ? ldg(g.inter_col + L.x0 + t) : -1;
+        const int e0 = (int)(sm.sip[li] - ebase);
+        R.e1 = (int)(sm.sip[li + 1] - ebase);
+        R.x0 = (int)(sm.sxp[li] - xbase);
+        R.x1 = (int)(sm.sxp[li + 1] - xbase);
+        R.p = e0 + 8 * t;
+        R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
       }
     };
-    int r = claim();
-    RowLoads cur{}, nxt{};
-    issue(r, cur);
-    while (r < nrows) {
-      const int rn = claim();
-      issue(rn, nxt);
-      const double2 zx = (cur.j >= 0) ? ldg(z_in + cur.j) : make_double2(0.0, 0.0);
+    auto stage_data = [&](int r, RowPipe &R) {
+      if (r < nrows) {
+        R.c0 = (R.p < R.e1) ? ldg(colv + (R.p >> 3)) : padv;
+        R.c1 = (R.p + 64 < R.e1) ? ldg(colv + ((R.p + 64) >> 3)) : padv;
+        R.z = (R.j >= 0) ? ldg(z_in + R.j) : make_double2(0.0, 0.0);
+      }
+    };
+    RowPipe A{}, B{}, C{};
+    int r = grp;
+    stage_ptr(r, A);
+    stage_ptr(r + NGROUPS, B);
+    stage_data(r, A);
+    for (; r < nrows; r += NGROUPS) {
+      stage_ptr(r + 2 * NGROUPS, C);
+      stage_data(r + NGROUPS, B);
       double sr = 0.0, si = 0.0;
       if (staged) {
-        gather8<true>(cur.c0, zwin, zero_slot, sr, si);
-        gather8<true>(cur.c1, zwin, zero_slot, sr, si);
-        for (int64_t p = cur.p + 128; p < cur.e1; p += 64)
-          gather8<true>(ldg(colv + (p >> 3)), zwin, zero_slot, sr, si);
+        gather8_smem(A.c0, zs_addr, zero_slot, sr, si);
+        gather8_smem(A.c1, zs_addr, zero_slot, sr, si);
+        for (int p = A.p + 128; p < A.e1; p += 64)
+          gather8_smem(ldg(colv + (p >> 3)), zs_addr, zero_slot, sr, si);
       } else {
-        gather8<false>(cur.c0, zwin, 0, sr, si);
-        gather8<false>(cur.c1, zwin, 0, sr, si);
-        for (int64_t p = cur.p + 128; p < cur.e1; p += 64)
-          gather8<false>(ldg(colv + (p >> 3)), zwin, 0, sr, si);
+        gather8_global(A.c0, zglob, sr, si);
+        gather8_global(A.c1, zglob, sr, si);
+        for (int p = A.p + 128; p < A.e1; p += 64)
+          gather8_global(ldg(colv + (p >> 3)), zglob, sr, si);
       }
-      sr += zx.x;
-      si += zx.y;
-      for (int64_t p = cur.x0 + 8 + t; p < cur.x1; p += 8) {
-        const double2 z = ldg(z_in + ldg(g.inter_col + p));
+      sr += A.z.x;
+      si += A.z.y;
+      for (int p = A.x0 + 8 + t; p < A.x1; p += 8) {
+        const double2 z = ldg(z_in + ldg(xcol + p));
         sr += z.x;
         si += z.y;
       }
@@ -343,12 +401,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
         si += __shfl_xor_sync(gmask, si, o);
       }
       if (t == 0) sm.acc[r] = make_double2(sr, si);
-      r = rn;
-      cur = nxt;
+      A = B;
+      B = C;
     }
     __syncthreads();
     PROF_MARK(t_gather);
-    if (tid == 0) s_claim = 0;  // next segment's claims start after the end barrier
 
     // ---- 3. epilogue: warp per rblock, lane = row ---------------------------
     const double kn = a.k_over_n;
@@ -363,7 +420,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
         const int64_t li = i - row0a;
         const double2 ac = sm.acc[i - row0];
         const double2 zi = staged ? sm.zs[i - w0] : ldg(z_in + i);
-        const double2 R = (c >= 0) ? ldcg2(a.R_in + c) : make_double2(0.0, 0.0);
+        const double2 R = (c >= 0) ? sR[c - cA] : make_double2(0.0, 0.0);
         double k = sm.som[li] + kn * (R.y * zi.x - R.x * zi.y);
         k = k + kn * (ac.y * zi.x - ac.x * zi.y);
         if (MODE == 0) {
@@ -391,7 +448,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
           a.z_out[i] = make_double2(zr, zim);
         }
       }
-      if (MODE != 0 && c >= 0) {
+      if (MODE != 0) {
         // canonical rblock partial: lane t < 8 sums rows t, t+8, t+16, t+24 in
         // order (absent rows = +0), then the 8-lane xor butterfly
         const double r8 = __shfl_down_sync(FULL, zr, 8), i8 = __shfl_down_sync(FULL, zim, 8);
@@ -403,25 +460,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
           pr += __shfl_xor_sync(FULL, pr, o);
           pim += __shfl_xor_sync(FULL, pim, o);
         }
-        int last = 0;
-        if (lane == 0) {
-          a.part[rb] = make_double2(pr, pim);
-          __threadfence();
-          const int total = g.comm_rblk_off[c + 1] - g.comm_rblk_off[c];
-          last = (atomicAdd(a.cnt + c, 1) + 1 == total);
-        }
-        last = __shfl_sync(FULL, last, 0);
-        if (last) {  // this warp finished community c: reduce its partials
-          __threadfence();
-          if (lane < 8) {
-            const double2 Rn =
-                reduce_comm8(a.part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane, 0xFFu);
-            if (lane == 0) {
-              a.R_out[c] = Rn;
-              a.cnt[c] = 0;
-            }
-          }
-        }
+        if (lane == 0) a.part_out[rb] = make_double2(pr, pim);
       }
     }
     __syncthreads();  // shared segment buffers reused by the next segment
@@ -470,23 +509,11 @@ __global__ void __launch_bounds__(256) prepare_kernel(cdk_graph g, const double 
   if (t == 0) part[rb] = make_double2(pr, pim);
 }
 
-__global__ void comm_reduce_kernel(cdk_graph g, const double2 *part, double2 *R, int32_t *cnt,
-                                   cdk_run_status *st) {
-  const int c = blockIdx.x;
-  const int lane = threadIdx.x;  // blockDim.x == 8
-  if (c < g.n_comm) {
-    const double2 Rc = reduce_comm8(part, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], lane, 0xFFu);
-    if (lane == 0) {
-      R[c] = Rc;
-      cnt[c] = 0;
-    }
-  }
-  if (c == 0 && lane == 0) {
-    st->nonfinite = 0;
-    st->first_bad_step = INT64_MAX;
-    st->steps_done = 0;
-    st->reserved = 0;
-  }
+__global__ void reset_status_kernel(cdk_run_status *st) {
+  st->nonfinite = 0;
+  st->first_bad_step = INT64_MAX;
+  st->steps_done = 0;
+  st->reserved = 0;
 }
 
 __global__ void advance_kernel(cdk_run_status *st, int64_t n) { st->steps_done += n; }
@@ -539,12 +566,11 @@ static int launch_stage(const StageArgs &a, cudaStream_t st) {
 static int prepare(const cdk_graph *g, const double *theta, const Workspace &w, cudaStream_t st) {
   if (g->n_rblk > 0) {
     const int gpb = 32;  // 8-lane groups per block
-    prepare_kernel<<<(g->n_rblk + gpb - 1) / gpb, 8 * gpb, 0, st>>>(*g, theta, w.z[0], w.part);
+    prepare_kernel<<<(g->n_rblk + gpb - 1) / gpb, 8 * gpb, 0, st>>>(*g, theta, w.z[0], w.part[0]);
     CDK_CHECK_LAUNCH("prepare_kernel");
   }
-  const int m = (int)g->n_comm;
-  comm_reduce_kernel<<<m > 0 ? m : 1, 8, 0, st>>>(*g, w.part, w.R[0], w.cnt, w.status);
-  CDK_CHECK_LAUNCH("comm_reduce_kernel");
+  reset_status_kernel<<<1, 1, 0, st>>>(w.status);
+  CDK_CHECK_LAUNCH("reset_status_kernel");
   return CDK_OK;
 }
 
@@ -555,8 +581,6 @@ static StageArgs base_args(const cdk_graph *g, const Workspace &w, double *theta
   StageArgs a{};
   a.prof = g_prof;
   a.g = *g;
-  a.part = w.part;
-  a.cnt = w.cnt;
   a.status = w.status;
   a.theta = theta;
   a.omega = omega;
@@ -593,7 +617,7 @@ extern "C" int cdk_kuramoto_rhs(const cdk_graph *g, const double *theta, const d
   if (rc) return rc;
   StageArgs a = base_args(g, w, const_cast<double *>(theta), omega, k_over_n);
   a.z_in = w.z[0];
-  a.R_in = w.R[0];
+  a.part_in = w.part[0];
   a.out = out;
   return launch_stage<0>(a, st);
 }
@@ -614,13 +638,13 @@ extern "C" int cdk_kuramoto_rk4(const cdk_graph *g, double *theta, const double 
   for (int64_t s = 0; s < n_steps; ++s) {
     a.step_rel = s;
     // stage 1: z0 -> z1
-    a.z_in = w.z[0]; a.z_out = w.z[1]; a.R_in = w.R[0]; a.R_out = w.R[1]; a.h = h2;
+    a.z_in = w.z[0]; a.z_out = w.z[1]; a.part_in = w.part[0]; a.part_out = w.part[1]; a.h = h2;
     if ((rc = launch_stage<1>(a, st))) return rc;
-    a.z_in = w.z[1]; a.z_out = w.z[0]; a.R_in = w.R[1]; a.R_out = w.R[0]; a.h = h2;
+    a.z_in = w.z[1]; a.z_out = w.z[0]; a.part_in = w.part[1]; a.part_out = w.part[0]; a.h = h2;
     if ((rc = launch_stage<2>(a, st))) return rc;
-    a.z_in = w.z[0]; a.z_out = w.z[1]; a.R_in = w.R[0]; a.R_out = w.R[1]; a.h = dt;
+    a.z_in = w.z[0]; a.z_out = w.z[1]; a.part_in = w.part[0]; a.part_out = w.part[1]; a.h = dt;
     if ((rc = launch_stage<3>(a, st))) return rc;
-    a.z_in = w.z[1]; a.z_out = w.z[0]; a.R_in = w.R[1]; a.R_out = w.R[0]; a.h = h6;
+    a.z_in = w.z[1]; a.z_out = w.z[0]; a.part_in = w.part[1]; a.part_out = w.part[0]; a.h = h6;
     if ((rc = launch_stage<4>(a, st))) return rc;
   }
   if (n_steps > 0) {
@@ -658,14 +682,15 @@ extern "C" int cdk_kuramoto_euler(const cdk_graph *g, double *theta, const doubl
   for (int64_t s = 0; s < n_steps; ++s) {
     const int src = (int)(s & 1);
     a.step_rel = s;
-    a.z_in = w.z[src]; a.z_out = w.z[src ^ 1]; a.R_in = w.R[src]; a.R_out = w.R[src ^ 1];
+    a.z_in = w.z[src]; a.z_out = w.z[src ^ 1];
+    a.part_in = w.part[src]; a.part_out = w.part[src ^ 1];
     if ((rc = launch_stage<5>(a, st))) return rc;
   }
   if (n_steps & 1) {  // leave the current state in buffer 0 (the rk4/euler entry invariant)
     cudaError_t e = cudaMemcpyAsync(w.z[0], w.z[1], sizeof(double2) * (size_t)g->n_rows,
                                     cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(w.R[0], w.R[1], sizeof(double2) * (size_t)(g->n_comm + 1),
+      e = cudaMemcpyAsync(w.part[0], w.part[1], sizeof(double2) * (size_t)(g->n_rblk + 1),
                           cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync(euler parity)");
   }
@@ -689,7 +714,8 @@ extern "C" int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const d
   Workspace w = carve(g, workspace, nullptr);
   StageArgs a = base_args(g, w, theta, omega, k_over_n);
   const int src = (stage - 1) & 1;
-  a.z_in = w.z[src]; a.z_out = w.z[src ^ 1]; a.R_in = w.R[src]; a.R_out = w.R[src ^ 1];
+  a.z_in = w.z[src]; a.z_out = w.z[src ^ 1];
+  a.part_in = w.part[src]; a.part_out = w.part[src ^ 1];
   a.step_rel = 0;
   switch (stage) {
     case 1: a.h = dt / 2.0; return launch_stage<1>(a, st);

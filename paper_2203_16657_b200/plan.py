@@ -180,6 +180,7 @@ def build_layout(dec: Decomposition) -> HostLayout:
 WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
 CTA_THREADS = 1024
 ROWS_CAP = 1536  # rows per segment (shared-memory row buffers; multiple of 8)
+SEG_MAX_COMM = 64  # communities per staged segment (csrc/kuramoto.cu SEG_MAX_COMM)
 
 
 def stage_smem_bytes(smem_nodes: int, rows_cap: int = ROWS_CAP) -> int:
@@ -193,7 +194,7 @@ def _rblk_rows(lay: HostLayout) -> np.ndarray:
 
 
 def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int = ROWS_CAP,
-                   smem_budget: int = SMEM_OPTIN - 1024) -> Schedule:
+                   smem_budget: int = SMEM_OPTIN - 2048) -> Schedule:
     """Cost-balanced contiguous CTA ranges of rblocks (one CTA per SM), split
     into segments of <= rows_cap rows whose intra neighbours fit one
     shared-memory window (or, for communities above the window capacity and
@@ -232,7 +233,8 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
                     cc = int(lay.rblk_comm[rb])
                     if cc < 0 or not stageable[cc]:
                         break
-                    if int(win_hi[cc]) - w0 > smem_nodes or rows[rb + 1] - rows[start] > rows_cap:
+                    if (int(win_hi[cc]) - w0 > smem_nodes or rows[rb + 1] - rows[start] > rows_cap
+                            or cc - c >= SEG_MAX_COMM):
                         break
                     rb += 1
                 seg_win.append((w0, int(win_hi[int(lay.rblk_comm[rb - 1])])))

@@ -177,7 +177,7 @@ def test_schedule_invariants(sm_count, seed, rows_cap):
         w0, w1 = sch.seg_win[s]
         assert rows_rb[seg[s + 1]] - rows_rb[seg[s]] <= max(rows_cap // 8 * 8, 32)
         if w1 > w0:  # staged: every community of the segment inside the window
-            assert np.all(cs >= 0)
+            assert np.all(cs >= 0) and cs.max() - cs.min() < PL.SEG_MAX_COMM
             assert w1 - w0 <= sch.smem_nodes and sch.seg_base[s] == w0
             assert np.all(off[cs] >= w0) and np.all(off[cs + 1] <= w1)
         else:
