@@ -378,8 +378,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       stage_data(r + NGROUPS, B);
       double sr = 0.0, si = 0.0;
       if (staged) {
-        gather8_smem(A.c0, zs_addr, zero_slot, sr, si);
-        gather8_smem(A.c1, zs_addr, zero_slot, sr, si);
+        if (A.p < A.e1) gather8_smem(A.c0, zs_addr, zero_slot, sr, si);  // skip all-pad chunks
+        if (A.p + 64 < A.e1) gather8_smem(A.c1, zs_addr, zero_slot, sr, si);
         for (int p = A.p + 128; p < A.e1; p += 64)
           gather8_smem(ldg(colv + (p >> 3)), zs_addr, zero_slot, sr, si);
       } else {

@@ -27,8 +27,11 @@ from .graph import NONE, Decomposition
 
 RB = 32
 INTRA_PAD = 0xFFFF
-ROW_COST = 24.0  # per-row overhead in "entry" units (pointer loads, epilogue, sincos)
-INTER_COST = 3.0  # an inter entry: 4-byte index + an L2 gather
+# Cost model in units of one padded intra entry, fitted to per-CTA cycle
+# counts of the stage kernel (tools/prof_cta.py; profiles/r01_v9_cta_phase_profile.txt):
+# cycles ~ 16.3 rows + 0.224 entries + 1.9 inter + 8.7e3 segments
+ROW_COST = 73.0  # per-row overhead (pipeline, reduction, epilogue, sincos)
+INTER_COST = 8.4  # an inter entry: 4-byte index + a random 16-byte L2 gather
 DEFAULT_SMS = 148
 SMEM_OPTIN = 232448  # max dynamic + static shared memory per block (227 KB)
 
