@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 4
+#define CDK_ABI_VERSION 5
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -117,7 +117,7 @@ typedef struct cdk_graph {
   int32_t cta_threads;          /* 1024 */
   int32_t smem_nodes;           /* window capacity (nodes, multiple of 8) */
   int32_t seg_rows_cap;         /* max rows per segment (multiple of 8) */
-  const int64_t *rblk_row0;     /* [n_rblk] */
+  const int64_t *rblk_row0;     /* [n_rblk+1]: rblock b = rows [rblk_row0[b], rblk_row0[b+1]) */
   const int32_t *rblk_comm;     /* [n_rblk], -1 = NONE pool */
   const int32_t *comm_rblk_off; /* [n_comm+1] */
   const int32_t *seg_rblk;      /* [n_seg+1] rblock boundaries of segments */
@@ -161,6 +161,17 @@ CDK_API int cdk_kuramoto_rk4(const cdk_graph *g, double *theta, const double *om
 CDK_API int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const double *omega,
                                    double k_over_n, double dt, int stage, void *workspace,
                                    void *stream);
+
+/* byte offsets inside the workspace of [z0, z1, ksum, part0, part1, status]
+ * (offsets: [host] int64[6]); z_s buffers hold exp(i theta) of the stage state,
+ * stage k (1..4) reads z[(k-1)&1] and writes z[k&1].  Used by multi-rank
+ * drivers to exchange each rank's freshly written rows after a stage. */
+CDK_API int cdk_kuramoto_workspace_layout(const cdk_graph *g, int64_t *offsets);
+
+/* add n_steps to the workspace step counter (for drivers calling
+ * cdk_kuramoto_rk4_stage directly; keeps BlowUp step numbers right). */
+CDK_API int cdk_kuramoto_advance(const cdk_graph *g, void *workspace, int64_t n_steps,
+                                 void *stream);
 
 /* n_steps explicit Euler steps, same wrap/blow-up semantics. */
 CDK_API int cdk_kuramoto_euler(const cdk_graph *g, double *theta, const double *omega, double k_over_n,

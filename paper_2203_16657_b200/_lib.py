@@ -66,6 +66,8 @@ _SIGS = {
     "cdk_kuramoto_rhs": [ctypes.POINTER(CdkGraph), P, P, D, P, P, P],
     "cdk_kuramoto_rk4": [ctypes.POINTER(CdkGraph), P, P, D, D, I64, P, P],
     "cdk_kuramoto_rk4_stage": [ctypes.POINTER(CdkGraph), P, P, D, D, I, P, P],
+    "cdk_kuramoto_workspace_layout": [ctypes.POINTER(CdkGraph), P],
+    "cdk_kuramoto_advance": [ctypes.POINTER(CdkGraph), P, I64, P],
     "cdk_kuramoto_euler": [ctypes.POINTER(CdkGraph), P, P, D, D, I64, P, P],
     "cdk_kuramoto_status": [ctypes.POINTER(CdkGraph), P, ctypes.POINTER(CdkRunStatus), P],
     "cdk_host_bank_order": [P, P, I64, I32, I32],
@@ -83,7 +85,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _lock = threading.Lock()
 _lib = None

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
   for (int s = segA; s < segB; ++s) {
     const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
     const int64_t row0 = g.rblk_row0[rbA];
-    const int64_t row1 = (rbB < g.n_rblk) ? g.rblk_row0[rbB] : g.n_rows;
+    const int64_t row1 = g.rblk_row0[rbB];
     const int64_t row0a = row0 & ~(int64_t)1;
     const int64_t w0 = g.seg_win[2 * s], w1 = g.seg_win[2 * s + 1];
     const bool staged = w1 > w0;
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
     const double kn = a.k_over_n;
     for (int rb = rbA + warp; rb < rbB; rb += NWARPS) {
       const int64_t rrow0 = g.rblk_row0[rb];
-      const int64_t rrow1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+      const int64_t rrow1 = g.rblk_row0[rb + 1];
       const int nr = (int)(rrow1 - rrow0);
       const int c = g.rblk_comm[rb];
       double zr = 0.0, zim = 0.0;
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(256) prepare_kernel(cdk_graph g, const double 
   if (rb >= g.n_rblk) return;  // whole 8-lane groups exit together
   const unsigned gmask = 0xFFu << (threadIdx.x & 24);
   const int64_t row0 = g.rblk_row0[rb];
-  const int64_t row1 = (rb + 1 < g.n_rblk) ? g.rblk_row0[rb + 1] : g.n_rows;
+  const int64_t row1 = g.rblk_row0[rb + 1];
   const int nr = (int)(row1 - row0);
   double zr[4], zi[4];
 #pragma unroll
@@ -729,4 +729,30 @@ extern "C" int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const d
 // of the most recent stage launch are written to prof (device, 4*n_cta u64).
 extern "C" CDK_API void cdk_debug_set_profile_buffer(void *prof) {
   g_prof = reinterpret_cast<unsigned long long *>(prof);
+}
+
+// Byte offsets of the workspace views (z[0], z[1], ksum, part[0], part[1],
+// status) so a host driver can exchange stage state between ranks.
+extern "C" int cdk_kuramoto_workspace_layout(const cdk_graph *g, int64_t *offsets) {
+  if (!g || !offsets) return CDK_INPUT;
+  char *base = reinterpret_cast<char *>(0x1000);  // any non-null base
+  Workspace w = carve(g, base, nullptr);
+  offsets[0] = reinterpret_cast<char *>(w.z[0]) - base;
+  offsets[1] = reinterpret_cast<char *>(w.z[1]) - base;
+  offsets[2] = reinterpret_cast<char *>(w.ksum) - base;
+  offsets[3] = reinterpret_cast<char *>(w.part[0]) - base;
+  offsets[4] = reinterpret_cast<char *>(w.part[1]) - base;
+  offsets[5] = reinterpret_cast<char *>(w.status) - base;
+  return CDK_OK;
+}
+
+// advance the workspace's step counter (drivers that run stages one by one)
+extern "C" int cdk_kuramoto_advance(const cdk_graph *g, void *workspace, int64_t n_steps,
+                                    void *stream) {
+  int rc = check_graph(g);
+  if (rc) return rc;
+  Workspace w = carve(g, workspace, nullptr);
+  advance_kernel<<<1, 1, 0, as_stream(stream)>>>(w.status, n_steps);
+  CDK_CHECK_LAUNCH("advance_kernel");
+  return CDK_OK;
 }

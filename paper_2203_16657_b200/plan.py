@@ -58,7 +58,7 @@ class HostLayout:
 
     @property
     def n_rblk(self) -> int:
-        return int(self.rblk_row0.shape[0])
+        return int(self.rblk_row0.shape[0] - 1)
 
     def nbytes(self) -> int:
         return int(sum(a.nbytes for a in (self.comm_off, self.intra_ptr, self.intra_col,
@@ -119,7 +119,10 @@ def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
     return np.sort(np.concatenate([row0, np.asarray(extra, dtype=np.int64)]))
 
 
-def build_layout(dec: Decomposition) -> HostLayout:
+def build_layout(dec: Decomposition, row_range=None) -> HostLayout:
+    """Device layout of the directed S.  ``row_range=(lo, hi)`` keeps only rows
+    in [lo, hi) (a rank's shard: whole communities; other rows are present but
+    empty, columns stay global)."""
     part = dec.partition
     n = int(dec.n_nodes)
     off = part.offsets
@@ -128,6 +131,10 @@ def build_layout(dec: Decomposition) -> HostLayout:
         raise InputError("community larger than 65534 nodes: uint16 intra columns do not fit")
     comm = part.comm_of_permuted()
     rows, cols, sg = dec.directed()
+    lo, hi = (0, n) if row_range is None else (int(row_range[0]), int(row_range[1]))
+    if row_range is not None:
+        keep = (rows >= lo) & (rows < hi)
+        rows, cols, sg = rows[keep], cols[keep], sg[keep]
     cr = comm[rows]
     intra = (cr == comm[cols]) & (cr != NONE)
     if np.any(sg[intra] != -1) or np.any(sg[~intra] != 1):
@@ -158,10 +165,13 @@ def build_layout(dec: Decomposition) -> HostLayout:
     xcounts, inter_ptr = _row_runs(rx, n)
     nnz_inter = int(rx.shape[0])
 
-    # rblocks: communities, then the NONE pool
+    # rblocks: communities, then the NONE pool (only rows of [lo, hi))
     n_in = int(off[-1])
     sizes = np.diff(off)
-    nb = (sizes + RB - 1) // RB
+    owned = (off[:-1] >= lo) & (off[1:] <= hi)
+    if row_range is not None and np.any((off[:-1] < hi) & (off[1:] > lo) & ~owned):
+        raise InputError("a shard's row range must not split a community")
+    nb = np.where(owned, (sizes + RB - 1) // RB, 0)
     comm_rblk_off = np.zeros(m + 1, dtype=np.int64)
     np.cumsum(nb, out=comm_rblk_off[1:])
     rc = np.repeat(np.arange(m, dtype=np.int64), nb)
@@ -171,8 +181,10 @@ def build_layout(dec: Decomposition) -> HostLayout:
     row0 = _split_heavy_rblocks(row0, off[rc + 1] if rc.size else row0, intra_ptr, inter_ptr)
     rc = np.searchsorted(off, row0, side="right").astype(np.int64) - 1
     comm_rblk_off = np.searchsorted(row0, off).astype(np.int64)
-    pool_row0 = np.arange(n_in, n, RB, dtype=np.int64)
-    rblk_row0 = np.concatenate([row0, pool_row0])
+    pool_row0 = np.arange(max(n_in, lo), max(min(n, hi), max(n_in, lo)), RB, dtype=np.int64)
+    # rblk_row0 carries a sentinel: rblock b spans [rblk_row0[b], rblk_row0[b+1])
+    end = min(n, hi) if row_range is not None else n
+    rblk_row0 = np.concatenate([row0, pool_row0, [end]]).astype(np.int64)
     rblk_comm = np.concatenate([rc, np.full(pool_row0.shape[0], -1, np.int64)]).astype(np.int32)
     row_cost = padded.astype(np.float64) + INTER_COST * xcounts + ROW_COST
     return HostLayout(n, m, off.astype(np.int64), intra_ptr, intra_col, inter_ptr, inter_col,
@@ -193,7 +205,7 @@ def stage_smem_bytes(smem_nodes: int, rows_cap: int = ROWS_CAP) -> int:
 
 
 def _rblk_rows(lay: HostLayout) -> np.ndarray:
-    return np.concatenate([lay.rblk_row0, [lay.n_rows]]).astype(np.int64)
+    return lay.rblk_row0  # n_rblk + 1 entries (sentinel = end of the last rblock)
 
 
 def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int = ROWS_CAP,
@@ -250,10 +262,12 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
 
     # rebase intra columns (community-local in the layout) to each row's segment base
     n = lay.n_rows
-    seg_of_row = np.repeat(np.arange(seg_base.shape[0]), np.diff(rows[seg_rblk]))
-    comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
-    cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
-    delta = (cstart - seg_base[seg_of_row]) if n else np.empty(0, np.int64)
+    delta = np.zeros(n, dtype=np.int64)  # rows outside the rblocks (other shards) stay 0
+    if nrb:
+        seg_of_row = np.repeat(np.arange(seg_base.shape[0]), np.diff(rows[seg_rblk]))
+        comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
+        cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
+        delta[rows[0]: rows[-1]] = cstart - seg_base[seg_of_row]
     col = lay.intra_col.copy()
     if np.any(delta != 0):
         d_ent = np.repeat(delta, np.diff(lay.intra_ptr))
@@ -289,7 +303,8 @@ class DeviceGraph:
     """Device-resident layout + schedule; owns the torch tensors behind the
     cdk_graph struct handed to the C ABI."""
 
-    def __init__(self, dec: Decomposition, device=None, sm_count: int | None = None):
+    def __init__(self, dec: Decomposition, device=None, sm_count: int | None = None,
+                 row_range=None):
         import torch
 
         from ._lib import CdkGraph
@@ -297,8 +312,9 @@ class DeviceGraph:
         dev = torch.device(device if device is not None else "cuda")
         if sm_count is None:
             sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-        lay = build_layout(dec)
+        lay = build_layout(dec, row_range=row_range)
         sch = build_schedule(lay, sm_count=sm_count)
+        self.row_range = (0, lay.n_rows) if row_range is None else tuple(int(x) for x in row_range)
         self.layout = lay
         self.schedule = sch
         self.n_rows = lay.n_rows

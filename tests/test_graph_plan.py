@@ -143,7 +143,7 @@ def test_bank_order_permutes_within_rows_and_spreads_banks():
 
 def _schedule_to_directed(lay, sch):
     """Directed S reconstructed from the device columns (rebased to segment bases)."""
-    rows_rb = np.concatenate([lay.rblk_row0, [lay.n_rows]])
+    rows_rb = lay.rblk_row0
     seg_rows = rows_rb[sch.seg_rblk]
     rows, cols = [], []
     for s in range(sch.n_seg):
@@ -170,7 +170,7 @@ def test_schedule_invariants(sm_count, seed, rows_cap):
     nrb = lay.n_rblk
     seg = sch.seg_rblk
     assert seg[0] == 0 and seg[-1] == nrb and np.all(np.diff(seg) > 0)
-    rows_rb = np.concatenate([lay.rblk_row0, [lay.n_rows]])
+    rows_rb = lay.rblk_row0
     off = lay.comm_off
     for s in range(sch.n_seg):
         cs = lay.rblk_comm[seg[s]:seg[s + 1]]
@@ -187,7 +187,8 @@ def test_schedule_invariants(sm_count, seed, rows_cap):
     assert sch.n_cta == cta.shape[0] - 1
     # rblocks: <= 32 rows, never straddle communities, cover all rows once
     ends = rows_rb[1:]
-    assert np.all(ends - lay.rblk_row0 <= 32) and np.all(ends > lay.rblk_row0)
+    assert np.all(ends - rows_rb[:-1] <= 32) and np.all(ends > rows_rb[:-1])
+    assert rows_rb[-1] == lay.n_rows
     # rebased device columns still encode exactly the directed S
     r, c = _schedule_to_directed(lay, sch)
     rows, cols, _ = dec.directed()

@@ -16,7 +16,7 @@ for it in range(3):
     eng.rk4_stage(c.dt, 1)
 torch.cuda.synchronize()
 P = prof.view(-1, 4).cpu().numpy().astype(np.float64)
-rows = np.concatenate([lay.rblk_row0, [lay.n_rows]])
+rows = lay.rblk_row0
 seg_rows = rows[sch.seg_rblk]
 feat = []
 for b in range(sch.n_cta):
