@@ -182,6 +182,44 @@ CDK_API int cdk_kuramoto_status(const cdk_graph *g, const void *workspace, cdk_r
                         void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* Higher-order (triadic) Kuramoto on 3-cliques (BASELINE config 3)          */
+/*   theta'_i = omega_i + K1/N sum_j a_ij sin(theta_j - theta_i)             */
+/*            + K2/N^2 sum_{ordered (j,k): {i,j,k} triangle}                 */
+/*                      sin(theta_j + theta_k - 2 theta_i)                   */
+/* CIA form: in-community triangles by inclusion-exclusion over the missing  */
+/* graph (two CSR passes + missing-graph triangles), spanning triangles      */
+/* listed explicitly.  No reference kernel exists for this model (the       */
+/* reference's ho_naive_block, _kernels.py:398-428, is the all-to-all block  */
+/* sum; it pins the dense part in the tests).                                */
+/* ------------------------------------------------------------------------ */
+typedef struct cdk_ho_graph {
+  int64_t n_rows;
+  int32_t n_rblk;
+  int32_t n_comm;
+  const int64_t *rblk_row0;      /* [n_rblk+1] */
+  const int32_t *rblk_comm;      /* [n_rblk], -1 = NONE pool */
+  const int32_t *comm_rblk_off;  /* [n_comm+1] */
+  const int64_t *miss_ptr;       /* [n_rows+1] proper missing intra edges */
+  const int32_t *miss_col;       /* global columns */
+  const int64_t *inter_ptr;      /* [n_rows+1] */
+  const int32_t *inter_col;      /* global columns */
+  const int64_t *tri_ptr;        /* [n_rows+1] triangle pairs per row */
+  const int32_t *tri_jk;         /* int32 pairs (j,k); j < 0: spanning triangle, j = -j-1 */
+} cdk_ho_graph;
+
+CDK_API size_t cdk_ho_workspace_bytes(const cdk_ho_graph *g);
+CDK_API int cdk_ho_prepare(const cdk_ho_graph *g, const double *theta, void *workspace,
+                           void *stream);
+CDK_API int cdk_ho_rhs(const cdk_ho_graph *g, const double *theta, const double *omega,
+                       double k1_over_n, double k2_over_n2, double *out, void *workspace,
+                       void *stream);
+CDK_API int cdk_ho_rk4(const cdk_ho_graph *g, double *theta, const double *omega,
+                       double k1_over_n, double k2_over_n2, double dt, int64_t n_steps,
+                       void *workspace, void *stream);
+CDK_API int cdk_ho_status(const cdk_ho_graph *g, const void *workspace, cdk_run_status *out,
+                          void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* host-side planning (no device needed)                                    */
 /* ------------------------------------------------------------------------ */
 
@@ -190,6 +228,13 @@ CDK_API int cdk_kuramoto_status(const cdk_graph *g, const void *workspace, cdk_r
  * groups (column mod 8); pads (pad_value) count as bank pad_bank. */
 CDK_API int cdk_host_bank_order(uint16_t *cols, const int64_t *ptr, int64_t n_rows,
                                 int32_t pad_value, int32_t pad_bank);
+
+/* [host] triangles {i<j<k} of a symmetric CSR (sorted global columns, no
+ * self loops); writes <= cap int32 triples to out (NULL ok), returns the count
+ * (-1 on bad input).  Used to enumerate the missing-edge-graph triangles of
+ * the higher-order (triadic) model. */
+CDK_API int64_t cdk_host_triangles(const int64_t *ptr, const int32_t *cols, int64_t n,
+                                   int32_t *out, int64_t cap);
 
 /* ------------------------------------------------------------------------ */
 /* misc                                                                      */

@@ -36,6 +36,10 @@ def __getattr__(name):  # lazy: these import torch / the CUDA library
         from . import integrator
 
         return getattr(integrator, name)
+    if name in ("HigherOrderKuramoto", "ho_kuramoto_model", "HOEngine"):
+        from . import ho
+
+        return getattr(ho, name)
     if name == "KuramotoEngine":
         from .engine import KuramotoEngine
 

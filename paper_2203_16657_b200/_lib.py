@@ -47,6 +47,23 @@ class CdkGraph(ctypes.Structure):
     ]
 
 
+class CdkHoGraph(ctypes.Structure):
+    _fields_ = [
+        ("n_rows", I64),
+        ("n_rblk", I32),
+        ("n_comm", I32),
+        ("rblk_row0", P),
+        ("rblk_comm", P),
+        ("comm_rblk_off", P),
+        ("miss_ptr", P),
+        ("miss_col", P),
+        ("inter_ptr", P),
+        ("inter_col", P),
+        ("tri_ptr", P),
+        ("tri_jk", P),
+    ]
+
+
 class CdkRunStatus(ctypes.Structure):
     _fields_ = [("nonfinite", I64), ("first_bad_step", I64), ("steps_done", I64),
                 ("reserved", I64)]
@@ -72,6 +89,12 @@ _SIGS = {
     "cdk_kuramoto_status": [ctypes.POINTER(CdkGraph), P, ctypes.POINTER(CdkRunStatus), P],
     "cdk_host_bank_order": [P, P, I64, I32, I32],
     "cdk_debug_set_profile_buffer": [P],
+    "cdk_host_triangles": [P, P, I64, P, I64],
+    "cdk_ho_workspace_bytes": [ctypes.POINTER(CdkHoGraph)],
+    "cdk_ho_prepare": [ctypes.POINTER(CdkHoGraph), P, P, P],
+    "cdk_ho_rhs": [ctypes.POINTER(CdkHoGraph), P, P, D, D, P, P, P],
+    "cdk_ho_rk4": [ctypes.POINTER(CdkHoGraph), P, P, D, D, D, I64, P, P],
+    "cdk_ho_status": [ctypes.POINTER(CdkHoGraph), P, ctypes.POINTER(CdkRunStatus), P],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],
@@ -82,6 +105,8 @@ _RESTYPES = {
     "cdk_last_error": ctypes.c_char_p,
     "cdk_launch_count": I64,
     "cdk_debug_set_profile_buffer": None,
+    "cdk_host_triangles": I64,
+    "cdk_ho_workspace_bytes": ctypes.c_size_t,
 }
 
 EXPORTED = tuple(_SIGS)

@@ -80,4 +80,45 @@ def scaled_config2(n: int, m: int, seed: int = 7) -> KuramotoCase:
     return KuramotoCase(f"cfg2_n{n}", sizes, 0.95, p_out, 5.0, 0.01, 2000, seed + 1, seed + 2)
 
 
-CONFIGS = {"cfg1": config1, "cfg2": config2}
+@dataclass(frozen=True)
+class HOCase:
+    """Higher-order (triadic) Kuramoto on 3-cliques (BASELINE configs[2])."""
+
+    name: str
+    sizes: tuple
+    p_in: float
+    p_out: float
+    k1: float
+    k2: float
+    dt: float
+    steps: int
+    graph_seed: int
+    state_seed: int
+
+    @property
+    def n(self) -> int:
+        return int(sum(self.sizes))
+
+    def decomposition(self):
+        return planted_partition_decomposition(self.sizes, self.p_in, self.p_out, self.graph_seed)
+
+    def state(self):
+        """omega ~ N(0,1) (BASELINE leaves it open), theta0 ~ U[0, 2pi)."""
+        rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(self.state_seed)))
+        omega = rng.standard_normal(self.n)
+        theta0 = rng.uniform(0.0, 2.0 * math.pi, self.n)
+        return omega, theta0
+
+
+def config3() -> HOCase:
+    """SBM N=50000, 100 x 500, p_in .9, p_out 1e-4; K1=1, K2=.5; RK4 dt .005 x 1000."""
+    return HOCase("cfg3", (500,) * 100, 0.9, 1e-4, 1.0, 0.5, 0.005, 1000, 3001, 3101)
+
+
+def scaled_config3(m: int = 8, lam: int = 120, p_out: float = 2e-3, seed: int = 31) -> HOCase:
+    """Config-3 family at a size the O(N^3) direct oracle handles."""
+    return HOCase(f"cfg3_{m}x{lam}", (lam,) * m, 0.9, p_out, 1.0, 0.5, 0.005, 1000, seed,
+                  seed + 1)
+
+
+CONFIGS = {"cfg1": config1, "cfg2": config2, "cfg3": config3}

@@ -50,3 +50,41 @@ extern "C" CDK_API int cdk_host_bank_order(uint16_t *cols, const int64_t *ptr, i
   }
   return CDK_OK;
 }
+
+// Triangles {i < j < k} of an undirected graph given as a symmetric CSR with
+// sorted global columns (no self loops).  Writes up to `cap` triangles as
+// int32 triples to out (may be NULL) and returns the total count (or -1 on
+// bad input).  O(sum over edges of min degree) via sorted-list intersection.
+extern "C" CDK_API int64_t cdk_host_triangles(const int64_t *ptr, const int32_t *cols,
+                                              int64_t n, int32_t *out, int64_t cap) {
+  if (!ptr || (!cols && ptr[n] > 0) || n < 0) return -1;
+  int64_t count = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t *ni = cols + ptr[i], *ni_end = cols + ptr[i + 1];
+    const int32_t *jt = std::upper_bound(ni, ni_end, (int32_t)i);
+    for (; jt < ni_end; ++jt) {
+      const int32_t j = *jt;
+      // common neighbours k > j of i and j
+      const int32_t *a = std::upper_bound(jt + 1 - 1, ni_end, j);
+      const int32_t *b = std::upper_bound(cols + ptr[j], cols + ptr[j + 1], j);
+      const int32_t *b_end = cols + ptr[j + 1];
+      while (a < ni_end && b < b_end) {
+        if (*a < *b) {
+          ++a;
+        } else if (*b < *a) {
+          ++b;
+        } else {
+          if (out && count < cap) {
+            out[3 * count] = (int32_t)i;
+            out[3 * count + 1] = j;
+            out[3 * count + 2] = *a;
+          }
+          ++count;
+          ++a;
+          ++b;
+        }
+      }
+    }
+  }
+  return count;
+}

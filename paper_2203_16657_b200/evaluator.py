@@ -40,14 +40,39 @@ def _engine(model: Kuramoto, dec: Decomposition) -> KuramotoEngine:
     return eng
 
 
+def _ho_engine(model, dec: Decomposition):
+    from .ho import HOEngine, HoDeviceGraph
+
+    cached = dec._cache.get("ho_engine")
+    eng = cached[1] if cached is not None and cached[0] is model else None
+    if eng is None:
+        dg = dec._cache.get("ho_graph")
+        if dg is None:
+            dg = dec._cache["ho_graph"] = HoDeviceGraph(dec)
+        perm = dec.partition.perm
+        eng = HOEngine(dec, np.asarray(model.omega)[perm], model.k1, model.k2,
+                       norm=model.norm_value(), graph=dg)
+        dec._cache["ho_engine"] = (model, eng)
+    return eng
+
+
+def engine_for(model, dec: Decomposition):
+    """The device engine of a model (Kuramoto or higher-order Kuramoto)."""
+    from .ho import HigherOrderKuramoto
+
+    if isinstance(model, Kuramoto):
+        return _engine(model, dec)
+    if isinstance(model, HigherOrderKuramoto):
+        return _ho_engine(model, dec)
+    raise InputError(f"unsupported model {type(model).__name__}")
+
+
 def eval_rhs_cia(model, dec: Decomposition, state) -> np.ndarray:
-    if not isinstance(model, Kuramoto):
-        raise InputError(f"eval_rhs_cia: unsupported model {type(model).__name__}")
     x = np.asarray(state, dtype=np.float64)
     if x.shape != (dec.n_nodes,):
         raise InputError("state shape does not match the decomposition")
     perm = dec.partition.perm
-    eng = _engine(model, dec)
+    eng = engine_for(model, dec)
     out_perm = eng.rhs(x[perm]).cpu().numpy()
     out = np.empty_like(out_perm)
     out[perm] = out_perm

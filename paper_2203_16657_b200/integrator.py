@@ -19,9 +19,8 @@ import numpy as np
 
 from . import _lib
 from .errors import InputError
-from .evaluator import _engine
+from .evaluator import engine_for
 from .graph import Decomposition
-from .models import Kuramoto
 
 
 @dataclass(frozen=True)
@@ -63,14 +62,14 @@ def integrate(model, dec: Decomposition, x0, plan: IntegrationPlan) -> Trajector
         raise InputError("integrate: only mode='cia' runs on the device path")
     if plan.scheme not in ("rk4", "euler"):
         raise InputError(f"unknown scheme {plan.scheme!r}")
-    if not isinstance(model, Kuramoto):
-        raise InputError(f"integrate: unsupported model {type(model).__name__}")
     x0 = np.asarray(x0, dtype=np.float64)
     if x0.shape != (dec.n_nodes,):
         raise InputError("x0 shape does not match the decomposition")
     n_steps, dt, dt_last = plan.step_sizes()
     perm = dec.partition.perm
-    eng = _engine(model, dec)
+    eng = engine_for(model, dec)
+    if plan.scheme == "euler" and not hasattr(eng, "euler"):
+        raise InputError("Euler is implemented for the classical Kuramoto engine only")
     lib = eng.lib
     launches0 = int(lib.cdk_launch_count())
     t0 = time.perf_counter()
