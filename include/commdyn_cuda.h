@@ -220,6 +220,47 @@ CDK_API int cdk_ho_status(const cdk_ho_graph *g, const void *workspace, cdk_run_
                           void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* Cucker-Smale flocking, 2-D (BASELINE config 4)                            */
+/*   s' = v,  v'_m = inv_n sum_l a_ml eta(|s_l - s_m|^2)(v_l - v_m),         */
+/*   eta(y) = K / (sigma2 + y)^beta.                                          */
+/* CIA with a per-community degree-8 polynomial of eta in the scaled squared */
+/* distance (host P2 fit, paper_2203_16657_b200/cs.py): bivariate moments up */
+/* to degree 16, contraction T_c (153 x 153), bivariate evaluation per node, */
+/* EXACT sparse correction (replaces pairs_cs, _kernels.py:297-314, on S).   */
+/* ------------------------------------------------------------------------ */
+typedef struct cdk_cs_graph {
+  int64_t n_rows;
+  int64_t n_comm;
+  int32_t n_rblk;
+  int32_t reserved;
+  const int64_t *comm_off;      /* [n_comm+1] */
+  const int64_t *rblk_row0;     /* [n_rblk+1] */
+  const int32_t *rblk_comm;     /* [n_rblk] */
+  const int64_t *miss_ptr;      /* [n_rows+1] missing intra edges (sign -1) */
+  const int32_t *miss_col;
+  const int64_t *inter_ptr;     /* [n_rows+1] inter / NONE-pool edges (sign +1) */
+  const int32_t *inter_col;
+  const double *mu;             /* [n_comm][2] community centres */
+  const double *inv_L;          /* [n_comm] 1 / scale */
+  const double *T;              /* [n_comm][153][153] contraction tensors */
+} cdk_cs_graph;
+
+CDK_API size_t cdk_cs_workspace_bytes(const cdk_cs_graph *g);
+/* reset the run status (domain-violation and blow-up counters) */
+CDK_API int cdk_cs_prepare(const cdk_cs_graph *g, void *workspace, void *stream);
+/* out (double[n][2]) = v' at (pos, vel) (double[n][2]); status.reserved counts
+ * nodes outside the expansion domain (DomainViolationError). */
+CDK_API int cdk_cs_rhs(const cdk_cs_graph *g, const double *pos, const double *vel, double K,
+                       double sigma2, double beta, double inv_n, double *out, void *workspace,
+                       void *stream);
+/* n_steps RK4 steps of (pos, vel) in place */
+CDK_API int cdk_cs_rk4(const cdk_cs_graph *g, double *pos, double *vel, double K, double sigma2,
+                       double beta, double inv_n, double dt, int64_t n_steps, void *workspace,
+                       void *stream);
+CDK_API int cdk_cs_status(const cdk_cs_graph *g, const void *workspace, cdk_run_status *out,
+                          void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* host-side planning (no device needed)                                    */
 /* ------------------------------------------------------------------------ */
 

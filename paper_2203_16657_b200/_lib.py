@@ -64,6 +64,25 @@ class CdkHoGraph(ctypes.Structure):
     ]
 
 
+class CdkCsGraph(ctypes.Structure):
+    _fields_ = [
+        ("n_rows", I64),
+        ("n_comm", I64),
+        ("n_rblk", I32),
+        ("reserved", I32),
+        ("comm_off", P),
+        ("rblk_row0", P),
+        ("rblk_comm", P),
+        ("miss_ptr", P),
+        ("miss_col", P),
+        ("inter_ptr", P),
+        ("inter_col", P),
+        ("mu", P),
+        ("inv_L", P),
+        ("T", P),
+    ]
+
+
 class CdkRunStatus(ctypes.Structure):
     _fields_ = [("nonfinite", I64), ("first_bad_step", I64), ("steps_done", I64),
                 ("reserved", I64)]
@@ -95,6 +114,11 @@ _SIGS = {
     "cdk_ho_rhs": [ctypes.POINTER(CdkHoGraph), P, P, D, D, P, P, P],
     "cdk_ho_rk4": [ctypes.POINTER(CdkHoGraph), P, P, D, D, D, I64, P, P],
     "cdk_ho_status": [ctypes.POINTER(CdkHoGraph), P, ctypes.POINTER(CdkRunStatus), P],
+    "cdk_cs_workspace_bytes": [ctypes.POINTER(CdkCsGraph)],
+    "cdk_cs_prepare": [ctypes.POINTER(CdkCsGraph), P, P],
+    "cdk_cs_rhs": [ctypes.POINTER(CdkCsGraph), P, P, D, D, D, D, P, P, P],
+    "cdk_cs_rk4": [ctypes.POINTER(CdkCsGraph), P, P, D, D, D, D, D, I64, P, P],
+    "cdk_cs_status": [ctypes.POINTER(CdkCsGraph), P, ctypes.POINTER(CdkRunStatus), P],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],
@@ -107,6 +131,7 @@ _RESTYPES = {
     "cdk_debug_set_profile_buffer": None,
     "cdk_host_triangles": I64,
     "cdk_ho_workspace_bytes": ctypes.c_size_t,
+    "cdk_cs_workspace_bytes": ctypes.c_size_t,
 }
 
 EXPORTED = tuple(_SIGS)

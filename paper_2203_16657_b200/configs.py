@@ -121,4 +121,49 @@ def scaled_config3(m: int = 8, lam: int = 120, p_out: float = 2e-3, seed: int = 
                   seed + 1)
 
 
-CONFIGS = {"cfg1": config1, "cfg2": config2, "cfg3": config3}
+@dataclass(frozen=True)
+class CSCase:
+    """Cucker-Smale 2-D (BASELINE configs[3])."""
+
+    name: str
+    sizes: tuple
+    p_in: float
+    p_out: float
+    K: float
+    sigma: float
+    beta: float
+    dt: float
+    steps: int
+    graph_seed: int
+    state_seed: int
+
+    @property
+    def n(self) -> int:
+        return int(sum(self.sizes))
+
+    @property
+    def t_end(self) -> float:
+        return self.dt * self.steps
+
+    def decomposition(self):
+        return planted_partition_decomposition(self.sizes, self.p_in, self.p_out, self.graph_seed)
+
+    def state(self):
+        """positions ~ U[0,10]^2, velocities ~ N(0,1)^2."""
+        rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(self.state_seed)))
+        pos = rng.uniform(0.0, 10.0, (self.n, 2))
+        vel = rng.standard_normal((self.n, 2))
+        return pos, vel
+
+
+def config4() -> CSCase:
+    """SBM N=100000, 100 x 1000, p_in .9, p_out 1e-4; psi=(1+r^2)^-1/4; RK4 dt .01 x 500."""
+    return CSCase("cfg4", (1000,) * 100, 0.9, 1e-4, 1.0, 1.0, 0.25, 0.01, 500, 4001, 4101)
+
+
+def scaled_config4(m: int = 5, lam: int = 80, p_out: float = 3e-3, seed: int = 41) -> CSCase:
+    return CSCase(f"cfg4_{m}x{lam}", (lam,) * m, 0.9, p_out, 1.0, 1.0, 0.25, 0.01, 500, seed,
+                  seed + 1)
+
+
+CONFIGS = {"cfg1": config1, "cfg2": config2, "cfg3": config3, "cfg4": config4}

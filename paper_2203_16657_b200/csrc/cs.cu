@@ -1,0 +1,413 @@
+// Cucker–Smale flocking (2-D) with the per-community polynomial expansion of
+// the coupling (BASELINE config 4), CIA form, fused into RK4.
+// Math and notation: paper_2203_16657_b200/cs.py.  Per stage:
+//   1. cs_moments_kernel: M^f_{ij} = sum_{l in c} x_l^i y_l^j f_l (f = 1, vx, vy),
+//      x, y = scaled centred positions, i + j <= 16 (153 monomials), one CTA
+//      per community, fixed node order;
+//   2. cs_contract_kernel: H^f = T_c M^f (153 x 153 per community);
+//   3. cs_rows_kernel: per row (8-lane group) the bivariate evaluation
+//      G^f(x_m, y_m) = sum H^f_{pq} x_m^p y_m^q split over lanes by p, the
+//      exact sparse correction sum_j s_mj eta(|s_j - s_m|^2)(v_j - v_m) over
+//      the missing (-1) and inter (+1) CSRs, the domain guard |p_m| <= 1 and
+//      the RK4 stage update of (s, v).
+// The reference kernel for the sparse part is pairs_cs (_kernels.py:297-314).
+#include "common.cuh"
+
+namespace cdk {
+
+constexpr int CS_D2 = 16;
+constexpr int CS_NMON = (CS_D2 + 1) * (CS_D2 + 2) / 2;  // 153
+constexpr int CS_NOUT = 3 * CS_NMON;                     // 459
+
+__constant__ unsigned char c_mono_i[CS_NMON];
+__constant__ unsigned char c_mono_j[CS_NMON];
+__constant__ short c_mono_row[CS_D2 + 2];  // first packed index of each i (i-major)
+
+struct CsArgs {
+  int64_t n_rows;
+  int32_t n_comm;
+  int32_t n_rblk;
+  const int64_t *comm_off;
+  const int64_t *rblk_row0;
+  const int32_t *rblk_comm;
+  const int64_t *miss_ptr;
+  const int32_t *miss_col;
+  const int64_t *inter_ptr;
+  const int32_t *inter_col;
+  const double2 *mu;
+  const double *inv_L;
+  const double *T;          // [M][153][153]
+  double *M;                // [M][3][153]
+  double *H;                // [M][3][153]
+  const double2 *s_in, *v_in;  // stage state
+  double2 *s_out, *v_out;
+  double2 *s0, *v0;         // step-start state (RK4 base; written at stage 4)
+  double2 *ks, *kv;         // RK4 accumulators
+  double2 *out;             // MODE 0: v'
+  cdk_run_status *status;   // reserved = domain violations
+  double K, sigma2, beta, inv_n, h;
+  int64_t step_rel;
+};
+
+__device__ __forceinline__ double eta_exact(double d2, double K, double sigma2, double beta) {
+  const double x = sigma2 + d2;
+  if (beta == 0.25) return K * rsqrt(sqrt(x));
+  return K / pow(x, beta);
+}
+
+__global__ void __launch_bounds__(256) cs_moments_kernel(const CsArgs a) {
+  __shared__ double px[128][CS_D2 + 1];
+  __shared__ double py[128][CS_D2 + 1];
+  __shared__ double pf[128][3];
+  const int c = blockIdx.x;
+  const int64_t b = a.comm_off[c], e = a.comm_off[c + 1];
+  const double2 mu = a.mu[c];
+  const double il = a.inv_L[c];
+  double acc[2] = {0.0, 0.0};
+  const int o0 = threadIdx.x, o1 = threadIdx.x + 256;
+  for (int64_t base = b; base < e; base += 128) {
+    const int cnt = (int)min((int64_t)128, e - base);
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const int n = threadIdx.x;
+      const double2 s = a.s_in[base + n];
+      const double2 v = a.v_in[base + n];
+      const double x = (s.x - mu.x) * il, y = (s.y - mu.y) * il;
+      double xp = 1.0, yp = 1.0;
+      for (int k = 0; k <= CS_D2; ++k) {
+        px[n][k] = xp;
+        py[n][k] = yp;
+        xp *= x;
+        yp *= y;
+      }
+      pf[n][0] = 1.0;
+      pf[n][1] = v.x;
+      pf[n][2] = v.y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int o = q ? o1 : o0;
+      if (o < CS_NOUT) {
+        const int f = o / CS_NMON, r = o % CS_NMON;
+        const int i = c_mono_i[r], j = c_mono_j[r];
+        double s = acc[q];
+        for (int n = 0; n < cnt; ++n) s += px[n][i] * py[n][j] * pf[n][f];
+        acc[q] = s;
+      }
+    }
+  }
+  if (o0 < CS_NOUT) a.M[(int64_t)c * CS_NOUT + o0] = acc[0];
+  if (o1 < CS_NOUT) a.M[(int64_t)c * CS_NOUT + o1] = acc[1];
+}
+
+__global__ void __launch_bounds__(512) cs_contract_kernel(const CsArgs a) {
+  const int c = blockIdx.x;
+  const int o = threadIdx.x;
+  if (o >= CS_NOUT) return;
+  const int f = o / CS_NMON, r = o % CS_NMON;
+  const double *Tr = a.T + ((int64_t)c * CS_NMON + r) * CS_NMON;
+  const double *Mf = a.M + (int64_t)c * CS_NOUT + f * CS_NMON;
+  double s = 0.0;
+  for (int q = 0; q < CS_NMON; ++q) s += Tr[q] * Mf[q];
+  a.H[(int64_t)c * CS_NOUT + o] = s;
+}
+
+// MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.
+template <int MODE>
+__global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
+  const int lane = threadIdx.x & 31, t = lane & 7;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  // rows of communities first, then NONE pool rows (no dense part)
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; i < a.n_rows;
+       i += ngroups) {
+    // community of row i (binary search over comm_off)
+    int c = -1;
+    if (a.n_comm > 0 && i < a.comm_off[a.n_comm]) {
+      int lo = 0, hi = a.n_comm;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.comm_off[mid] <= i) lo = mid; else hi = mid;
+      }
+      c = lo;
+    }
+    const double2 sm = a.s_in[i], vm = a.v_in[i];
+    double g0 = 0.0, gx = 0.0, gy = 0.0;
+    bool out_of_domain = false;
+    if (c >= 0) {
+      const double2 mu = a.mu[c];
+      const double il = a.inv_L[c];
+      const double x = (sm.x - mu.x) * il, y = (sm.y - mu.y) * il;
+      out_of_domain = (x * x + y * y) > 1.0 + 1e-12;
+      const double *Hc = a.H + (int64_t)c * CS_NOUT;
+      double xp = 1.0;
+      for (int k = 0; k < t; ++k) xp *= x;
+      double x8 = 1.0;
+      for (int k = 0; k < 8; ++k) x8 *= x;
+      for (int p = t; p <= CS_D2; p += 8) {
+        const int r0 = c_mono_row[p];
+        double yq = 1.0;
+        for (int q = 0; q <= CS_D2 - p; ++q) {
+          const double w = xp * yq;
+          g0 += Hc[r0 + q] * w;
+          gx += Hc[CS_NMON + r0 + q] * w;
+          gy += Hc[2 * CS_NMON + r0 + q] * w;
+          yq *= y;
+        }
+        xp *= x8;
+      }
+    }
+    // exact sparse correction
+    double ax = 0.0, ay = 0.0;
+    for (int64_t p = a.miss_ptr[i] + t; p < a.miss_ptr[i + 1]; p += 8) {
+      const int j = a.miss_col[p];
+      const double2 sj = a.s_in[j], vj = a.v_in[j];
+      const double dx = sj.x - sm.x, dy = sj.y - sm.y;
+      const double w = eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta);
+      ax -= w * (vj.x - vm.x);
+      ay -= w * (vj.y - vm.y);
+    }
+    for (int64_t p = a.inter_ptr[i] + t; p < a.inter_ptr[i + 1]; p += 8) {
+      const int j = a.inter_col[p];
+      const double2 sj = a.s_in[j], vj = a.v_in[j];
+      const double dx = sj.x - sm.x, dy = sj.y - sm.y;
+      const double w = eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta);
+      ax += w * (vj.x - vm.x);
+      ay += w * (vj.y - vm.y);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      g0 += __shfl_xor_sync(gmask, g0, o);
+      gx += __shfl_xor_sync(gmask, gx, o);
+      gy += __shfl_xor_sync(gmask, gy, o);
+      ax += __shfl_xor_sync(gmask, ax, o);
+      ay += __shfl_xor_sync(gmask, ay, o);
+    }
+    if (t == 0) {
+      if (out_of_domain) atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->reserved), 1ull);
+      const double accx = (gx - vm.x * g0) + ax, accy = (gy - vm.y * g0) + ay;
+      const double2 acc = make_double2(accx * a.inv_n, accy * a.inv_n);
+      if (MODE == 0) {
+        a.out[i] = acc;
+      } else {
+        const double2 s0 = a.s0[i], v0 = a.v0[i];
+        double2 ks, kv;
+        if (MODE == 1) {
+          ks = vm;
+          kv = acc;
+        } else {
+          const double2 ps = a.ks[i], pv = a.kv[i];
+          const double w = (MODE == 4) ? 1.0 : 2.0;
+          ks = make_double2(add_rn(ps.x, mul_rn(w, vm.x)), add_rn(ps.y, mul_rn(w, vm.y)));
+          kv = make_double2(add_rn(pv.x, mul_rn(w, acc.x)), add_rn(pv.y, mul_rn(w, acc.y)));
+        }
+        if (MODE < 4) {
+          a.ks[i] = ks;
+          a.kv[i] = kv;
+          a.s_out[i] = make_double2(add_rn(s0.x, mul_rn(a.h, vm.x)), add_rn(s0.y, mul_rn(a.h, vm.y)));
+          a.v_out[i] = make_double2(add_rn(v0.x, mul_rn(a.h, acc.x)), add_rn(v0.y, mul_rn(a.h, acc.y)));
+        } else {
+          const double2 sn = make_double2(add_rn(s0.x, mul_rn(a.h, ks.x)), add_rn(s0.y, mul_rn(a.h, ks.y)));
+          const double2 vn = make_double2(add_rn(v0.x, mul_rn(a.h, kv.x)), add_rn(v0.y, mul_rn(a.h, kv.y)));
+          a.s_out[i] = sn;
+          a.v_out[i] = vn;
+          if (!isfinite(sn.x) || !isfinite(sn.y) || !isfinite(vn.x) || !isfinite(vn.y)) {
+            atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->nonfinite), 1ull);
+            atomicMin(reinterpret_cast<long long *>(&a.status->first_bad_step),
+                      (long long)(a.status->steps_done + a.step_rel + 1));
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void cs_reset_status_kernel(cdk_run_status *st) {
+  st->nonfinite = 0;
+  st->first_bad_step = INT64_MAX;
+  st->steps_done = 0;
+  st->reserved = 0;
+}
+__global__ void cs_advance_kernel(cdk_run_status *st, int64_t n) { st->steps_done += n; }
+
+struct CsWs {
+  double2 *s[2], *v[2], *ks, *kv;
+  double *M, *H;
+  cdk_run_status *status;
+};
+
+static CsWs cs_carve(const cdk_cs_graph *g, void *base, size_t *total) {
+  CsWs w{};
+  size_t off = 0;
+  char *b = reinterpret_cast<char *>(base);
+  auto take = [&](size_t bytes) {
+    void *p = b ? b + off : nullptr;
+    off = (off + bytes + 255) / 256 * 256;
+    return p;
+  };
+  const size_t n = (size_t)g->n_rows + 1, m = (size_t)g->n_comm + 1;
+  for (int k = 0; k < 2; ++k) {
+    w.s[k] = (double2 *)take(n * 16);
+    w.v[k] = (double2 *)take(n * 16);
+  }
+  w.ks = (double2 *)take(n * 16);
+  w.kv = (double2 *)take(n * 16);
+  w.M = (double *)take(m * CS_NOUT * 8);
+  w.H = (double *)take(m * CS_NOUT * 8);
+  w.status = (cdk_run_status *)take(sizeof(cdk_run_status));
+  if (total) *total = off;
+  return w;
+}
+
+static bool g_cs_tables = false;
+static int cs_tables() {
+  if (g_cs_tables) return CDK_OK;
+  unsigned char mi[CS_NMON], mj[CS_NMON];
+  short row[CS_D2 + 2];
+  int k = 0;
+  for (int i = 0; i <= CS_D2; ++i) {
+    row[i] = (short)k;
+    for (int j = 0; j <= CS_D2 - i; ++j, ++k) {
+      mi[k] = (unsigned char)i;
+      mj[k] = (unsigned char)j;
+    }
+  }
+  row[CS_D2 + 1] = (short)k;
+  cudaError_t e = cudaMemcpyToSymbol(c_mono_i, mi, sizeof(mi));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mono_j, mj, sizeof(mj));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mono_row, row, sizeof(row));
+  if (e != cudaSuccess) return cuda_status(e, "cs constant tables");
+  g_cs_tables = true;
+  return CDK_OK;
+}
+
+static CsArgs cs_args(const cdk_cs_graph *g, const CsWs &w, double K, double sigma2, double beta,
+                      double inv_n) {
+  CsArgs a{};
+  a.n_rows = g->n_rows;
+  a.n_comm = (int32_t)g->n_comm;
+  a.n_rblk = g->n_rblk;
+  a.comm_off = g->comm_off;
+  a.rblk_row0 = g->rblk_row0;
+  a.rblk_comm = g->rblk_comm;
+  a.miss_ptr = g->miss_ptr;
+  a.miss_col = g->miss_col;
+  a.inter_ptr = g->inter_ptr;
+  a.inter_col = g->inter_col;
+  a.mu = reinterpret_cast<const double2 *>(g->mu);
+  a.inv_L = g->inv_L;
+  a.T = g->T;
+  a.M = w.M;
+  a.H = w.H;
+  a.ks = w.ks;
+  a.kv = w.kv;
+  a.status = w.status;
+  a.K = K;
+  a.sigma2 = sigma2;
+  a.beta = beta;
+  a.inv_n = inv_n;
+  return a;
+}
+
+static unsigned cs_row_grid(int64_t n) {
+  const int64_t groups_per_block = 256 / 8;
+  int64_t g = (n + groups_per_block - 1) / groups_per_block;
+  if (g > 148 * 16) g = 148 * 16;
+  return (unsigned)(g > 0 ? g : 1);
+}
+
+template <int MODE>
+static int cs_stage(CsArgs a, cudaStream_t st) {
+  if (a.n_comm > 0) {
+    cs_moments_kernel<<<a.n_comm, 256, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("cs_moments_kernel");
+    cs_contract_kernel<<<a.n_comm, 512, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("cs_contract_kernel");
+  }
+  cs_rows_kernel<MODE><<<cs_row_grid(a.n_rows), 256, 0, st>>>(a);
+  CDK_CHECK_LAUNCH("cs_rows_kernel");
+  return CDK_OK;
+}
+
+static int cs_check(const cdk_cs_graph *g) {
+  if (!g || g->n_rows < 0 || g->n_comm < 0) {
+    set_error("cdk_cs_graph: invalid sizes");
+    return CDK_INPUT;
+  }
+  return cs_tables();
+}
+
+}  // namespace cdk
+
+using namespace cdk;
+
+extern "C" size_t cdk_cs_workspace_bytes(const cdk_cs_graph *g) {
+  size_t total = 0;
+  cs_carve(g, nullptr, &total);
+  return total;
+}
+
+extern "C" int cdk_cs_prepare(const cdk_cs_graph *g, void *workspace, void *stream) {
+  int rc = cs_check(g);
+  if (rc) return rc;
+  CsWs w = cs_carve(g, workspace, nullptr);
+  cs_reset_status_kernel<<<1, 1, 0, as_stream(stream)>>>(w.status);
+  CDK_CHECK_LAUNCH("cs_reset_status_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_cs_rhs(const cdk_cs_graph *g, const double *pos, const double *vel, double K,
+                          double sigma2, double beta, double inv_n, double *out, void *workspace,
+                          void *stream) {
+  int rc = cs_check(g);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  CsWs w = cs_carve(g, workspace, nullptr);
+  CsArgs a = cs_args(g, w, K, sigma2, beta, inv_n);
+  a.s_in = reinterpret_cast<const double2 *>(pos);
+  a.v_in = reinterpret_cast<const double2 *>(vel);
+  a.out = reinterpret_cast<double2 *>(out);
+  return cs_stage<0>(a, st);
+}
+
+extern "C" int cdk_cs_rk4(const cdk_cs_graph *g, double *pos, double *vel, double K,
+                          double sigma2, double beta, double inv_n, double dt, int64_t n_steps,
+                          void *workspace, void *stream) {
+  int rc = cs_check(g);
+  if (rc) return rc;
+  if (n_steps < 0) return set_error("n_steps < 0"), CDK_INPUT;
+  cudaStream_t st = as_stream(stream);
+  CsWs w = cs_carve(g, workspace, nullptr);
+  CsArgs a = cs_args(g, w, K, sigma2, beta, inv_n);
+  double2 *s0 = reinterpret_cast<double2 *>(pos), *v0 = reinterpret_cast<double2 *>(vel);
+  a.s0 = s0;
+  a.v0 = v0;
+  for (int64_t s = 0; s < n_steps; ++s) {
+    a.step_rel = s;
+    a.s_in = s0; a.v_in = v0; a.s_out = w.s[0]; a.v_out = w.v[0]; a.h = dt / 2.0;
+    if ((rc = cs_stage<1>(a, st))) return rc;
+    a.s_in = w.s[0]; a.v_in = w.v[0]; a.s_out = w.s[1]; a.v_out = w.v[1]; a.h = dt / 2.0;
+    if ((rc = cs_stage<2>(a, st))) return rc;
+    a.s_in = w.s[1]; a.v_in = w.v[1]; a.s_out = w.s[0]; a.v_out = w.v[0]; a.h = dt;
+    if ((rc = cs_stage<3>(a, st))) return rc;
+    a.s_in = w.s[0]; a.v_in = w.v[0]; a.s_out = s0; a.v_out = v0; a.h = dt / 6.0;
+    if ((rc = cs_stage<4>(a, st))) return rc;
+  }
+  if (n_steps > 0) {
+    cs_advance_kernel<<<1, 1, 0, st>>>(w.status, n_steps);
+    CDK_CHECK_LAUNCH("cs_advance_kernel");
+  }
+  return CDK_OK;
+}
+
+extern "C" int cdk_cs_status(const cdk_cs_graph *g, const void *workspace, cdk_run_status *out,
+                             void *stream) {
+  int rc = cs_check(g);
+  if (rc) return rc;
+  CsWs w = cs_carve(g, const_cast<void *>(workspace), nullptr);
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMemcpyAsync(out, w.status, sizeof(cdk_run_status), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_status(e, "cdk_cs_status");
+}
