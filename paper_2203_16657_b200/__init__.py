@@ -40,6 +40,10 @@ def __getattr__(name):  # lazy: these import torch / the CUDA library
         from . import ho
 
         return getattr(ho, name)
+    if name in ("CuckerSmale", "CSEngine"):
+        from . import cs
+
+        return getattr(cs, name)
     if name == "KuramotoEngine":
         from .engine import KuramotoEngine
 

@@ -67,7 +67,35 @@ def engine_for(model, dec: Decomposition):
     raise InputError(f"unsupported model {type(model).__name__}")
 
 
+def _cs_engine(model, dec: Decomposition, pos_perm, vel_perm, t_end: float):
+    from .cs import CSEngine
+
+    key = ("cs_engine", id(model), float(t_end))
+    cached = dec._cache.get("cs_engine")
+    if cached is not None and cached[0] == key and cached[1] is model:
+        eng = cached[2]
+        eng.set_state(pos_perm, vel_perm)
+        return eng
+    eng = CSEngine(dec, model, pos_perm, vel_perm, t_end=t_end)
+    dec._cache["cs_engine"] = (key, model, eng)
+    return eng
+
+
 def eval_rhs_cia(model, dec: Decomposition, state) -> np.ndarray:
+    from .cs import CuckerSmale
+
+    if isinstance(model, CuckerSmale):  # state [N, 4] = (s_x, s_y, v_x, v_y)
+        x = np.asarray(state, dtype=np.float64)
+        if x.shape != (dec.n_nodes, 4):
+            raise InputError("Cucker-Smale state must have shape (N, 4)")
+        perm = dec.partition.perm
+        xp = x[perm]
+        eng = _cs_engine(model, dec, xp[:, :2], xp[:, 2:], t_end=0.0)
+        sd, vd = eng.rhs(xp[:, :2], xp[:, 2:])
+        outp = np.concatenate([sd.cpu().numpy(), vd.cpu().numpy()], 1)
+        out = np.empty_like(outp)
+        out[perm] = outp
+        return out
     x = np.asarray(state, dtype=np.float64)
     if x.shape != (dec.n_nodes,):
         raise InputError("state shape does not match the decomposition")

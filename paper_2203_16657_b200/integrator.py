@@ -62,7 +62,11 @@ def integrate(model, dec: Decomposition, x0, plan: IntegrationPlan) -> Trajector
         raise InputError("integrate: only mode='cia' runs on the device path")
     if plan.scheme not in ("rk4", "euler"):
         raise InputError(f"unknown scheme {plan.scheme!r}")
+    from .cs import CuckerSmale
+
     x0 = np.asarray(x0, dtype=np.float64)
+    if isinstance(model, CuckerSmale):
+        return _integrate_cs(model, dec, x0, plan)
     if x0.shape != (dec.n_nodes,):
         raise InputError("x0 shape does not match the decomposition")
     n_steps, dt, dt_last = plan.step_sizes()
@@ -97,6 +101,46 @@ def integrate(model, dec: Decomposition, x0, plan: IntegrationPlan) -> Trajector
     wall = time.perf_counter() - t0
     return Trajectory(np.asarray(times), states, wall, int(lib.cdk_launch_count()) - launches0,
                       {"n_steps": n_steps, "dt": dt, "dt_last": dt_last})
+
+
+def _integrate_cs(model, dec: Decomposition, x0, plan: IntegrationPlan) -> Trajectory:
+    """Cucker-Smale trajectory: state [N, 4] = (s_x, s_y, v_x, v_y), no wrap.
+    The P2 fit domain covers [0, t_end] (cs.cs_plan)."""
+    from .evaluator import _cs_engine
+
+    if plan.scheme != "rk4":
+        raise InputError("Cucker-Smale integrates with rk4")
+    if x0.shape != (dec.n_nodes, 4):
+        raise InputError("Cucker-Smale state must have shape (N, 4)")
+    n_steps, dt, dt_last = plan.step_sizes()
+    perm = dec.partition.perm
+    xp = x0[perm]
+    t0 = time.perf_counter()
+    eng = _cs_engine(model, dec, xp[:, :2], xp[:, 2:], t_end=plan.t_end)
+    launches0 = int(eng.lib.cdk_launch_count())
+    stride = plan.record_every if plan.record_every > 0 else n_steps
+    import torch
+
+    snaps = [torch.cat([eng.pos, eng.vel], 1).clone()]
+    times = [0.0]
+    done = 0
+    while done < n_steps:
+        chunk = min(stride, n_steps - done)
+        full = chunk if done + chunk < n_steps else chunk - 1
+        if full > 0:
+            eng.rk4(dt, full)
+        if done + chunk == n_steps:
+            eng.rk4(dt_last, 1)
+        done += chunk
+        times.append(min(done * dt, plan.t_end) if done < n_steps else plan.t_end)
+        snaps.append(torch.cat([eng.pos, eng.vel], 1).clone())
+    eng.check()
+    sp = np.stack([s.cpu().numpy() for s in snaps])
+    states = np.empty_like(sp)
+    states[:, perm] = sp
+    return Trajectory(np.asarray(times), states, time.perf_counter() - t0,
+                      int(eng.lib.cdk_launch_count()) - launches0,
+                      {"n_steps": n_steps, "dt": dt, "sup_err": float(eng.plan.sup_err.max())})
 
 
 __all__ = ["IntegrationPlan", "Trajectory", "integrate", "_lib"]

@@ -65,3 +65,18 @@ def test_cs_domain_guard():
     far[0] += 1e3
     with pytest.raises(DomainViolationError):
         eng.rhs(far, vel)
+
+
+def test_cs_public_api():
+    from paper_2203_16657_b200 import IntegrationPlan, eval_rhs_cia, integrate
+
+    c = configs.scaled_config4(m=3, lam=50, seed=9)
+    dec = c.decomposition()
+    pos, vel = c.state()
+    model = cs.CuckerSmale(c.K, c.sigma, c.beta)
+    x0 = np.concatenate([pos, vel], 1)
+    d = eval_rhs_cia(model, dec, x0)
+    assert d.shape == (c.n, 4)
+    np.testing.assert_array_equal(d[:, :2], vel)
+    tr = integrate(model, dec, x0, IntegrationPlan(t_end=0.05, dt=0.01))
+    assert tr.states.shape == (2, c.n, 4) and np.all(np.isfinite(tr.final))
