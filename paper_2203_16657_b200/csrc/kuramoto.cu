@@ -43,6 +43,7 @@ struct Workspace {
   double *ksum;
   double2 *part[2];  // canonical rblock partials of z (ping-pong with z)
   cdk_run_status *status;
+  unsigned int *bar;  // grid-barrier counter of the persistent kernel
 };
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -64,6 +65,7 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
   w.part[0] = (double2 *)take(((size_t)g->n_rblk + 1) * sizeof(double2));
   w.part[1] = (double2 *)take(((size_t)g->n_rblk + 1) * sizeof(double2));
   w.status = (cdk_run_status *)take(sizeof(cdk_run_status));
+  w.bar = (unsigned int *)take(256);
   if (total) *total = off;
   return w;
 }
@@ -166,7 +168,7 @@ __device__ __forceinline__ void gather8_global(const uint4 w, const double2 *__r
   for (int k = 0; k < 8; ++k) {
     const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
     if (u != CDK_INTRA_PAD) {
-      const double2 z = ldg(zbase + u);
+      const double2 z = __ldcg(zbase + u);
       sr -= z.x;
       si -= z.y;
     }
@@ -236,13 +238,20 @@ struct RowPipe {
   double2 z;    // z of column j
 };
 
+struct ProfAcc {
+  unsigned long long t_stage = 0, t_gather = 0, t_epi = 0, t_mark = 0;
+};
+
+// z_in / partial reads: L2-coherent (.cg) so a persistent multi-stage launch
+// never sees a stale L1 line of a buffer another CTA rewrote since.
+__device__ __forceinline__ double2 ldz(const double2 *p) { return __ldcg(p); }
+
+// One stage over this CTA's segments (see the kernel comment above).
 template <int MODE>
-__global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar_seg;
-  __shared__ double2 sR[SEG_MAX_COMM];
+__device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm,
+                                           uint64_t &bar_seg, uint64_t &bar_epi, double2 *sR,
+                                           uint32_t &parity, ProfAcc &pa) {
   const cdk_graph &g = a.g;
-  const SegSmem sm = carve_smem(smem_raw, g.seg_rows_cap, g.smem_nodes);
   const uint32_t zero_slot = (uint32_t)g.smem_nodes;  // zs[smem_nodes] == 0
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t = lane & 7;
@@ -252,27 +261,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
   const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
   const double2 *__restrict__ z_in = a.z_in;
   const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
-  if (tid == 0) {
-    mbar_init(&bar_seg, 1);
-    sm.zs[zero_slot] = make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  uint32_t parity = 0;
 #ifdef CDK_PROFILE
-  unsigned long long t_stage = 0, t_gather = 0, t_epi = 0, t_mark = clock64();
-  const unsigned long long t_begin = t_mark;
-#define PROF_MARK(acc)                        \
-  do {                                        \
-    const unsigned long long _n = clock64();  \
-    acc += _n - t_mark;                       \
-    t_mark = _n;                              \
+#define PROF_MARK(acc)                           \
+  do {                                           \
+    const unsigned long long _n = clock64();     \
+    pa.acc += _n - pa.t_mark;                    \
+    pa.t_mark = _n;                              \
   } while (0)
 #else
 #define PROF_MARK(acc) \
   do {                 \
   } while (0)
 #endif
-
   for (int s = segA; s < segB; ++s) {
     const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
     const int64_t row0 = g.rblk_row0[rbA];
@@ -290,13 +290,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       const uint32_t bp = (uint32_t)((((row1 + 2) & ~(int64_t)1) - row0a) * 8);
       const uint32_t br = (uint32_t)((((row1 + 1) & ~(int64_t)1) - row0a) * 8);
       const int nr_in = (MODE == 0) ? 1 : ((MODE == 1 || MODE == 5) ? 2 : 3);
-      mbar_expect_tx(&bar_seg, bw + 2 * bp + (uint32_t)nr_in * br);
+      mbar_expect_tx(&bar_seg, bw + 2 * bp);
       if (bw) bulk_g2s(sm.zs, z_in + w0, bw, &bar_seg);
       bulk_g2s(sm.sip, g.intra_ptr + row0a, bp, &bar_seg);
       bulk_g2s(sm.sxp, g.inter_ptr + row0a, bp, &bar_seg);
-      bulk_g2s(sm.som, a.omega + row0a, br, &bar_seg);
-      if (MODE != 0) bulk_g2s(sm.sth, a.theta + row0a, br, &bar_seg);
-      if (MODE >= 2 && MODE <= 4) bulk_g2s(sm.sks, a.ksum + row0a, br, &bar_seg);
+      // epilogue inputs on their own barrier: they land during the gathers
+      mbar_expect_tx(&bar_epi, (uint32_t)nr_in * br);
+      bulk_g2s(sm.som, a.omega + row0a, br, &bar_epi);
+      if (MODE != 0) bulk_g2s(sm.sth, a.theta + row0a, br, &bar_epi);
+      if (MODE >= 2 && MODE <= 4) bulk_g2s(sm.sks, a.ksum + row0a, br, &bar_epi);
     }
     // community observables R_c of the segment's communities, reduced (in the
     // canonical 8-lane order) from the previous stage's rblock partials while
@@ -338,7 +340,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       __syncthreads();  // accumulator buffer free for the gather phase
     }
     mbar_wait(&bar_seg, parity);
-    parity ^= 1;
     PROF_MARK(t_stage);
     const uint32_t zs_addr = smem_u32(sm.zs);
     const double2 *__restrict__ zglob = z_in + g.seg_base[s];
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       if (r < nrows) {
         R.c0 = (R.p < R.e1) ? ldg(colv + (R.p >> 3)) : padv;
         R.c1 = (R.p + 64 < R.e1) ? ldg(colv + ((R.p + 64) >> 3)) : padv;
-        R.z = (R.j >= 0) ? ldg(z_in + R.j) : make_double2(0.0, 0.0);
+        R.z = (R.j >= 0) ? ldz(z_in + R.j) : make_double2(0.0, 0.0);
       }
     };
     RowPipe A{}, B{}, C{};
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
       sr += A.z.x;
       si += A.z.y;
       for (int p = A.x0 + 8 + t; p < A.x1; p += 8) {
-        const double2 z = ldg(z_in + ldg(xcol + p));
+        const double2 z = ldz(z_in + ldg(xcol + p));
         sr += z.x;
         si += z.y;
       }
@@ -408,6 +409,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
     PROF_MARK(t_gather);
 
     // ---- 3. epilogue: warp per rblock, lane = row ---------------------------
+    mbar_wait(&bar_epi, parity);
+    parity ^= 1;
     const double kn = a.k_over_n;
     for (int rb = rbA + warp; rb < rbB; rb += NWARPS) {
       const int64_t rrow0 = g.rblk_row0[rb];
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
         const int64_t i = rrow0 + lane;
         const int64_t li = i - row0a;
         const double2 ac = sm.acc[i - row0];
-        const double2 zi = staged ? sm.zs[i - w0] : ldg(z_in + i);
+        const double2 zi = staged ? sm.zs[i - w0] : ldz(z_in + i);
         const double2 R = (c >= 0) ? sR[c - cA] : make_double2(0.0, 0.0);
         double k = sm.som[li] + kn * (R.y * zi.x - R.x * zi.y);
         k = k + kn * (ac.y * zi.x - ac.x * zi.y);
@@ -466,15 +469,99 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
     __syncthreads();  // shared segment buffers reused by the next segment
     PROF_MARK(t_epi);
   }
+}
+
+__device__ __forceinline__ void init_cta(const cdk_graph &g, const SegSmem &sm, uint64_t &bar_seg,
+                                         uint64_t &bar_epi) {
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_seg, 1);
+    mbar_init(&bar_epi, 1);
+    sm.zs[g.smem_nodes] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+}
+
+// single stage launch (MODE 0: RHS, 1..4: RK4 stage, 5: Euler)
+template <int MODE>
+__global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar_seg, bar_epi;
+  __shared__ double2 sR[SEG_MAX_COMM];
+  const SegSmem sm = carve_smem(smem_raw, a.g.seg_rows_cap, a.g.smem_nodes);
+  init_cta(a.g, sm, bar_seg, bar_epi);
+  uint32_t parity = 0;
+  ProfAcc pa;
 #ifdef CDK_PROFILE
-  if (tid == 0 && a.prof) {
+  pa.t_mark = clock64();
+  const unsigned long long t_begin = pa.t_mark;
+#endif
+  stage_body<MODE>(a, sm, bar_seg, bar_epi, sR, parity, pa);
+#ifdef CDK_PROFILE
+  if (threadIdx.x == 0 && a.prof) {
     unsigned long long *p = a.prof + 4 * blockIdx.x;
     p[0] = clock64() - t_begin;
-    p[1] = t_stage;
-    p[2] = t_gather;
-    p[3] = t_epi;
+    p[1] = pa.t_stage;
+    p[2] = pa.t_gather;
+    p[3] = pa.t_epi;
   }
 #endif
+}
+
+// grid-wide barrier for the cooperative (co-resident) persistent kernel:
+// monotone arrival counter, target = (sync index + 1) * gridDim.x
+__device__ __forceinline__ void grid_sync(unsigned int *counter, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(counter, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      if (v < target) __nanosleep(64);
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct StepPtrs {
+  double2 *z[2];
+  double2 *part[2];
+  unsigned int *bar;
+};
+
+// Persistent RK4: n_steps x 4 stages in ONE cooperative launch, grid barrier
+// between stages (no launch gaps; the CSR slices and window reloads are the
+// only per-stage traffic).
+__global__ void __launch_bounds__(NTHREADS, 1) kuramoto_rk4_kernel(StageArgs a, StepPtrs ptr,
+                                                                   int64_t n_steps, double dt) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar_seg, bar_epi;
+  __shared__ double2 sR[SEG_MAX_COMM];
+  const SegSmem sm = carve_smem(smem_raw, a.g.seg_rows_cap, a.g.smem_nodes);
+  init_cta(a.g, sm, bar_seg, bar_epi);
+  uint32_t parity = 0;
+  ProfAcc pa;
+  unsigned int sync_idx = 0;
+  const double h2 = dt / 2.0, h6 = dt / 6.0;
+  for (int64_t step = 0; step < n_steps; ++step) {
+    a.step_rel = step;
+    a.z_in = ptr.z[0]; a.z_out = ptr.z[1]; a.part_in = ptr.part[0]; a.part_out = ptr.part[1];
+    a.h = h2;
+    stage_body<1>(a, sm, bar_seg, bar_epi, sR, parity, pa);
+    grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+    a.z_in = ptr.z[1]; a.z_out = ptr.z[0]; a.part_in = ptr.part[1]; a.part_out = ptr.part[0];
+    stage_body<2>(a, sm, bar_seg, bar_epi, sR, parity, pa);
+    grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+    a.z_in = ptr.z[0]; a.z_out = ptr.z[1]; a.part_in = ptr.part[0]; a.part_out = ptr.part[1];
+    a.h = dt;
+    stage_body<3>(a, sm, bar_seg, bar_epi, sR, parity, pa);
+    grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+    a.z_in = ptr.z[1]; a.z_out = ptr.z[0]; a.part_in = ptr.part[1]; a.part_out = ptr.part[0];
+    a.h = h6;
+    stage_body<4>(a, sm, bar_seg, bar_epi, sR, parity, pa);
+    if (step + 1 < n_steps) grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+  }
 }
 
 // z = exp(i theta) and the canonical rblock partials (prepare).  One 8-lane
@@ -622,6 +709,48 @@ extern "C" int cdk_kuramoto_rhs(const cdk_graph *g, const double *theta, const d
   return launch_stage<0>(a, st);
 }
 
+static int launch_rk4_persistent(const StageArgs &a, const Workspace &w, int64_t n_steps,
+                                 double dt, cudaStream_t st) {
+  static int attr_bytes = -1;
+  const size_t smem = stage_smem(&a.g);
+  if (attr_bytes < 0) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, kuramoto_rk4_kernel);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncGetAttributes(rk4)");
+    const int dyn_max = cdk_max_smem_optin() - (int)fa.sharedSizeBytes;
+    e = cudaFuncSetAttribute(kuramoto_rk4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dyn_max);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(rk4)");
+    attr_bytes = dyn_max;
+  }
+  if ((int)smem > attr_bytes) {
+    set_error("community state does not fit the shared-memory opt-in limit");
+    return CDK_INPUT;
+  }
+  StepPtrs ptr{};
+  ptr.z[0] = w.z[0];
+  ptr.z[1] = w.z[1];
+  ptr.part[0] = w.part[0];
+  ptr.part[1] = w.part[1];
+  ptr.bar = w.bar;
+  cudaError_t e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(grid barrier)");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)a.g.n_cta);
+  cfg.blockDim = dim3((unsigned)a.g.cta_threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel, a, ptr, n_steps, dt);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(kuramoto_rk4_kernel)");
+  return CDK_OK;
+}
+
 extern "C" int cdk_kuramoto_rk4(const cdk_graph *g, double *theta, const double *omega,
                                 double k_over_n, double dt, int64_t n_steps, void *workspace,
                                 void *stream) {
@@ -631,26 +760,13 @@ extern "C" int cdk_kuramoto_rk4(const cdk_graph *g, double *theta, const double 
     set_error("n_steps < 0");
     return CDK_INPUT;
   }
+  if (n_steps == 0) return CDK_OK;
   cudaStream_t st = as_stream(stream);
   Workspace w = carve(g, workspace, nullptr);
   StageArgs a = base_args(g, w, theta, omega, k_over_n);
-  const double h2 = dt / 2.0, h6 = dt / 6.0;
-  for (int64_t s = 0; s < n_steps; ++s) {
-    a.step_rel = s;
-    // stage 1: z0 -> z1
-    a.z_in = w.z[0]; a.z_out = w.z[1]; a.part_in = w.part[0]; a.part_out = w.part[1]; a.h = h2;
-    if ((rc = launch_stage<1>(a, st))) return rc;
-    a.z_in = w.z[1]; a.z_out = w.z[0]; a.part_in = w.part[1]; a.part_out = w.part[0]; a.h = h2;
-    if ((rc = launch_stage<2>(a, st))) return rc;
-    a.z_in = w.z[0]; a.z_out = w.z[1]; a.part_in = w.part[0]; a.part_out = w.part[1]; a.h = dt;
-    if ((rc = launch_stage<3>(a, st))) return rc;
-    a.z_in = w.z[1]; a.z_out = w.z[0]; a.part_in = w.part[1]; a.part_out = w.part[0]; a.h = h6;
-    if ((rc = launch_stage<4>(a, st))) return rc;
-  }
-  if (n_steps > 0) {
-    advance_kernel<<<1, 1, 0, st>>>(w.status, n_steps);
-    CDK_CHECK_LAUNCH("advance_kernel");
-  }
+  if ((rc = launch_rk4_persistent(a, w, n_steps, dt, st))) return rc;
+  advance_kernel<<<1, 1, 0, st>>>(w.status, n_steps);
+  CDK_CHECK_LAUNCH("advance_kernel");
   return CDK_OK;
 }
 
