@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 5
+#define CDK_ABI_VERSION 6
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -124,6 +124,7 @@ typedef struct cdk_graph {
   const int64_t *seg_win;       /* [2*n_seg] staged node window [w0, w1) */
   const int64_t *seg_base;      /* [n_seg] base of the segment's intra columns */
   const int32_t *cta_seg;       /* [n_cta+1] segment boundaries per CTA */
+  const int32_t *seg_lpr;       /* [n_seg] lanes per row of the segment's gathers (4|8|16|32) */
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */

@@ -44,6 +44,7 @@ class CdkGraph(ctypes.Structure):
         ("seg_win", P),
         ("seg_base", P),
         ("cta_seg", P),
+        ("seg_lpr", P),
     ]
 
 
@@ -135,7 +136,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _lock = threading.Lock()
 _lib = None

@@ -151,14 +151,21 @@ __device__ __forceinline__ double2 lds_d2(uint32_t addr) {
 // capacity.  Unstaged (global, huge communities / NONE pool): predicated loads.
 __device__ __forceinline__ void gather8_smem(const uint4 w, uint32_t zs_addr, uint32_t zero_slot,
                                              double &sr, double &si) {
+  // two independent accumulation chains (even / odd entries), fixed combine
   const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
-    const double2 z = lds_d2(zs_addr + (min(u, zero_slot) << 4));
-    sr -= z.x;
-    si -= z.y;
+  for (int k = 0; k < 8; k += 2) {
+    const uint32_t u0 = wv[k >> 1] & 0xFFFFu, u1 = wv[k >> 1] >> 16;
+    const double2 z0 = lds_d2(zs_addr + (min(u0, zero_slot) << 4));
+    const double2 z1 = lds_d2(zs_addr + (min(u1, zero_slot) << 4));
+    ar += z0.x;
+    ai += z0.y;
+    br += z1.x;
+    bi += z1.y;
   }
+  sr -= ar + br;
+  si -= ai + bi;
 }
 
 __device__ __forceinline__ void gather8_global(const uint4 w, const double2 *__restrict__ zbase,
@@ -238,13 +245,93 @@ struct RowPipe {
   double2 z;    // z of column j
 };
 
-struct ProfAcc {
-  unsigned long long t_stage = 0, t_gather = 0, t_epi = 0, t_mark = 0;
-};
-
 // z_in / partial reads: L2-coherent (.cg) so a persistent multi-stage launch
 // never sees a stale L1 line of a buffer another CTA rewrote since.
 __device__ __forceinline__ double2 ldz(const double2 *p) { return __ldcg(p); }
+
+// Gather phase of one segment: rows r = grp, grp + NG, ... (NG = 1024/LPR
+// groups of LPR lanes); 3-deep pipeline per group:
+//   C: pointers + first inter column (2 rows ahead)
+//   B: first two column chunks + z of the inter column (1 row ahead)
+//   A: gathers, tails, reduction -> acc[r]
+// Lane t of a row reads the 8 entries [8t, 8t+8) of every 8*LPR-entry block,
+// so for LPR >= 8 one quarter-warp phase (8 lanes) covers one 64-entry block
+// and the host bank ordering (cdk_host_bank_order) is conflict-free; for
+// LPR = 4 a phase spans two rows (distinct within each row).
+template <int LPR>
+__device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &sm, int nrows,
+                                             int64_t row0, int64_t row0a, int64_t ebase,
+                                             int64_t xbase, bool staged, uint32_t zs_addr,
+                                             uint32_t zero_slot, const double2 *zglob,
+                                             const uint4 *__restrict__ colv,
+                                             const int32_t *__restrict__ xcol) {
+  constexpr int NG = NTHREADS / LPR;
+  constexpr int STRIDE = 8 * LPR;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t = lane & (LPR - 1);
+  const int grp = tid / LPR;
+  const unsigned gmask = (LPR == 32) ? FULL : (((1u << LPR) - 1u) << (lane & ~(LPR - 1)));
+  const double2 *__restrict__ z_in = a.z_in;
+  const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
+  auto stage_ptr = [&](int r, RowPipe &R) {
+    if (r < nrows) {
+      const int64_t li = row0 + r - row0a;
+      const int e0 = (int)(sm.sip[li] - ebase);
+      R.e1 = (int)(sm.sip[li + 1] - ebase);
+      R.x0 = (int)(sm.sxp[li] - xbase);
+      R.x1 = (int)(sm.sxp[li + 1] - xbase);
+      R.p = e0 + 8 * t;
+      R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
+    }
+  };
+  auto stage_data = [&](int r, RowPipe &R) {
+    if (r < nrows) {
+      R.c0 = (R.p < R.e1) ? ldg(colv + (R.p >> 3)) : padv;
+      R.c1 = (R.p + STRIDE < R.e1) ? ldg(colv + ((R.p + STRIDE) >> 3)) : padv;
+      R.z = (R.j >= 0) ? ldz(z_in + R.j) : make_double2(0.0, 0.0);
+    }
+  };
+  RowPipe A{}, B{}, C{};
+  int r = grp;
+  stage_ptr(r, A);
+  stage_ptr(r + NG, B);
+  stage_data(r, A);
+  for (; r < nrows; r += NG) {
+    stage_ptr(r + 2 * NG, C);
+    stage_data(r + NG, B);
+    double sr = 0.0, si = 0.0;
+    if (staged) {
+      if (A.p < A.e1) gather8_smem(A.c0, zs_addr, zero_slot, sr, si);  // skip all-pad chunks
+      if (A.p + STRIDE < A.e1) gather8_smem(A.c1, zs_addr, zero_slot, sr, si);
+      for (int p = A.p + 2 * STRIDE; p < A.e1; p += STRIDE)
+        gather8_smem(ldg(colv + (p >> 3)), zs_addr, zero_slot, sr, si);
+    } else {
+      gather8_global(A.c0, zglob, sr, si);
+      gather8_global(A.c1, zglob, sr, si);
+      for (int p = A.p + 2 * STRIDE; p < A.e1; p += STRIDE)
+        gather8_global(ldg(colv + (p >> 3)), zglob, sr, si);
+    }
+    sr += A.z.x;
+    si += A.z.y;
+    for (int p = A.x0 + LPR + t; p < A.x1; p += LPR) {
+      const double2 z = ldz(z_in + ldg(xcol + p));
+      sr += z.x;
+      si += z.y;
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+      sr += __shfl_xor_sync(gmask, sr, o);
+      si += __shfl_xor_sync(gmask, si, o);
+    }
+    if (t == 0) sm.acc[r] = make_double2(sr, si);
+    A = B;
+    B = C;
+  }
+}
+
+struct ProfAcc {
+  unsigned long long t_stage = 0, t_gather = 0, t_epi = 0, t_mark = 0;
+};
 
 // One stage over this CTA's segments (see the kernel comment above).
 template <int MODE>
@@ -347,63 +434,23 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col + ebase);
     const int32_t *__restrict__ xcol = g.inter_col + xbase;
 
-    // ---- 2. gather: static rows grp, grp+NGROUPS, ...; 3-deep pipeline ----
-    //   C: pointers + first inter column (2 rows ahead)
-    //   B: first two column chunks + z of the inter column (1 row ahead)
-    //   A: gathers, tails, reduction
-    auto stage_ptr = [&](int r, RowPipe &R) {
-      if (r < nrows) {
-        const int64_t li = row0 + r - row0a;
-        const int e0 = (int)(sm.sip[li] - ebase);
-        R.e1 = (int)(sm.sip[li + 1] - ebase);
-        R.x0 = (int)(sm.sxp[li] - xbase);
-        R.x1 = (int)(sm.sxp[li + 1] - xbase);
-        R.p = e0 + 8 * t;
-        R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
-      }
-    };
-    auto stage_data = [&](int r, RowPipe &R) {
-      if (r < nrows) {
-        R.c0 = (R.p < R.e1) ? ldg(colv + (R.p >> 3)) : padv;
-        R.c1 = (R.p + 64 < R.e1) ? ldg(colv + ((R.p + 64) >> 3)) : padv;
-        R.z = (R.j >= 0) ? ldz(z_in + R.j) : make_double2(0.0, 0.0);
-      }
-    };
-    RowPipe A{}, B{}, C{};
-    int r = grp;
-    stage_ptr(r, A);
-    stage_ptr(r + NGROUPS, B);
-    stage_data(r, A);
-    for (; r < nrows; r += NGROUPS) {
-      stage_ptr(r + 2 * NGROUPS, C);
-      stage_data(r + NGROUPS, B);
-      double sr = 0.0, si = 0.0;
-      if (staged) {
-        if (A.p < A.e1) gather8_smem(A.c0, zs_addr, zero_slot, sr, si);  // skip all-pad chunks
-        if (A.p + 64 < A.e1) gather8_smem(A.c1, zs_addr, zero_slot, sr, si);
-        for (int p = A.p + 128; p < A.e1; p += 64)
-          gather8_smem(ldg(colv + (p >> 3)), zs_addr, zero_slot, sr, si);
-      } else {
-        gather8_global(A.c0, zglob, sr, si);
-        gather8_global(A.c1, zglob, sr, si);
-        for (int p = A.p + 128; p < A.e1; p += 64)
-          gather8_global(ldg(colv + (p >> 3)), zglob, sr, si);
-      }
-      sr += A.z.x;
-      si += A.z.y;
-      for (int p = A.x0 + 8 + t; p < A.x1; p += 8) {
-        const double2 z = ldz(z_in + ldg(xcol + p));
-        sr += z.x;
-        si += z.y;
-      }
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        sr += __shfl_xor_sync(gmask, sr, o);
-        si += __shfl_xor_sync(gmask, si, o);
-      }
-      if (t == 0) sm.acc[r] = make_double2(sr, si);
-      A = B;
-      B = C;
+    // ---- 2. gather: lanes per row chosen per segment (8 / 16 / 32) ---------
+    switch (g.seg_lpr[s]) {
+      case 32:
+        gather_phase<32>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
+                         zglob, colv, xcol);
+        break;
+      case 16:
+        gather_phase<16>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
+                         zglob, colv, xcol);
+        break;
+      case 4:
+        gather_phase<4>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
+                        zglob, colv, xcol);
+        break;
+      default:
+        gather_phase<8>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
+                        zglob, colv, xcol);
     }
     __syncthreads();
     PROF_MARK(t_gather);

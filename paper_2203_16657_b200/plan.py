@@ -75,6 +75,7 @@ class Schedule:
     seg_win: np.ndarray  # int64[n_seg, 2]
     seg_base: np.ndarray  # int64[n_seg]
     cta_seg: np.ndarray  # int32[n_cta+1]
+    seg_lpr: np.ndarray  # int32[n_seg] lanes per row (4 | 8 | 16 | 32)
     intra_col: np.ndarray  # uint16, rebased to each row's segment base, bank-ordered
 
     @property
@@ -277,8 +278,20 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
             raise InputError("rebased intra column out of uint16 range")
         col[m] = newc.astype(np.uint16)
     _bank_order(col, lay.intra_ptr, smem_nodes)
+    # lanes per row: rows in flight matter more than lanes per row (measured:
+    # 16/32 lanes per row double the gather time); short rows use 4 lanes
+    seg_rows = rows[seg_rblk]
+    lens = (lay.intra_ptr[seg_rows[1:]] - lay.intra_ptr[seg_rows[:-1]]) / np.maximum(
+        np.diff(seg_rows), 1)
+    import os
+
+    forced = os.environ.get("CDK_LPR")
+    if forced:  # experiments: one width for every segment
+        seg_lpr = np.full(lens.shape[0], int(forced), dtype=np.int32)
+    else:
+        seg_lpr = np.where(lens > 24, 8, 4).astype(np.int32)
     return Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
-                    seg_base, np.asarray(cta_seg, dtype=np.int32), col)
+                    seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, col)
 
 
 def _bank_order(col: np.ndarray, ptr: np.ndarray, smem_nodes: int) -> None:
@@ -340,6 +353,7 @@ class DeviceGraph:
             "seg_win": up(sch.seg_win.reshape(-1)),
             "seg_base": up(sch.seg_base),
             "cta_seg": up(sch.cta_seg),
+            "seg_lpr": up(sch.seg_lpr if sch.n_seg else np.zeros(1, np.int32)),
         }
         # keep a 16-byte tail on intra_col so uint4 loads never run past the allocation
         if self._t["intra_col"].numel() == 0:
@@ -357,7 +371,7 @@ class DeviceGraph:
             rblk_row0=t["rblk_row0"].data_ptr(), rblk_comm=t["rblk_comm"].data_ptr(),
             comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
             seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
-            cta_seg=t["cta_seg"].data_ptr(),
+            cta_seg=t["cta_seg"].data_ptr(), seg_lpr=t["seg_lpr"].data_ptr(),
         )
 
     def device_bytes(self) -> int:
