@@ -262,6 +262,40 @@ CDK_API int cdk_cs_status(const cdk_cs_graph *g, const void *workspace, cdk_run_
                           void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* Device-side deterministic generator (BASELINE config 5) */
+/* Produces the stage kernel's CSR directly on the device (counter-based     */
+/* hashes: identical on any GPU count, any row regenerable).                 */
+/* ------------------------------------------------------------------------ */
+typedef struct cdk_gen_params {
+  uint64_t seed;
+  int64_t n_rows;
+  int64_t n_comm;
+  const int64_t *comm_off;   /* [n_comm+1] device */
+  const double *node_cdf;    /* [n_rows] device, cumulative endpoint weights, last = 1 */
+  int64_t n_inter_edges;     /* sampled inter edges (before drops / dedupe) */
+  uint32_t miss_thr;         /* intra pair missing iff hash < miss_thr (q * 2^32) */
+  uint32_t reserved;
+} cdk_gen_params;
+
+/* intra: per-row missing-partner counts (int64[n_rows]); then, with ptr = the
+ * prefix sum of the counts padded to multiples of 8, the uint16 columns */
+CDK_API int cdk_gen_intra_count(const cdk_gen_params *p, int64_t *cnt, void *stream);
+CDK_API int cdk_gen_intra_fill(const cdk_gen_params *p, const int64_t *ptr, uint16_t *col,
+                               void *stream);
+/* inter: counts (atomic int64[n_rows], zeroed by the caller), scatter via a
+ * cursor (= row starts), per-row sort + dedupe (writes unique counts), compact */
+CDK_API int cdk_gen_inter_count(const cdk_gen_params *p, int64_t *cnt, void *stream);
+CDK_API int cdk_gen_inter_fill(const cdk_gen_params *p, int64_t *cursor, int32_t *col,
+                               void *stream);
+CDK_API int cdk_gen_inter_sort(int64_t n_rows, const int64_t *ptr, int32_t *col, int64_t *uniq,
+                               void *stream);
+CDK_API int cdk_gen_inter_compact(int64_t n_rows, const int64_t *ptr_raw, const int64_t *ptr_new,
+                                  const int32_t *col_raw, int32_t *col_new, void *stream);
+/* add delta[row] to every non-padding intra column (segment-window rebasing) */
+CDK_API int cdk_gen_rebase(int64_t n_rows, const int64_t *ptr, const int32_t *delta,
+                           uint16_t *col, void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* host-side planning (no device needed)                                    */
 /* ------------------------------------------------------------------------ */
 

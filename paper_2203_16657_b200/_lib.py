@@ -84,6 +84,19 @@ class CdkCsGraph(ctypes.Structure):
     ]
 
 
+class CdkGenParams(ctypes.Structure):
+    _fields_ = [
+        ("seed", ctypes.c_uint64),
+        ("n_rows", I64),
+        ("n_comm", I64),
+        ("comm_off", P),
+        ("node_cdf", P),
+        ("n_inter_edges", I64),
+        ("miss_thr", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+    ]
+
+
 class CdkRunStatus(ctypes.Structure):
     _fields_ = [("nonfinite", I64), ("first_bad_step", I64), ("steps_done", I64),
                 ("reserved", I64)]
@@ -120,6 +133,13 @@ _SIGS = {
     "cdk_cs_rhs": [ctypes.POINTER(CdkCsGraph), P, P, D, D, D, D, P, P, P],
     "cdk_cs_rk4": [ctypes.POINTER(CdkCsGraph), P, P, D, D, D, D, D, I64, P, P],
     "cdk_cs_status": [ctypes.POINTER(CdkCsGraph), P, ctypes.POINTER(CdkRunStatus), P],
+    "cdk_gen_intra_count": [ctypes.POINTER(CdkGenParams), P, P],
+    "cdk_gen_intra_fill": [ctypes.POINTER(CdkGenParams), P, P, P],
+    "cdk_gen_inter_count": [ctypes.POINTER(CdkGenParams), P, P],
+    "cdk_gen_inter_fill": [ctypes.POINTER(CdkGenParams), P, P, P],
+    "cdk_gen_inter_sort": [I64, P, P, P, P],
+    "cdk_gen_inter_compact": [I64, P, P, P, P, P],
+    "cdk_gen_rebase": [I64, P, P, P, P],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],

@@ -120,6 +120,33 @@ def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
     return np.sort(np.concatenate([row0, np.asarray(extra, dtype=np.int64)]))
 
 
+def _rblocks(off, n, intra_ptr, inter_ptr, row_range=None):
+    """rblocks (<= 32 rows of one community, capped entries) of the rows in
+    row_range, then the NONE pool; returns (rblk_row0 [+sentinel], rblk_comm,
+    comm_rblk_off)."""
+    lo, hi = (0, n) if row_range is None else (int(row_range[0]), int(row_range[1]))
+    m = off.shape[0] - 1
+    n_in = int(off[-1])
+    sizes = np.diff(off)
+    owned = (off[:-1] >= lo) & (off[1:] <= hi)
+    if row_range is not None and np.any((off[:-1] < hi) & (off[1:] > lo) & ~owned):
+        raise InputError("a shard's row range must not split a community")
+    nb = np.where(owned, (sizes + RB - 1) // RB, 0)
+    comm_rblk_off = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(nb, out=comm_rblk_off[1:])
+    rc = np.repeat(np.arange(m, dtype=np.int64), nb)
+    within = np.arange(rc.shape[0], dtype=np.int64) - comm_rblk_off[rc]
+    row0 = off[rc] + RB * within
+    row0 = _split_heavy_rblocks(row0, off[rc + 1] if rc.size else row0, intra_ptr, inter_ptr)
+    rc = np.searchsorted(off, row0, side="right").astype(np.int64) - 1
+    comm_rblk_off = np.searchsorted(row0, off).astype(np.int64)
+    pool_row0 = np.arange(max(n_in, lo), max(min(n, hi), max(n_in, lo)), RB, dtype=np.int64)
+    end = min(n, hi) if row_range is not None else n
+    rblk_row0 = np.concatenate([row0, pool_row0, [end]]).astype(np.int64)
+    rblk_comm = np.concatenate([rc, np.full(pool_row0.shape[0], -1, np.int64)]).astype(np.int32)
+    return rblk_row0, rblk_comm, comm_rblk_off.astype(np.int32)
+
+
 def build_layout(dec: Decomposition, row_range=None) -> HostLayout:
     """Device layout of the directed S.  ``row_range=(lo, hi)`` keeps only rows
     in [lo, hi) (a rank's shard: whole communities; other rows are present but
@@ -166,31 +193,10 @@ def build_layout(dec: Decomposition, row_range=None) -> HostLayout:
     xcounts, inter_ptr = _row_runs(rx, n)
     nnz_inter = int(rx.shape[0])
 
-    # rblocks: communities, then the NONE pool (only rows of [lo, hi))
-    n_in = int(off[-1])
-    sizes = np.diff(off)
-    owned = (off[:-1] >= lo) & (off[1:] <= hi)
-    if row_range is not None and np.any((off[:-1] < hi) & (off[1:] > lo) & ~owned):
-        raise InputError("a shard's row range must not split a community")
-    nb = np.where(owned, (sizes + RB - 1) // RB, 0)
-    comm_rblk_off = np.zeros(m + 1, dtype=np.int64)
-    np.cumsum(nb, out=comm_rblk_off[1:])
-    rc = np.repeat(np.arange(m, dtype=np.int64), nb)
-    within = np.arange(rc.shape[0], dtype=np.int64) - comm_rblk_off[rc]
-    row0 = off[rc] + RB * within
-    # split 32-row blocks whose entries exceed the caps (dense long rows)
-    row0 = _split_heavy_rblocks(row0, off[rc + 1] if rc.size else row0, intra_ptr, inter_ptr)
-    rc = np.searchsorted(off, row0, side="right").astype(np.int64) - 1
-    comm_rblk_off = np.searchsorted(row0, off).astype(np.int64)
-    pool_row0 = np.arange(max(n_in, lo), max(min(n, hi), max(n_in, lo)), RB, dtype=np.int64)
-    # rblk_row0 carries a sentinel: rblock b spans [rblk_row0[b], rblk_row0[b+1])
-    end = min(n, hi) if row_range is not None else n
-    rblk_row0 = np.concatenate([row0, pool_row0, [end]]).astype(np.int64)
-    rblk_comm = np.concatenate([rc, np.full(pool_row0.shape[0], -1, np.int64)]).astype(np.int32)
+    rblk_row0, rblk_comm, comm_rblk_off = _rblocks(off, n, intra_ptr, inter_ptr, row_range)
     row_cost = padded.astype(np.float64) + INTER_COST * xcounts + ROW_COST
     return HostLayout(n, m, off.astype(np.int64), intra_ptr, intra_col, inter_ptr, inter_col,
-                      rblk_row0, rblk_comm, comm_rblk_off.astype(np.int32), row_cost,
-                      nnz_intra, nnz_inter)
+                      rblk_row0, rblk_comm, comm_rblk_off, row_cost, nnz_intra, nnz_inter)
 
 
 WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
@@ -269,6 +275,19 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
         cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
         delta[rows[0]: rows[-1]] = cstart - seg_base[seg_of_row]
+    if lay.intra_col is None:  # columns live on the device: caller rebases (cdk_gen_rebase)
+        import os
+
+        seg_rows = rows[seg_rblk]
+        lens = (lay.intra_ptr[seg_rows[1:]] - lay.intra_ptr[seg_rows[:-1]]) / np.maximum(
+            np.diff(seg_rows), 1)
+        forced = os.environ.get("CDK_LPR")
+        seg_lpr = (np.full(lens.shape[0], int(forced), dtype=np.int32) if forced
+                   else np.where(lens > 24, 8, 4).astype(np.int32))
+        sch = Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
+                       seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, None)
+        sch.row_delta = delta.astype(np.int32)
+        return sch
     col = lay.intra_col.copy()
     if np.any(delta != 0):
         d_ent = np.repeat(delta, np.diff(lay.intra_ptr))
@@ -376,3 +395,57 @@ class DeviceGraph:
 
     def device_bytes(self) -> int:
         return int(sum(v.numel() * v.element_size() for v in self._t.values()))
+
+    @classmethod
+    def from_device_csr(cls, lay: "HostLayout", intra_col_dev, inter_col_dev, device,
+                        sm_count: int | None = None):
+        """Graph whose columns were generated on the device (config 5): the
+        schedule is planned from the host copies of the row pointers and the
+        intra columns are rebased in place on the device."""
+        import torch
+
+        from ._lib import CdkGraph, check, load_library
+
+        self = cls.__new__(cls)
+        dev = torch.device(device)
+        if sm_count is None:
+            sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        sch = build_schedule(lay, sm_count=sm_count)
+        self.layout, self.schedule = lay, sch
+        self.n_rows, self.n_comm, self.device = lay.n_rows, lay.n_comm, dev
+        self.row_range = (0, lay.n_rows)
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+        pad = np.zeros(4, dtype=np.int64)
+        self._t = {
+            "comm_off": up(lay.comm_off),
+            "intra_ptr": up(np.concatenate([lay.intra_ptr, pad + lay.intra_ptr[-1]])),
+            "intra_col": intra_col_dev,
+            "inter_ptr": up(np.concatenate([lay.inter_ptr, pad + lay.inter_ptr[-1]])),
+            "inter_col": inter_col_dev,
+            "rblk_row0": up(lay.rblk_row0), "rblk_comm": up(lay.rblk_comm),
+            "comm_rblk_off": up(lay.comm_rblk_off), "seg_rblk": up(sch.seg_rblk),
+            "seg_win": up(sch.seg_win.reshape(-1)), "seg_base": up(sch.seg_base),
+            "cta_seg": up(sch.cta_seg), "seg_lpr": up(sch.seg_lpr),
+        }
+        t = self._t
+        delta = up(sch.row_delta)
+        lib = load_library()
+        check(lib.cdk_gen_rebase(lay.n_rows, t["intra_ptr"].data_ptr(), delta.data_ptr(),
+                                 t["intra_col"].data_ptr(), torch.cuda.current_stream().cuda_stream),
+              "gen_rebase")
+        self.struct = CdkGraph(
+            n_rows=lay.n_rows, n_comm=lay.n_comm,
+            comm_off=t["comm_off"].data_ptr(), intra_ptr=t["intra_ptr"].data_ptr(),
+            intra_col=t["intra_col"].data_ptr(), inter_ptr=t["inter_ptr"].data_ptr(),
+            inter_col=t["inter_col"].data_ptr(),
+            n_rblk=lay.n_rblk, n_seg=sch.n_seg, n_cta=sch.n_cta, cta_threads=sch.cta_threads,
+            smem_nodes=sch.smem_nodes, seg_rows_cap=sch.seg_rows_cap,
+            rblk_row0=t["rblk_row0"].data_ptr(), rblk_comm=t["rblk_comm"].data_ptr(),
+            comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
+            seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
+            cta_seg=t["cta_seg"].data_ptr(), seg_lpr=t["seg_lpr"].data_ptr(),
+        )
+        return self
