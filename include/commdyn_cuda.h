@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 6
+#define CDK_ABI_VERSION 7
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -125,6 +125,13 @@ typedef struct cdk_graph {
   const int64_t *seg_base;      /* [n_seg] base of the segment's intra columns */
   const int32_t *cta_seg;       /* [n_cta+1] segment boundaries per CTA */
   const int32_t *seg_lpr;       /* [n_seg] lanes per row of the segment's gathers (4|8|16|32) */
+  /* Communities wider than the window (smem_nodes) but at most 4 windows
+   * wide are staged in passes of smem_nodes nodes: each row's intra run is
+   * then up to 4 sub-runs (one per pass, each padded to 8, columns of pass p
+   * in [p*smem_nodes, (p+1)*smem_nodes) after rebasing) and intra_split[row]
+   * packs the sub-run starts in 8-entry chunks from the row start (bits
+   * 0-15: pass 1, 16-31: pass 2, 32-47: pass 3).  NULL if no such community. */
+  const uint64_t *intra_split;  /* [n_rows] or NULL */
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */
@@ -274,14 +281,18 @@ typedef struct cdk_gen_params {
   const double *node_cdf;    /* [n_rows] device, cumulative endpoint weights, last = 1 */
   int64_t n_inter_edges;     /* sampled inter edges (before drops / dedupe) */
   uint32_t miss_thr;         /* intra pair missing iff hash < miss_thr (q * 2^32) */
-  uint32_t reserved;
+  uint32_t pass_nodes;       /* window capacity of the stage kernel (cdk_graph.smem_nodes):
+                                rows of communities wider than it get per-pass sub-runs */
 } cdk_gen_params;
 
-/* intra: per-row missing-partner counts (int64[n_rows]); then, with ptr = the
- * prefix sum of the counts padded to multiples of 8, the uint16 columns */
-CDK_API int cdk_gen_intra_count(const cdk_gen_params *p, int64_t *cnt, void *stream);
-CDK_API int cdk_gen_intra_fill(const cdk_gen_params *p, const int64_t *ptr, uint16_t *col,
-                               void *stream);
+/* intra: per-row padded run lengths (int64[n_rows], sub-runs per pass each
+ * padded to 8), raw missing-partner counts (int64[n_rows]) and the packed
+ * sub-run starts (uint64[n_rows], see cdk_graph.intra_split); then, with ptr =
+ * the prefix sum of the padded lengths, the uint16 community-local columns */
+CDK_API int cdk_gen_intra_count(const cdk_gen_params *p, int64_t *padded, int64_t *raw,
+                                uint64_t *split, void *stream);
+CDK_API int cdk_gen_intra_fill(const cdk_gen_params *p, const int64_t *ptr,
+                               const uint64_t *split, uint16_t *col, void *stream);
 /* inter: counts (atomic int64[n_rows], zeroed by the caller), scatter via a
  * cursor (= row starts), per-row sort + dedupe (writes unique counts), compact */
 CDK_API int cdk_gen_inter_count(const cdk_gen_params *p, int64_t *cnt, void *stream);

@@ -70,32 +70,58 @@ def inter_endpoints(seed: int, n_edges: int, node_cdf: np.ndarray):
     return out[0], out[1]
 
 
-def generate_csr(seed: int, offsets: np.ndarray, node_cdf: np.ndarray, n_edges: int, thr: int):
+def _passes(c0: int, lam: int, wn: int) -> int:
+    """window passes of a community (csrc/gen.cu pass_geom): 1, or 2..4"""
+    w0 = c0 // 8 * 8
+    width = (c0 + lam + 7) // 8 * 8 - w0
+    if wn and width > wn:
+        q = (width + wn - 1) // wn
+        return q if q <= 4 else 1
+    return 1
+
+
+def generate_csr(seed: int, offsets: np.ndarray, node_cdf: np.ndarray, n_edges: int, thr: int,
+                 pass_nodes: int = 0):
     """The generator's output: (intra_ptr, intra_col uint16 local ascending,
-    padded with 0xFFFF to multiples of 8; inter_ptr, inter_col int32 sorted
-    unique) plus the undirected triples (iu, iv, sgn) with the in-community
-    diagonal, i.e. the reference's sparse-correction wire format."""
+    padded with 0xFFFF to multiples of 8 per window-pass sub-run; inter_ptr,
+    inter_col int32 sorted unique; intra_split uint64) plus the undirected
+    triples (iu, iv, sgn) with the in-community diagonal, i.e. the reference's
+    sparse-correction wire format."""
     n = int(node_cdf.shape[0])
     off = np.asarray(offsets, np.int64)
     m = off.shape[0] - 1
     rows_i, cols_i = [], []
+    intra_len = np.zeros(n, np.int64)
+    split = np.zeros(n, np.uint64)
+    runs = []  # per community: (rows, [per pass (row-local entries)])
     for c in range(m):
-        lam = int(off[c + 1] - off[c])
+        c0, lam = int(off[c]), int(off[c + 1] - off[c])
         mm = intra_missing(seed, c, lam, thr)
         r, q = np.nonzero(mm)
-        rows_i.append(r + off[c])
+        rows_i.append(r + c0)
         cols_i.append(q.astype(np.int64))
+        np_c = _passes(c0, lam, pass_nodes)
+        w0 = c0 // 8 * 8
+        bounds = [0] + [min(max(w0 + k * pass_nodes - c0, 0), lam) for k in range(1, np_c)] + [lam]
+        cnt = np.stack([np.count_nonzero(mm[:, bounds[k]:bounds[k + 1]], axis=1)
+                        for k in range(np_c)], axis=1)
+        pad = (cnt + 7) // 8 * 8
+        intra_len[c0:c0 + lam] = pad.sum(axis=1)
+        sub = np.cumsum(pad, axis=1) - pad
+        for k in range(1, np_c):
+            split[c0:c0 + lam] |= (sub[:, k] // 8).astype(np.uint64) << np.uint64(16 * (k - 1))
+        runs.append((c0, lam, mm, bounds, sub))
     ri = np.concatenate(rows_i) if rows_i else np.zeros(0, np.int64)
     ci = np.concatenate(cols_i) if cols_i else np.zeros(0, np.int64)
-    cnt = np.bincount(ri, minlength=n)
-    padded = (cnt + 7) // 8 * 8
     intra_ptr = np.zeros(n + 1, np.int64)
-    np.cumsum(padded, out=intra_ptr[1:])
+    np.cumsum(intra_len, out=intra_ptr[1:])
     intra_col = np.full(int(intra_ptr[-1]), 0xFFFF, np.uint16)
-    start = np.zeros(n + 1, np.int64)
-    np.cumsum(cnt, out=start[1:])
-    rank = np.arange(ri.shape[0]) - start[ri]
-    intra_col[intra_ptr[ri] + rank] = ci.astype(np.uint16)
+    for c0, lam, mm, bounds, sub in runs:
+        for a in range(lam):
+            for k in range(len(bounds) - 1):
+                cols = np.nonzero(mm[a, bounds[k]:bounds[k + 1]])[0] + bounds[k]
+                s = intra_ptr[c0 + a] + sub[a, k]
+                intra_col[s:s + cols.shape[0]] = cols.astype(np.uint16)
 
     comm = np.full(n, -1, np.int64)
     comm[: off[-1]] = np.repeat(np.arange(m), np.diff(off))
@@ -123,4 +149,4 @@ def generate_csr(seed: int, offsets: np.ndarray, node_cdf: np.ndarray, n_edges: 
     iv = np.concatenate([mi_v, diag, xv])
     sg = np.concatenate([-np.ones(mi_u.shape[0] + diag.shape[0]), np.ones(xu.shape[0])])
     order = np.lexsort((iv, iu))
-    return (intra_ptr, intra_col, inter_ptr, inter_col), (iu[order], iv[order], sg[order])
+    return (intra_ptr, intra_col, inter_ptr, inter_col, split), (iu[order], iv[order], sg[order])

@@ -45,6 +45,7 @@ class CdkGraph(ctypes.Structure):
         ("seg_base", P),
         ("cta_seg", P),
         ("seg_lpr", P),
+        ("intra_split", P),
     ]
 
 
@@ -93,7 +94,7 @@ class CdkGenParams(ctypes.Structure):
         ("node_cdf", P),
         ("n_inter_edges", I64),
         ("miss_thr", ctypes.c_uint32),
-        ("reserved", ctypes.c_uint32),
+        ("pass_nodes", ctypes.c_uint32),
     ]
 
 
@@ -133,8 +134,8 @@ _SIGS = {
     "cdk_cs_rhs": [ctypes.POINTER(CdkCsGraph), P, P, D, D, D, D, P, P, P],
     "cdk_cs_rk4": [ctypes.POINTER(CdkCsGraph), P, P, D, D, D, D, D, I64, P, P],
     "cdk_cs_status": [ctypes.POINTER(CdkCsGraph), P, ctypes.POINTER(CdkRunStatus), P],
-    "cdk_gen_intra_count": [ctypes.POINTER(CdkGenParams), P, P],
-    "cdk_gen_intra_fill": [ctypes.POINTER(CdkGenParams), P, P, P],
+    "cdk_gen_intra_count": [ctypes.POINTER(CdkGenParams), P, P, P, P],
+    "cdk_gen_intra_fill": [ctypes.POINTER(CdkGenParams), P, P, P, P],
     "cdk_gen_inter_count": [ctypes.POINTER(CdkGenParams), P, P],
     "cdk_gen_inter_fill": [ctypes.POINTER(CdkGenParams), P, P, P],
     "cdk_gen_inter_sort": [I64, P, P, P, P],
@@ -156,7 +157,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 _lock = threading.Lock()
 _lib = None

@@ -49,44 +49,100 @@ __device__ __forceinline__ int find_comm64(const int64_t *off, int64_t m, int64_
   return (int)lo;
 }
 
-// warp per row: count missing partners (ballot)
-__global__ void gen_intra_count_kernel(cdk_gen_params p, int64_t *cnt) {
+// Pass layout of a community (cdk_graph.intra_split): the community's staged
+// window starts at w0 = c0 rounded down to 8 (plan.py win_lo); if it is wider
+// than pass_nodes (and at most 4 passes), pass q covers global nodes
+// [w0 + q*pass_nodes, w0 + (q+1)*pass_nodes).
+struct PassGeom {
+  int np;         // passes (1 = a single run)
+  int64_t c0;     // community start
+  uint32_t lam;   // community size
+  int64_t w0;
+  uint32_t wn;
+  __device__ __forceinline__ uint32_t lo(int q) const {
+    if (np == 1) return 0u;
+    const int64_t v = w0 + (int64_t)q * wn - c0;
+    return v < 0 ? 0u : (uint32_t)v;
+  }
+  __device__ __forceinline__ uint32_t hi(int q) const {
+    if (np == 1) return lam;
+    const int64_t v = w0 + (int64_t)(q + 1) * wn - c0;
+    return v > (int64_t)lam ? lam : (uint32_t)v;
+  }
+};
+
+__device__ __forceinline__ PassGeom pass_geom(const cdk_gen_params &p, int c) {
+  PassGeom g;
+  g.c0 = p.comm_off[c];
+  g.lam = (uint32_t)(p.comm_off[c + 1] - g.c0);
+  g.w0 = g.c0 & ~(int64_t)7;
+  g.wn = p.pass_nodes;
+  const int64_t width = ((g.c0 + g.lam + 7) & ~(int64_t)7) - g.w0;
+  g.np = 1;
+  if (g.wn && width > (int64_t)g.wn) {
+    const int64_t q = (width + g.wn - 1) / g.wn;
+    g.np = q <= 4 ? (int)q : 1;  // wider: unstaged global gathers, one run
+  }
+  return g;
+}
+
+// warp per row: count missing partners per pass (ballot)
+__global__ void gen_intra_count_kernel(cdk_gen_params p, int64_t *padded, int64_t *raw,
+                                       uint64_t *split) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_in = p.comm_off[p.n_comm];
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_in; i += warps) {
     const int c = find_comm64(p.comm_off, p.n_comm, i);
-    const int64_t c0 = p.comm_off[c];
-    const uint32_t lam = (uint32_t)(p.comm_off[c + 1] - c0), a = (uint32_t)(i - c0);
-    int64_t count = 0;
-    for (uint32_t base = 0; base < lam; base += 32) {
-      const uint32_t b = base + lane;
-      const bool m = b < lam && b != a && missing_pair(p.seed, (uint32_t)c, a, b, p.miss_thr);
-      count += __popc(__ballot_sync(FULL, m));
+    const PassGeom G = pass_geom(p, c);
+    const uint32_t a = (uint32_t)(i - G.c0);
+    int64_t pad = 0, tot = 0;
+    uint64_t sp = 0;
+    for (int q = 0; q < G.np; ++q) {
+      if (q > 0) sp |= (uint64_t)(pad >> 3) << (16 * (q - 1));
+      const uint32_t lo = G.lo(q), hi = G.hi(q);
+      int64_t count = 0;
+      for (uint32_t base = lo; base < hi; base += 32) {
+        const uint32_t b = base + lane;
+        const bool m = b < hi && b != a && missing_pair(p.seed, (uint32_t)c, a, b, p.miss_thr);
+        count += __popc(__ballot_sync(FULL, m));
+      }
+      tot += count;
+      pad += (count + 7) & ~(int64_t)7;
     }
-    if (lane == 0) cnt[i] = count;  // the caller pads runs to multiples of 8
+    if (lane == 0) {
+      padded[i] = pad;
+      if (raw) raw[i] = tot;
+      if (split) split[i] = sp;
+    }
   }
 }
 
-// warp per row: write local columns ascending, pad with 0xFFFF
-__global__ void gen_intra_fill_kernel(cdk_gen_params p, const int64_t *ptr, uint16_t *col) {
+// warp per row: write local columns ascending per pass sub-run, pad with 0xFFFF
+__global__ void gen_intra_fill_kernel(cdk_gen_params p, const int64_t *ptr, const uint64_t *split,
+                                      uint16_t *col) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_in = p.comm_off[p.n_comm];
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_in; i += warps) {
     const int c = find_comm64(p.comm_off, p.n_comm, i);
-    const int64_t c0 = p.comm_off[c];
-    const uint32_t lam = (uint32_t)(p.comm_off[c + 1] - c0), a = (uint32_t)(i - c0);
-    int64_t pos = ptr[i];
-    const int64_t end = ptr[i + 1];
-    for (uint32_t base = 0; base < lam; base += 32) {
-      const uint32_t b = base + lane;
-      const bool m = b < lam && b != a && missing_pair(p.seed, (uint32_t)c, a, b, p.miss_thr);
-      const unsigned bal = __ballot_sync(FULL, m);
-      if (m) col[pos + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)b;
-      pos += __popc(bal);
+    const PassGeom G = pass_geom(p, c);
+    const uint32_t a = (uint32_t)(i - G.c0);
+    const uint64_t sp = (G.np > 1) ? split[i] : 0ull;
+    for (int q = 0; q < G.np; ++q) {
+      int64_t pos = ptr[i] + (q ? 8 * (int64_t)((sp >> (16 * (q - 1))) & 0xFFFFu) : 0);
+      const int64_t end = (q + 1 < G.np) ? ptr[i] + 8 * (int64_t)((sp >> (16 * q)) & 0xFFFFu)
+                                         : ptr[i + 1];
+      const uint32_t lo = G.lo(q), hi = G.hi(q);
+      for (uint32_t base = lo; base < hi; base += 32) {
+        const uint32_t b = base + lane;
+        const bool m = b < hi && b != a && missing_pair(p.seed, (uint32_t)c, a, b, p.miss_thr);
+        const unsigned bal = __ballot_sync(FULL, m);
+        if (m) col[pos + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)b;
+        pos += __popc(bal);
+      }
+      for (int64_t r = pos + lane; r < end; r += 32) col[r] = (uint16_t)0xFFFF;
     }
-    for (int64_t q = pos + lane; q < end; q += 32) col[q] = (uint16_t)0xFFFF;
   }
 }
 
@@ -204,17 +260,20 @@ static unsigned gen_grid(int64_t work, int per_block) {
 
 using namespace cdk;
 
-extern "C" int cdk_gen_intra_count(const cdk_gen_params *p, int64_t *cnt, void *stream) {
-  if (!p || p->n_comm < 0) return set_error("gen: bad params"), CDK_INPUT;
-  gen_intra_count_kernel<<<gen_grid(p->n_rows, 8), 256, 0, as_stream(stream)>>>(*p, cnt);
+extern "C" int cdk_gen_intra_count(const cdk_gen_params *p, int64_t *padded, int64_t *raw,
+                                   uint64_t *split, void *stream) {
+  if (!p || p->n_comm < 0 || !padded) return set_error("gen: bad params"), CDK_INPUT;
+  gen_intra_count_kernel<<<gen_grid(p->n_rows, 8), 256, 0, as_stream(stream)>>>(*p, padded, raw,
+                                                                                 split);
   CDK_CHECK_LAUNCH("gen_intra_count_kernel");
   return CDK_OK;
 }
 
-extern "C" int cdk_gen_intra_fill(const cdk_gen_params *p, const int64_t *ptr, uint16_t *col,
-                                  void *stream) {
+extern "C" int cdk_gen_intra_fill(const cdk_gen_params *p, const int64_t *ptr,
+                                  const uint64_t *split, uint16_t *col, void *stream) {
   if (!p) return CDK_INPUT;
-  gen_intra_fill_kernel<<<gen_grid(p->n_rows, 8), 256, 0, as_stream(stream)>>>(*p, ptr, col);
+  gen_intra_fill_kernel<<<gen_grid(p->n_rows, 8), 256, 0, as_stream(stream)>>>(*p, ptr, split,
+                                                                                col);
   CDK_CHECK_LAUNCH("gen_intra_fill_kernel");
   return CDK_OK;
 }

@@ -264,7 +264,8 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
                                              int64_t xbase, bool staged, uint32_t zs_addr,
                                              uint32_t zero_slot, const double2 *zglob,
                                              const uint4 *__restrict__ colv,
-                                             const int32_t *__restrict__ xcol) {
+                                             const int32_t *__restrict__ xcol, int pass,
+                                             int npass) {
   constexpr int NG = NTHREADS / LPR;
   constexpr int STRIDE = 8 * LPR;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -276,10 +277,15 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
   auto stage_ptr = [&](int r, RowPipe &R) {
     if (r < nrows) {
       const int64_t li = row0 + r - row0a;
-      const int e0 = (int)(sm.sip[li] - ebase);
+      int e0 = (int)(sm.sip[li] - ebase);
       R.e1 = (int)(sm.sip[li + 1] - ebase);
+      if (npass > 1) {  // this pass's sub-run (cdk_graph.intra_split)
+        const uint64_t sw = __ldg(a.g.intra_split + row0 + r);
+        if (pass + 1 < npass) R.e1 = e0 + 8 * (int)((sw >> (16 * pass)) & 0xFFFFu);
+        if (pass > 0) e0 += 8 * (int)((sw >> (16 * (pass - 1))) & 0xFFFFu);
+      }
       R.x0 = (int)(sm.sxp[li] - xbase);
-      R.x1 = (int)(sm.sxp[li + 1] - xbase);
+      R.x1 = pass == 0 ? (int)(sm.sxp[li + 1] - xbase) : R.x0;  // inter entries: pass 0
       R.p = e0 + 8 * t;
       R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
     }
@@ -323,7 +329,14 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
       sr += __shfl_xor_sync(gmask, sr, o);
       si += __shfl_xor_sync(gmask, si, o);
     }
-    if (t == 0) sm.acc[r] = make_double2(sr, si);
+    if (t == 0) {
+      if (pass == 0) {
+        sm.acc[r] = make_double2(sr, si);
+      } else {
+        const double2 prev = sm.acc[r];
+        sm.acc[r] = make_double2(prev.x + sr, prev.y + si);
+      }
+    }
     A = B;
     B = C;
   }
@@ -347,7 +360,9 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
   const unsigned gmask = 0xFFu << leader;  // this 8-lane group only
   const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
   const double2 *__restrict__ z_in = a.z_in;
-  const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
+  const int wn = g.smem_nodes;
+  // mbarrier phases: bar_seg completes once per pass, bar_epi once per segment
+  uint32_t pseg = (parity >> 1) & 1u, pepi = parity & 1u;
 #ifdef CDK_PROFILE
 #define PROF_MARK(acc)                           \
   do {                                           \
@@ -367,13 +382,14 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     const int64_t row0a = row0 & ~(int64_t)1;
     const int64_t w0 = g.seg_win[2 * s], w1 = g.seg_win[2 * s + 1];
     const bool staged = w1 > w0;
+    const int npass = staged ? (int)((w1 - w0 + wn - 1) / wn) : 1;  // window passes (<= 4)
     const int nrows = (int)(row1 - row0);
     const int cA = g.rblk_comm[rbA];
 
     // ---- 1. stage window, pointer slices, epilogue inputs (async) ----------
     if (tid == 0) {
       fence_proxy_async_smem();  // earlier generic accesses before the async overwrite
-      const uint32_t bw = staged ? (uint32_t)((w1 - w0) * 16) : 0u;
+      const uint32_t bw = staged ? (uint32_t)(min(w1 - w0, (int64_t)wn) * 16) : 0u;
       const uint32_t bp = (uint32_t)((((row1 + 2) & ~(int64_t)1) - row0a) * 8);
       const uint32_t br = (uint32_t)((((row1 + 1) & ~(int64_t)1) - row0a) * 8);
       const int nr_in = (MODE == 0) ? 1 : ((MODE == 1 || MODE == 5) ? 2 : 3);
@@ -426,38 +442,59 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
       }
       __syncthreads();  // accumulator buffer free for the gather phase
     }
-    mbar_wait(&bar_seg, parity);
+    mbar_wait(&bar_seg, pseg);
+    pseg ^= 1u;
     PROF_MARK(t_stage);
     const uint32_t zs_addr = smem_u32(sm.zs);
     const double2 *__restrict__ zglob = z_in + g.seg_base[s];
     const int64_t ebase = sm.sip[row0 - row0a], xbase = sm.sxp[row0 - row0a];
     const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col + ebase);
     const int32_t *__restrict__ xcol = g.inter_col + xbase;
+    const int lpr = g.seg_lpr[s];
 
-    // ---- 2. gather: lanes per row chosen per segment (8 / 16 / 32) ---------
-    switch (g.seg_lpr[s]) {
-      case 32:
-        gather_phase<32>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
-                         zglob, colv, xcol);
-        break;
-      case 16:
-        gather_phase<16>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
-                         zglob, colv, xcol);
-        break;
-      case 4:
-        gather_phase<4>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
-                        zglob, colv, xcol);
-        break;
-      default:
-        gather_phase<8>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_addr, zero_slot,
-                        zglob, colv, xcol);
+    // ---- 2. gather: lanes per row chosen per segment (4 / 8 / 16 / 32); a
+    //         community wider than the window is gathered in passes, each
+    //         with its slice of the window restaged (rebased columns of pass
+    //         q lie in [q*wn, (q+1)*wn): the window base address is shifted)
+    for (int pass = 0; pass < npass; ++pass) {
+      if (pass > 0) {
+        __syncthreads();  // every gather of the previous pass is done with zs
+        if (tid == 0) {
+          fence_proxy_async_smem();
+          const int64_t q0 = w0 + (int64_t)pass * wn, q1 = min(w1, q0 + wn);
+          const uint32_t bq = (uint32_t)((q1 - q0) * 16);
+          mbar_expect_tx(&bar_seg, bq);
+          bulk_g2s(sm.zs, z_in + q0, bq, &bar_seg);
+        }
+        mbar_wait(&bar_seg, pseg);
+        pseg ^= 1u;
+      }
+      const uint32_t zs_p = zs_addr - (uint32_t)pass * (uint32_t)wn * 16u;
+      const uint32_t zero_p = zero_slot + (uint32_t)pass * (uint32_t)wn;
+      switch (lpr) {
+        case 32:
+          gather_phase<32>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
+                           colv, xcol, pass, npass);
+          break;
+        case 16:
+          gather_phase<16>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
+                           colv, xcol, pass, npass);
+          break;
+        case 4:
+          gather_phase<4>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
+                          colv, xcol, pass, npass);
+          break;
+        default:
+          gather_phase<8>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
+                          colv, xcol, pass, npass);
+      }
     }
     __syncthreads();
     PROF_MARK(t_gather);
 
     // ---- 3. epilogue: warp per rblock, lane = row ---------------------------
-    mbar_wait(&bar_epi, parity);
-    parity ^= 1;
+    mbar_wait(&bar_epi, pepi);
+    pepi ^= 1u;
     const double kn = a.k_over_n;
     for (int rb = rbA + warp; rb < rbB; rb += NWARPS) {
       const int64_t rrow0 = g.rblk_row0[rb];
@@ -469,7 +506,7 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
         const int64_t i = rrow0 + lane;
         const int64_t li = i - row0a;
         const double2 ac = sm.acc[i - row0];
-        const double2 zi = staged ? sm.zs[i - w0] : ldz(z_in + i);
+        const double2 zi = (staged && npass == 1) ? sm.zs[i - w0] : ldz(z_in + i);
         const double2 R = (c >= 0) ? sR[c - cA] : make_double2(0.0, 0.0);
         double k = sm.som[li] + kn * (R.y * zi.x - R.x * zi.y);
         k = k + kn * (ac.y * zi.x - ac.x * zi.y);
@@ -516,6 +553,7 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     __syncthreads();  // shared segment buffers reused by the next segment
     PROF_MARK(t_epi);
   }
+  parity = (pseg << 1) | pepi;
 }
 
 __device__ __forceinline__ void init_cta(const cdk_graph &g, const SegSmem &sm, uint64_t &bar_seg,

@@ -34,7 +34,8 @@ import numpy as np
 from . import _lib
 from .errors import InputError
 from .graph import power_law_sizes
-from .plan import INTER_COST, ROW_COST, HostLayout, _rblocks
+from .plan import (INTER_COST, ROW_COST, HostLayout, _rblocks, community_passes,
+                   window_nodes)
 
 
 @dataclass(frozen=True)
@@ -129,6 +130,8 @@ class GeneratedCsr:
     inter_col: object  # device int32, +4 slack
     n_inter_edges: int
     nnz_intra: int
+    intra_split: object = None  # device int64 (uint64 bits) or None
+    pass_nodes: int = 0
 
     def layout(self) -> HostLayout:
         n = self.n_rows
@@ -137,9 +140,16 @@ class GeneratedCsr:
         padded = np.diff(self.intra_ptr)
         xcounts = np.diff(self.inter_ptr)
         row_cost = padded.astype(np.float64) + INTER_COST * xcounts + ROW_COST
+        split = (self.intra_split.cpu().numpy().view(np.uint64)
+                 if self.intra_split is not None else None)
         return HostLayout(n, self.n_comm, off, self.intra_ptr, None, self.inter_ptr, None,
                           rblk_row0, rblk_comm, comm_rblk_off, row_cost,
-                          self.nnz_intra, int(self.inter_ptr[-1]))
+                          self.nnz_intra, int(self.inter_ptr[-1]), split, self.pass_nodes)
+
+    def split_host(self) -> np.ndarray:
+        if self.intra_split is None:
+            return np.zeros(self.n_rows, dtype=np.uint64)
+        return self.intra_split.cpu().numpy().view(np.uint64)
 
     def to_host(self):
         """(intra_ptr, intra_col uint16 local, inter_ptr, inter_col int32) on the host."""
@@ -148,10 +158,13 @@ class GeneratedCsr:
                 self.inter_ptr, self.inter_col[:nx].cpu().numpy())
 
 
-def generate(case: LfrCase, device=None, stream=None) -> GeneratedCsr:
-    """Run the device generator for ``case``; returns the CSR on ``device``."""
+def generate(case: LfrCase, device=None, stream=None, pass_nodes: int | None = None) -> GeneratedCsr:
+    """Run the device generator for ``case``; returns the CSR on ``device``.
+    Rows of communities wider than ``pass_nodes`` (default: the stage
+    kernel's window) get one sub-run per window pass (cdk_graph.intra_split)."""
     import torch
 
+    pass_nodes = window_nodes() if pass_nodes is None else int(pass_nodes)
     dev = torch.device(device if device is not None else "cuda")
     lib = _lib.lib()
     off, cdf, n_edges, thr = case.gen_inputs()
@@ -160,19 +173,26 @@ def generate(case: LfrCase, device=None, stream=None) -> GeneratedCsr:
     d_cdf = torch.from_numpy(cdf).to(dev)
     p = _lib.CdkGenParams(seed=int(case.graph_seed), n_rows=n, n_comm=m,
                           comm_off=d_off.data_ptr(), node_cdf=d_cdf.data_ptr(),
-                          n_inter_edges=n_edges, miss_thr=thr, reserved=0)
+                          n_inter_edges=n_edges, miss_thr=thr, pass_nodes=pass_nodes)
     pp = ctypes.byref(p)
     sp = _lib.stream_ptr(stream)
 
-    # intra: padded counts -> pointers -> columns
+    # intra: padded run lengths (per-pass sub-runs) -> pointers -> columns
     cnt = torch.zeros(n, dtype=torch.int64, device=dev)
-    _lib.check(lib.cdk_gen_intra_count(pp, cnt.data_ptr(), sp), "gen_intra_count")
-    nnz_intra = int(cnt.sum().item())
+    raw = torch.zeros(n, dtype=torch.int64, device=dev)
+    split = torch.zeros(n, dtype=torch.int64, device=dev)
+    _lib.check(lib.cdk_gen_intra_count(pp, cnt.data_ptr(), raw.data_ptr(), split.data_ptr(), sp),
+               "gen_intra_count")
+    nnz_intra = int(raw.sum().item())
+    del raw
     iptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    torch.cumsum((cnt + 7) // 8 * 8, 0, out=iptr[1:])
+    torch.cumsum(cnt, 0, out=iptr[1:])
     ni = int(iptr[-1].item())
     icol = torch.full((ni + 8,), -1, dtype=torch.int16, device=dev)
-    _lib.check(lib.cdk_gen_intra_fill(pp, iptr.data_ptr(), icol.data_ptr(), sp), "gen_intra_fill")
+    _lib.check(lib.cdk_gen_intra_fill(pp, iptr.data_ptr(), split.data_ptr(), icol.data_ptr(), sp),
+               "gen_intra_fill")
+    if not (community_passes(off, pass_nodes) > 1).any():
+        split = None
 
     # inter: counts -> scatter -> per-row sort + dedupe -> compact
     cnt.zero_()
@@ -195,16 +215,21 @@ def generate(case: LfrCase, device=None, stream=None) -> GeneratedCsr:
                                          xcol.data_ptr(), sp), "gen_inter_compact")
     del raw
     return GeneratedCsr(n, m, off, iptr.cpu().numpy(), xptr.cpu().numpy(), icol, xcol, n_edges,
-                        nnz_intra)
+                        nnz_intra, split, pass_nodes)
 
 
-def device_graph(case: LfrCase, device=None, sm_count: int | None = None):
-    """(DeviceGraph, GeneratedCsr) for ``case``: generate, plan, rebase in place."""
-    from .plan import DeviceGraph
+def device_graph(case: LfrCase, device=None, sm_count: int | None = None,
+                 smem_budget: int | None = None):
+    """(DeviceGraph, GeneratedCsr) for ``case``: generate, plan, rebase in place.
+    ``smem_budget`` shrinks the stage kernel's window (tests: multi-pass paths
+    at small sizes)."""
+    from .plan import ROWS_CAP, SMEM_OPTIN, DeviceGraph
 
-    csr = generate(case, device)
+    budget = SMEM_OPTIN - 2048 if smem_budget is None else int(smem_budget)
+    csr = generate(case, device, pass_nodes=window_nodes(ROWS_CAP, budget))
     dg = DeviceGraph.from_device_csr(csr.layout(), csr.intra_col, csr.inter_col,
-                                     csr.intra_col.device, sm_count=sm_count)
+                                     csr.intra_col.device, sm_count=sm_count,
+                                     split_dev=csr.intra_split, smem_budget=budget)
     return dg, csr
 
 

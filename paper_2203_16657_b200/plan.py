@@ -51,6 +51,8 @@ class HostLayout:
     row_cost: np.ndarray
     nnz_intra: int
     nnz_inter: int
+    intra_split: np.ndarray | None = None  # uint64[n] sub-run starts (cdk_graph.intra_split)
+    pass_nodes: int = 0  # window capacity the sub-runs were cut for
 
     @property
     def nnz_dir(self) -> int:
@@ -120,6 +122,34 @@ def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
     return np.sort(np.concatenate([row0, np.asarray(extra, dtype=np.int64)]))
 
 
+WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
+CTA_THREADS = 1024
+ROWS_CAP = 1536  # rows per segment (shared-memory row buffers; multiple of 8)
+SEG_MAX_COMM = 64  # communities per staged segment (csrc/kuramoto.cu SEG_MAX_COMM)
+MAX_PASS = 4  # window passes per community (cdk_graph.intra_split packs 3 sub-run starts)
+
+
+def stage_smem_bytes(smem_nodes: int, rows_cap: int = ROWS_CAP) -> int:
+    """dynamic shared memory of the stage kernel (csrc/kuramoto.cu:stage_smem_bytes):
+    row accumulators + pointer slices + epilogue inputs + window (+8 spare)"""
+    return (rows_cap + 4) * (16 + 5 * 8) + 16 * (smem_nodes + 8)
+
+
+def window_nodes(rows_cap: int = ROWS_CAP, smem_budget: int = SMEM_OPTIN - 2048) -> int:
+    """staged window capacity (nodes, multiple of 8) of the stage kernel"""
+    rows_cap = int(rows_cap) // 8 * 8
+    return max(0, (smem_budget - stage_smem_bytes(0, rows_cap)) // 16) // WIN_ALIGN * WIN_ALIGN
+
+
+def community_passes(off: np.ndarray, wn: int) -> np.ndarray:
+    """window passes per community: 1 = fits, 2..MAX_PASS = staged in passes,
+    0 = wider (gathered from global memory, one run)"""
+    off = np.asarray(off, dtype=np.int64)
+    width = (off[1:] + WIN_ALIGN - 1) // WIN_ALIGN * WIN_ALIGN - off[:-1] // WIN_ALIGN * WIN_ALIGN
+    q = (width + max(wn, 1) - 1) // max(wn, 1) if wn > 0 else np.zeros_like(width)
+    return np.where(q <= MAX_PASS, np.maximum(q, 1), 0).astype(np.int64)
+
+
 def _rblocks(off, n, intra_ptr, inter_ptr, row_range=None):
     """rblocks (<= 32 rows of one community, capped entries) of the rows in
     row_range, then the NONE pool; returns (rblk_row0 [+sentinel], rblk_comm,
@@ -147,10 +177,11 @@ def _rblocks(off, n, intra_ptr, inter_ptr, row_range=None):
     return rblk_row0, rblk_comm, comm_rblk_off.astype(np.int32)
 
 
-def build_layout(dec: Decomposition, row_range=None) -> HostLayout:
+def build_layout(dec: Decomposition, row_range=None, pass_nodes: int | None = None) -> HostLayout:
     """Device layout of the directed S.  ``row_range=(lo, hi)`` keeps only rows
     in [lo, hi) (a rank's shard: whole communities; other rows are present but
-    empty, columns stay global)."""
+    empty, columns stay global).  ``pass_nodes``: window capacity the
+    multi-pass sub-runs are cut for (default: the stage kernel's)."""
     part = dec.partition
     n = int(dec.n_nodes)
     off = part.offsets
@@ -169,20 +200,46 @@ def build_layout(dec: Decomposition, row_range=None) -> HostLayout:
         raise InputError("sparse correction signs inconsistent with the partition "
                          "(-1 must be intra-community, +1 inter-community)")
 
-    # intra: uint16 local columns, rows padded to multiples of 8
+    # intra: uint16 local columns, rows padded to multiples of 8; rows of
+    # communities wider than the window: one padded sub-run per pass
     key = (rows[intra].astype(np.int64) << 16) | (cols[intra] - off[cr[intra]])
     key.sort()
     ri = key >> 16
-    ci = (key & 0xFFFF).astype(np.uint16)
-    counts, start = _row_runs(ri, n)
-    padded = (counts + 7) // 8 * 8
-    intra_ptr = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(padded, out=intra_ptr[1:])
+    ci = (key & 0xFFFF).astype(np.int64)
+    wn = window_nodes() if pass_nodes is None else int(pass_nodes)
+    npass_c = community_passes(off, wn)
+    multi_c = npass_c > 1
+    split = None
+    if not multi_c.any():
+        counts, start = _row_runs(ri, n)
+        padded = (counts + 7) // 8 * 8
+        intra_ptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(padded, out=intra_ptr[1:])
+        pos = intra_ptr[ri] + np.arange(ri.shape[0], dtype=np.int64) - start[ri]
+    else:
+        ce = comm[ri]
+        ps = np.where(multi_c[ce], (ci + off[ce] - (off[ce] // 8 * 8)) // wn, 0)
+        gid = ri * MAX_PASS + ps
+        cnt4 = np.bincount(gid, minlength=n * MAX_PASS).reshape(n, MAX_PASS)
+        pad4 = (cnt4 + 7) // 8 * 8
+        padded = pad4.sum(axis=1)
+        intra_ptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(padded, out=intra_ptr[1:])
+        sub = np.cumsum(pad4, axis=1) - pad4  # sub-run starts within the row
+        np_row = np.ones(n, dtype=np.int64)
+        np_row[: off[-1]] = np.repeat(npass_c, np.diff(off))
+        split = np.zeros(n, dtype=np.uint64)
+        for q in range(1, MAX_PASS):
+            on = np_row > q
+            split[on] |= (sub[on, q] // 8).astype(np.uint64) << np.uint64(16 * (q - 1))
+        gstart = np.zeros(n * MAX_PASS + 1, dtype=np.int64)
+        np.cumsum(cnt4.reshape(-1), out=gstart[1:])
+        pos = intra_ptr[ri] + sub[ri, ps] + np.arange(ri.shape[0], dtype=np.int64) - gstart[gid]
+        counts = cnt4.sum(axis=1)
     intra_col = np.full(int(intra_ptr[-1]), INTRA_PAD, dtype=np.uint16)
-    rank = np.arange(ri.shape[0], dtype=np.int64) - start[ri]
-    intra_col[intra_ptr[ri] + rank] = ci
+    intra_col[pos] = ci.astype(np.uint16)
     nnz_intra = int(ri.shape[0])
-    del key, ri, ci, rank
+    del key, ri, ci, pos
 
     # inter: int32 global columns
     rx = rows[~intra]
@@ -196,19 +253,10 @@ def build_layout(dec: Decomposition, row_range=None) -> HostLayout:
     rblk_row0, rblk_comm, comm_rblk_off = _rblocks(off, n, intra_ptr, inter_ptr, row_range)
     row_cost = padded.astype(np.float64) + INTER_COST * xcounts + ROW_COST
     return HostLayout(n, m, off.astype(np.int64), intra_ptr, intra_col, inter_ptr, inter_col,
-                      rblk_row0, rblk_comm, comm_rblk_off, row_cost, nnz_intra, nnz_inter)
+                      rblk_row0, rblk_comm, comm_rblk_off, row_cost, nnz_intra, nnz_inter,
+                      split, wn)
 
 
-WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
-CTA_THREADS = 1024
-ROWS_CAP = 1536  # rows per segment (shared-memory row buffers; multiple of 8)
-SEG_MAX_COMM = 64  # communities per staged segment (csrc/kuramoto.cu SEG_MAX_COMM)
-
-
-def stage_smem_bytes(smem_nodes: int, rows_cap: int = ROWS_CAP) -> int:
-    """dynamic shared memory of the stage kernel (csrc/kuramoto.cu:stage_smem_bytes):
-    row accumulators + pointer slices + epilogue inputs + window (+8 spare)"""
-    return (rows_cap + 4) * (16 + 5 * 8) + 16 * (smem_nodes + 8)
 
 
 def _rblk_rows(lay: HostLayout) -> np.ndarray:
@@ -222,7 +270,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
     shared-memory window (or, for communities above the window capacity and
     the NONE pool, gather from global memory)."""
     rows_cap = int(rows_cap) // 8 * 8
-    smem_nodes = max(0, (smem_budget - stage_smem_bytes(0, rows_cap)) // 16) // WIN_ALIGN * WIN_ALIGN
+    smem_nodes = window_nodes(rows_cap, smem_budget)
     n_cta = max(1, int(sm_count))
     nrb = lay.n_rblk
     rows = _rblk_rows(lay)
@@ -236,24 +284,34 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
     off = lay.comm_off
     win_lo = off[:-1] // WIN_ALIGN * WIN_ALIGN
     win_hi = (off[1:] + WIN_ALIGN - 1) // WIN_ALIGN * WIN_ALIGN
-    stageable = (win_hi - win_lo) <= smem_nodes
+    npass_c = community_passes(off, smem_nodes)
+    if lay.intra_split is not None and lay.pass_nodes != smem_nodes:
+        raise InputError("layout sub-runs were cut for another window capacity")
+    if lay.intra_split is None:  # a layout without sub-runs: wide communities unstaged
+        npass_c = np.where(npass_c == 1, 1, 0)
+    stageable = npass_c >= 1
+    multi = npass_c > 1
     seg_rblk, seg_win, seg_base, cta_seg = [0], [], [], [0]
     for b in range(n_cta):
         rb, rb_end = int(cta_bounds[b]), int(cta_bounds[b + 1])
         while rb < rb_end:
             c = int(lay.rblk_comm[rb])
             start = rb
-            if c < 0 or not stageable[c]:  # unstaged run of one community / the pool
+            if c < 0 or not stageable[c] or multi[c]:  # a run of one community / the pool
                 while (rb < rb_end and lay.rblk_comm[rb] == c
                        and rows[rb + 1] - rows[start] <= rows_cap):
                     rb += 1
-                seg_win.append((0, 0))
-                seg_base.append(int(off[c]) if c >= 0 else 0)
+                if c >= 0 and multi[c]:  # staged in passes over the community's window
+                    seg_win.append((int(win_lo[c]), int(win_hi[c])))
+                    seg_base.append(int(win_lo[c]))
+                else:  # unstaged: global gathers
+                    seg_win.append((0, 0))
+                    seg_base.append(int(off[c]) if c >= 0 else 0)
             else:  # staged window over whole communities, 128-byte aligned
                 w0 = int(win_lo[c])
                 while rb < rb_end:
                     cc = int(lay.rblk_comm[rb])
-                    if cc < 0 or not stageable[cc]:
+                    if cc < 0 or not stageable[cc] or multi[cc]:
                         break
                     if (int(win_hi[cc]) - w0 > smem_nodes or rows[rb + 1] - rows[start] > rows_cap
                             or cc - c >= SEG_MAX_COMM):
@@ -296,7 +354,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         if newc.size and (newc.min() < 0 or newc.max() >= INTRA_PAD):
             raise InputError("rebased intra column out of uint16 range")
         col[m] = newc.astype(np.uint16)
-    _bank_order(col, lay.intra_ptr, smem_nodes)
+    _bank_order(col, _sub_run_ptr(lay), smem_nodes)
     # lanes per row: rows in flight matter more than lanes per row (measured:
     # 16/32 lanes per row double the gather time); short rows use 4 lanes
     seg_rows = rows[seg_rblk]
@@ -311,6 +369,17 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         seg_lpr = np.where(lens > 24, 8, 4).astype(np.int32)
     return Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
                     seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, col)
+
+
+def _sub_run_ptr(lay: HostLayout) -> np.ndarray:
+    """run boundaries for the bank ordering: rows, split at pass sub-runs"""
+    if lay.intra_split is None:
+        return lay.intra_ptr
+    sp = lay.intra_split
+    extra = [lay.intra_ptr[:-1][sp != 0] + 8 * ((sp[sp != 0] >> np.uint64(16 * q)) &
+                                                np.uint64(0xFFFF)).astype(np.int64)
+             for q in range(MAX_PASS - 1)]
+    return np.unique(np.concatenate([lay.intra_ptr] + extra))
 
 
 def _bank_order(col: np.ndarray, ptr: np.ndarray, smem_nodes: int) -> None:
@@ -336,7 +405,7 @@ class DeviceGraph:
     cdk_graph struct handed to the C ABI."""
 
     def __init__(self, dec: Decomposition, device=None, sm_count: int | None = None,
-                 row_range=None):
+                 row_range=None, smem_budget: int = SMEM_OPTIN - 2048):
         import torch
 
         from ._lib import CdkGraph
@@ -344,8 +413,9 @@ class DeviceGraph:
         dev = torch.device(device if device is not None else "cuda")
         if sm_count is None:
             sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-        lay = build_layout(dec, row_range=row_range)
-        sch = build_schedule(lay, sm_count=sm_count)
+        lay = build_layout(dec, row_range=row_range,
+                           pass_nodes=window_nodes(ROWS_CAP, smem_budget))
+        sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget)
         self.row_range = (0, lay.n_rows) if row_range is None else tuple(int(x) for x in row_range)
         self.layout = lay
         self.schedule = sch
@@ -374,6 +444,8 @@ class DeviceGraph:
             "cta_seg": up(sch.cta_seg),
             "seg_lpr": up(sch.seg_lpr if sch.n_seg else np.zeros(1, np.int32)),
         }
+        if lay.intra_split is not None:
+            self._t["intra_split"] = up(lay.intra_split.view(np.int64))
         # keep a 16-byte tail on intra_col so uint4 loads never run past the allocation
         if self._t["intra_col"].numel() == 0:
             self._t["intra_col"] = torch.full((8,), -1, dtype=torch.int16, device=dev)
@@ -391,6 +463,7 @@ class DeviceGraph:
             comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
             seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
             cta_seg=t["cta_seg"].data_ptr(), seg_lpr=t["seg_lpr"].data_ptr(),
+            intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
         )
 
     def device_bytes(self) -> int:
@@ -398,7 +471,8 @@ class DeviceGraph:
 
     @classmethod
     def from_device_csr(cls, lay: "HostLayout", intra_col_dev, inter_col_dev, device,
-                        sm_count: int | None = None):
+                        sm_count: int | None = None, split_dev=None,
+                        smem_budget: int = SMEM_OPTIN - 2048):
         """Graph whose columns were generated on the device (config 5): the
         schedule is planned from the host copies of the row pointers and the
         intra columns are rebased in place on the device."""
@@ -410,7 +484,7 @@ class DeviceGraph:
         dev = torch.device(device)
         if sm_count is None:
             sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-        sch = build_schedule(lay, sm_count=sm_count)
+        sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget)
         self.layout, self.schedule = lay, sch
         self.n_rows, self.n_comm, self.device = lay.n_rows, lay.n_comm, dev
         self.row_range = (0, lay.n_rows)
@@ -430,6 +504,8 @@ class DeviceGraph:
             "seg_win": up(sch.seg_win.reshape(-1)), "seg_base": up(sch.seg_base),
             "cta_seg": up(sch.cta_seg), "seg_lpr": up(sch.seg_lpr),
         }
+        if split_dev is not None:
+            self._t["intra_split"] = split_dev
         t = self._t
         delta = up(sch.row_delta)
         lib = load_library()
@@ -447,5 +523,6 @@ class DeviceGraph:
             comm_rblk_off=t["comm_rblk_off"].data_ptr(), seg_rblk=t["seg_rblk"].data_ptr(),
             seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
             cta_seg=t["cta_seg"].data_ptr(), seg_lpr=t["seg_lpr"].data_ptr(),
+            intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
         )
         return self

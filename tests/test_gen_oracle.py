@@ -39,7 +39,8 @@ def test_hash_matches_known_values():
 def test_oracle_csr_properties():
     c = _case()
     off, cdf, n_edges, thr = c.gen_inputs()
-    (iptr, icol, xptr, xcol), (iu, iv, sg) = OG.generate_csr(c.graph_seed, off, cdf, n_edges, thr)
+    (iptr, icol, xptr, xcol, _), (iu, iv, sg) = OG.generate_csr(c.graph_seed, off, cdf, n_edges,
+                                                                  thr)
     n = c.n
     comm = np.repeat(np.arange(off.shape[0] - 1), np.diff(off))
     # intra: padded to 8, ascending local columns, symmetric, density ~ 1 - p_in
@@ -66,3 +67,71 @@ def test_oracle_csr_properties():
     assert (iu == iv).sum() == off[-1]
     assert np.all(np.diff(iu * n + iv) > 0)
     assert 2 * (iu != iv).sum() == real.sum() + xcol.shape[0]
+
+
+def _dec_from_triples(off, n, iu, iv, sg):
+    from paper_2203_16657_b200 import graph as G
+
+    part = G.Partition.from_assignment(np.repeat(np.arange(off.shape[0] - 1), np.diff(off)))
+    return G.Decomposition(part, G.SparseCorrection(iu, iv, sg), n)
+
+
+def test_host_layout_matches_generator_layout_with_passes():
+    """plan.build_layout on the generator's triples reproduces the generator's
+    CSR bit for bit, including the per-pass sub-runs (window of
+    192 nodes: staged, multi-pass and unstaged communities all present)."""
+    from paper_2203_16657_b200 import plan
+
+    c = gen.scaled_config5(n=5000, lo=100, hi=1400, seed=58)
+    off, cdf, n_edges, thr = c.gen_inputs()
+    wn = 192
+    npass = plan.community_passes(off, wn)
+    assert (npass == 1).any() and (npass > 1).any() and (npass == 0).any()
+    (iptr, icol, xptr, xcol, split), (iu, iv, sg) = OG.generate_csr(c.graph_seed, off, cdf,
+                                                                     n_edges, thr, wn)
+    lay = plan.build_layout(_dec_from_triples(off, c.n, iu, iv, sg), pass_nodes=wn)
+    assert np.array_equal(lay.intra_ptr, iptr)
+    assert np.array_equal(lay.intra_col, icol)
+    assert np.array_equal(lay.intra_split, split)
+    assert np.array_equal(lay.inter_ptr, xptr)
+    assert np.array_equal(lay.inter_col, xcol)
+
+
+def test_schedule_multipass_segments():
+    from paper_2203_16657_b200 import plan
+
+    c = gen.scaled_config5(n=5000, lo=100, hi=1400, seed=58)
+    off, cdf, n_edges, thr = c.gen_inputs()
+    _, (iu, iv, sg) = OG.generate_csr(c.graph_seed, off, cdf, n_edges, thr)
+    budget = plan.stage_smem_bytes(192) - 128
+    wn = plan.window_nodes(plan.ROWS_CAP, budget)
+    lay = plan.build_layout(_dec_from_triples(off, c.n, iu, iv, sg), pass_nodes=wn)
+    sch = plan.build_schedule(lay, sm_count=16, smem_budget=budget)
+    npass = plan.community_passes(off, wn)
+    rows = lay.rblk_row0
+    for s_ in range(sch.n_seg):
+        rb0, rb1 = sch.seg_rblk[s_], sch.seg_rblk[s_ + 1]
+        comms = set(lay.rblk_comm[rb0:rb1].tolist())
+        w0, w1 = sch.seg_win[s_]
+        if w1 > w0 and (w1 - w0) > wn:  # multi-pass: one community, its whole window
+            assert len(comms) == 1
+            cc = comms.pop()
+            assert npass[cc] > 1 and w0 == off[cc] // 8 * 8
+            assert rows[rb1] - rows[rb0] <= sch.seg_rows_cap
+        # every rebased real column of pass q lies in [q wn, (q+1) wn)
+        multi = w1 > w0 and (w1 - w0) > wn
+        for i in range(rows[rb0], min(rows[rb1], rows[rb0] + 40)):
+            e0, e1 = lay.intra_ptr[i], lay.intra_ptr[i + 1]
+            col = sch.intra_col[e0:e1].astype(np.int64)
+            if not multi:
+                if w1 > w0:
+                    assert np.all(col[col != 0xFFFF] < w1 - w0)
+                continue
+            np_ = int((w1 - w0 + wn - 1) // wn)
+            sp = int(lay.intra_split[i])
+            cuts = [0] + [8 * ((sp >> (16 * q)) & 0xFFFF) for q in range(np_ - 1)] + [e1 - e0]
+            for q in range(np_):
+                sub = col[cuts[q]:cuts[q + 1]]
+                assert (cuts[q + 1] - cuts[q]) % 8 == 0
+                sub = sub[sub != 0xFFFF]
+                assert np.all((sub >= q * wn) & (sub < (q + 1) * wn))

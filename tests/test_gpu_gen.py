@@ -24,9 +24,10 @@ def case():
 
 
 def test_device_csr_bit_exact(case):
-    c, ((iptr, icol, xptr, xcol), _) = case
+    c, ((iptr, icol, xptr, xcol, split), _) = case
     csr = gen.generate(c, "cuda")
     dptr, dcol, dxptr, dxcol = csr.to_host()
+    assert np.array_equal(csr.split_host(), split)
     assert np.array_equal(dptr, iptr)
     assert np.array_equal(dcol, icol)
     assert np.array_equal(dxptr, xptr)
@@ -72,6 +73,85 @@ def test_generated_graph_rhs_and_rk4_vs_oracle(case):
     assert err <= 1e-9, err
 
 
+def _small_window_case():
+    c = gen.scaled_config5(n=5000, lo=100, hi=1400, seed=58)
+    from paper_2203_16657_b200 import plan
+
+    budget = plan.stage_smem_bytes(192) - 128  # 192-node window: 3 gather modes present
+    return c, budget, plan.window_nodes(plan.ROWS_CAP, budget)
+
+
+def test_multipass_generated_graph_vs_oracle():
+    """Communities wider than the window, staged in passes (cdk_graph.intra_split):
+    generator CSR bit-exact, RHS and 30 RK4 steps vs the oracle."""
+    import torch
+
+    from paper_2203_16657_b200 import plan
+    from paper_2203_16657_b200.engine import KuramotoEngine
+
+    c, budget, wn = _small_window_case()
+    off, cdf, n_edges, thr = c.gen_inputs()
+    npass = plan.community_passes(off, wn)
+    assert (npass == 1).any() and (npass > 1).any() and (npass == 0).any()
+    (iptr, icol, xptr, xcol, split), (iu, iv, sg) = OG.generate_csr(c.graph_seed, off, cdf,
+                                                                     n_edges, thr, wn)
+    csr = gen.generate(c, "cuda", pass_nodes=wn)
+    dptr, dcol, dxptr, dxcol = csr.to_host()
+    assert np.array_equal(dptr, iptr) and np.array_equal(dcol, icol)
+    assert np.array_equal(csr.split_host(), split)
+    assert np.array_equal(dxptr, xptr) and np.array_equal(dxcol, xcol)
+
+    omega, theta0 = c.state()
+    omega = np.clip(omega, -20, 20)
+    dg, _ = gen.device_graph(c, "cuda", smem_budget=budget)
+    segw = dg.schedule.seg_win
+    assert ((segw[:, 1] - segw[:, 0]) > wn).any()  # multi-pass segments scheduled
+    eng = KuramotoEngine(None, omega, coupling=c.coupling, norm=c.n, graph=dg)
+    k = eng.rhs(torch.from_numpy(theta0).cuda()).cpu().numpy()
+    ko = cia.kuramoto_rhs_cia(K, theta0, omega, off, iu, iv, sg, c.coupling, c.n)
+    assert np.abs(k - ko).max() <= 1e-13
+
+    def rhs(x):
+        return cia.kuramoto_rhs_cia(K, x, omega, off, iu, iv, sg, c.coupling, c.n)
+
+    ref, _ = cia.rk4_integrate(rhs, theta0, c.dt, 30)
+    eng.set_state(theta0)
+    eng.rk4(c.dt, 30)
+    eng.check()
+    assert cia.circ_dist(eng.theta.cpu().numpy(), ref).max() <= 1e-9
+
+
+def test_multipass_host_layout_vs_oracle():
+    """The same pass machinery through plan.build_layout (Decomposition input,
+    bank-ordered sub-runs): config-2 family with a 192-node window."""
+    import torch
+
+    from paper_2203_16657_b200 import configs, plan
+    from paper_2203_16657_b200.engine import KuramotoEngine
+
+    cs = configs.scaled_config2(20000, 24, seed=9)
+    dec = cs.decomposition()
+    omega, theta0 = cs.state()
+    budget = plan.stage_smem_bytes(192) - 128
+    dg = plan.DeviceGraph(dec, smem_budget=budget)
+    assert dg.layout.intra_split is not None
+    eng = KuramotoEngine(dec, omega, coupling=cs.coupling, norm=cs.n, graph=dg)
+    s = dec.correction
+    k = eng.rhs(torch.from_numpy(theta0).cuda()).cpu().numpy()
+    ko = cia.kuramoto_rhs_cia(K, theta0, omega, dec.offsets, s.iu, s.iv, s.sgn, cs.coupling, cs.n)
+    assert np.abs(k - ko).max() <= 1e-13
+
+    def rhs(x):
+        return cia.kuramoto_rhs_cia(K, x, omega, dec.offsets, s.iu, s.iv, s.sgn, cs.coupling,
+                                    cs.n)
+
+    ref, _ = cia.rk4_integrate(rhs, theta0, cs.dt, 20)
+    eng.set_state(theta0)
+    eng.rk4(cs.dt, 20)
+    eng.check()
+    assert cia.circ_dist(eng.theta.cpu().numpy(), ref).max() <= 1e-9
+
+
 def test_full_size_row_regeneration():
     """BASELINE-size config 5: sampled intra rows regenerated by the numpy
     restatement; inter symmetry on sampled rows; totals near SURVEY App. A.4."""
@@ -91,7 +171,7 @@ def test_full_size_row_regeneration():
         h = OG.hash4(c.graph_seed, np.full_like(b, cc), lo.astype(np.uint32), hi.astype(np.uint32))
         want = np.nonzero((h < np.uint32(thr)) & (b != a))[0]
         s, e = int(csr.intra_ptr[i]), int(csr.intra_ptr[i + 1])
-        got = csr.intra_col[s:e].cpu().numpy().view(np.uint16)
+        got = csr.intra_col[s:e].cpu().numpy().view(np.uint16)  # ascending across sub-runs
         got = got[got != 0xFFFF].astype(np.int64)
         assert np.array_equal(got, want)
     xptr = csr.inter_ptr

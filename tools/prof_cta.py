@@ -6,8 +6,15 @@ os.environ.setdefault("CDK_LIB", os.path.join(REPO, "paper_2203_16657_b200/_buil
 import numpy as np, torch
 from paper_2203_16657_b200 import configs
 from paper_2203_16657_b200.engine import KuramotoEngine
-c = configs.config2(); dec = c.decomposition(); omega, theta0 = c.state()
-eng = KuramotoEngine(dec, omega, coupling=c.coupling, norm=c.n)
+if "--cfg5" in sys.argv:
+    from paper_2203_16657_b200 import gen
+    c = gen.config5() if "--small" not in sys.argv else gen.scaled_config5(400_000, 1000, 20000)
+    omega, theta0 = c.state()
+    dg, _ = gen.device_graph(c, "cuda")
+    eng = KuramotoEngine(None, omega, coupling=c.coupling, norm=c.n, graph=dg)
+else:
+    c = configs.config2(); dec = c.decomposition(); omega, theta0 = c.state()
+    eng = KuramotoEngine(dec, omega, coupling=c.coupling, norm=c.n)
 sch = eng.graph.schedule; lay = eng.graph.layout
 prof = torch.zeros(4 * sch.n_cta, dtype=torch.int64, device="cuda")
 eng.lib.cdk_debug_set_profile_buffer(prof.data_ptr())
@@ -24,17 +31,18 @@ for b in range(sch.n_cta):
     r0, r1 = seg_rows[s0], seg_rows[s1]
     ent = lay.intra_ptr[r1] - lay.intra_ptr[r0]
     xen = lay.inter_ptr[r1] - lay.inter_ptr[r0]
-    win = sum(int(sch.seg_win[s][1] - sch.seg_win[s][0]) for s in range(s0, s1))
-    feat.append((r1 - r0, ent, xen, s1 - s0, win))
+    un = sum(int(lay.intra_ptr[seg_rows[s + 1]] - lay.intra_ptr[seg_rows[s]])
+             for s in range(s0, s1) if sch.seg_win[s][1] == sch.seg_win[s][0])
+    feat.append((r1 - r0, ent - un, un, xen, s1 - s0))
 F = np.array(feat, dtype=np.float64)
 np.set_printoptions(linewidth=150)
 print("cycles total/stage/gather/epi: mean", P.mean(0).astype(int), "max", P.max(0).astype(int), "min", P.min(0).astype(int))
-print("rows/entries/inter/segs/window: mean", F.mean(0).astype(int), "max", F.max(0).astype(int), "min", F.min(0).astype(int))
+print("rows/staged ent/unstaged ent/inter/segs: mean", F.mean(0).astype(int), "max", F.max(0).astype(int), "min", F.min(0).astype(int))
 X = np.column_stack([F[:, :5], np.ones(len(F))])
 for j, name in enumerate(["total", "stage", "gather", "epi"]):
     coef, *_ = np.linalg.lstsq(X, P[:, j], rcond=None)
     pred = X @ coef
-    print(name, "fit rows/ent/inter/segs/win/const", np.round(coef, 3), "R2", round(1 - ((P[:, j] - pred) ** 2).sum() / ((P[:, j] - P[:, j].mean()) ** 2).sum(), 3))
+    print(name, "fit rows/staged/unstaged/inter/segs/const", np.round(coef, 3), "R2", round(1 - ((P[:, j] - pred) ** 2).sum() / ((P[:, j] - P[:, j].mean()) ** 2).sum(), 3))
 order = np.argsort(-P[:, 0])[:8]
 for b in order: print("slow cta", b, P[b].astype(int), F[b].astype(int))
 order = np.argsort(P[:, 0])[:4]
