@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 7
+#define CDK_ABI_VERSION 8
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -103,6 +103,8 @@ CDK_API int cdk_dense_poly(const double *x, const int64_t *offsets, int64_t m_co
  *             capacity (and the NONE pool), in global memory (w0 == w1).
  * Padding contract (bulk copies move 16-byte units): intra_ptr / inter_ptr
  * readable up to index n_rows + 3, theta / omega up to n_rows + 1. */
+#define CDK_SEG_INTER_PHASE 256
+
 typedef struct cdk_graph {
   int64_t n_rows;
   int64_t n_comm;
@@ -124,7 +126,8 @@ typedef struct cdk_graph {
   const int64_t *seg_win;       /* [2*n_seg] staged node window [w0, w1) */
   const int64_t *seg_base;      /* [n_seg] base of the segment's intra columns */
   const int32_t *cta_seg;       /* [n_cta+1] segment boundaries per CTA */
-  const int32_t *seg_lpr;       /* [n_seg] lanes per row of the segment's gathers (4|8|16|32) */
+  const int32_t *seg_lpr;       /* [n_seg] lanes per row of the segment's gathers (4|8|16|32),
+                                   | CDK_SEG_INTER_PHASE: inter entries in a separate phase */
   /* Communities wider than the window (smem_nodes) but at most 4 windows
    * wide are staged in passes of smem_nodes nodes: each row's intra run is
    * then up to 4 sub-runs (one per pass, each padded to 8, columns of pass p
@@ -132,6 +135,14 @@ typedef struct cdk_graph {
    * packs the sub-run starts in 8-entry chunks from the row start (bits
    * 0-15: pass 1, 16-31: pass 2, 32-47: pass 3).  NULL if no such community. */
   const uint64_t *intra_split;  /* [n_rows] or NULL */
+  /* Large graphs (z above the L2 share): inter entries are swept per CTA in
+   * inter_blocks column blocks of inter_block_nodes nodes (all rows for
+   * block 0, then block 1, ...), so the random z gathers of the whole GPU hit
+   * one L2-resident block at a time; inter_split[row] packs the block
+   * sub-run starts like intra_split (entries from the row start).  0 = off. */
+  int32_t inter_blocks;         /* 0 or 2..4 */
+  int32_t inter_block_nodes;
+  const uint64_t *inter_split;  /* [n_rows] or NULL (see cdk_inter_split) */
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */
@@ -305,6 +316,11 @@ CDK_API int cdk_gen_inter_compact(int64_t n_rows, const int64_t *ptr_raw, const 
 /* add delta[row] to every non-padding intra column (segment-window rebasing) */
 CDK_API int cdk_gen_rebase(int64_t n_rows, const int64_t *ptr, const int32_t *delta,
                            uint16_t *col, void *stream);
+/* cdk_graph.inter_split of a row-sorted inter CSR (device arrays): block q
+ * sub-run = columns in [q*block_nodes, (q+1)*block_nodes); rows longer than
+ * 65535 entries are rejected */
+CDK_API int cdk_inter_split(int64_t n_rows, const int64_t *ptr, const int32_t *col, int blocks,
+                            int block_nodes, uint64_t *split, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* host-side planning (no device needed)                                    */

@@ -46,6 +46,9 @@ class CdkGraph(ctypes.Structure):
         ("cta_seg", P),
         ("seg_lpr", P),
         ("intra_split", P),
+        ("inter_blocks", I32),
+        ("inter_block_nodes", I32),
+        ("inter_split", P),
     ]
 
 
@@ -141,6 +144,7 @@ _SIGS = {
     "cdk_gen_inter_sort": [I64, P, P, P, P],
     "cdk_gen_inter_compact": [I64, P, P, P, P, P],
     "cdk_gen_rebase": [I64, P, P, P, P],
+    "cdk_inter_split": [I64, P, P, ctypes.c_int, ctypes.c_int, P, P],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],
@@ -157,7 +161,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _lock = threading.Lock()
 _lib = None

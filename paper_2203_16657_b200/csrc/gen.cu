@@ -335,3 +335,53 @@ extern "C" int cdk_gen_rebase(int64_t n_rows, const int64_t *ptr, const int32_t 
   CDK_CHECK_LAUNCH("gen_rebase_kernel");
   return CDK_OK;
 }
+
+namespace cdk {
+// warp per row: block sub-run starts of a sorted inter run (ballot counts)
+__global__ void inter_split_kernel(int64_t n_rows, const int64_t *ptr, const int32_t *col,
+                                   int blocks, int block_nodes, uint64_t *split, int *bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows; i += warps) {
+    const int64_t b = ptr[i], e = ptr[i + 1];
+    if (e - b > 0xFFFF) {
+      if (lane == 0) atomicExch(bad, 1);
+      continue;
+    }
+    int cnt[4] = {0, 0, 0, 0};  // entries below block boundary q+1
+    for (int64_t q = b + lane; q < e; q += 32) {
+      const int c = col[q];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cnt[k] += (k + 1 < blocks && c < (k + 1) * block_nodes) ? 1 : 0;
+    }
+    uint64_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      int v = cnt[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (k + 1 < blocks) w |= (uint64_t)v << (16 * k);
+    }
+    if (lane == 0) split[i] = w;
+  }
+}
+}  // namespace cdk
+
+extern "C" int cdk_inter_split(int64_t n_rows, const int64_t *ptr, const int32_t *col, int blocks,
+                               int block_nodes, uint64_t *split, void *stream) {
+  if (blocks < 2 || blocks > 4 || block_nodes <= 0) return set_error("inter_split: bad blocks"), CDK_INPUT;
+  int *bad = nullptr;
+  cudaError_t e = cudaMallocAsync(&bad, sizeof(int), as_stream(stream));
+  if (e != cudaSuccess) return cuda_status(e, "inter_split alloc");
+  cudaMemsetAsync(bad, 0, sizeof(int), as_stream(stream));
+  cdk::inter_split_kernel<<<cdk::gen_grid(n_rows, 8), 256, 0, as_stream(stream)>>>(
+      n_rows, ptr, col, blocks, block_nodes, split, bad);
+  CDK_CHECK_LAUNCH("inter_split_kernel");
+  int hbad = 0;
+  cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream));
+  cudaFreeAsync(bad, as_stream(stream));
+  e = cudaStreamSynchronize(as_stream(stream));
+  if (e != cudaSuccess) return cuda_status(e, "inter_split");
+  if (hbad) return set_error("inter_split: a row has more than 65535 inter entries"), CDK_INPUT;
+  return CDK_OK;
+}

@@ -44,6 +44,7 @@ struct Workspace {
   double2 *part[2];  // canonical rblock partials of z (ping-pong with z)
   cdk_run_status *status;
   unsigned int *bar;  // grid-barrier counter of the persistent kernel
+  double2 *xacc;      // per-row inter sums (block-phased inter sweep only)
 };
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -66,6 +67,7 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
   w.part[1] = (double2 *)take(((size_t)g->n_rblk + 1) * sizeof(double2));
   w.status = (cdk_run_status *)take(sizeof(cdk_run_status));
   w.bar = (unsigned int *)take(256);
+  w.xacc = g->inter_blocks > 0 ? (double2 *)take(n * sizeof(double2)) : nullptr;
   if (total) *total = off;
   return w;
 }
@@ -81,6 +83,7 @@ struct StageArgs {
   const double *omega;
   double *ksum;
   double *out;  // MODE 0
+  double2 *xacc;  // block-phased inter sums (g.inter_blocks > 0)
   double k_over_n;
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
@@ -265,7 +268,7 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
                                              uint32_t zero_slot, const double2 *zglob,
                                              const uint4 *__restrict__ colv,
                                              const int32_t *__restrict__ xcol, int pass,
-                                             int npass) {
+                                             int npass, bool inter_inline) {
   constexpr int NG = NTHREADS / LPR;
   constexpr int STRIDE = 8 * LPR;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -285,7 +288,8 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
         if (pass > 0) e0 += 8 * (int)((sw >> (16 * (pass - 1))) & 0xFFFFu);
       }
       R.x0 = (int)(sm.sxp[li] - xbase);
-      R.x1 = pass == 0 ? (int)(sm.sxp[li + 1] - xbase) : R.x0;  // inter entries: pass 0
+      // inter entries: in pass 0, unless the segment runs a separate inter phase
+      R.x1 = (pass == 0 && inter_inline) ? (int)(sm.sxp[li + 1] - xbase) : R.x0;
       R.p = e0 + 8 * t;
       R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
     }
@@ -342,6 +346,104 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
   }
 }
 
+// Separate inter phase (segments whose rows carry many inter entries, e.g.
+// config 5's ~400 per row): 8 lanes per row, each lane keeps IU independent
+// random z gathers in flight (the inline path keeps one), fixed per-lane
+// order + 8-lane butterfly, added onto the row's intra sum.
+template <int IU>
+__device__ __forceinline__ void inter_phase(const StageArgs &a, const SegSmem &sm, int nrows,
+                                            int64_t row0, int64_t row0a, int64_t xbase,
+                                            const int32_t *__restrict__ xcol) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t = lane & 7, grp = tid >> 3;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  const double2 *__restrict__ z_in = a.z_in;
+  for (int r = grp; r < nrows; r += NGROUPS) {
+    const int64_t li = row0 + r - row0a;
+    const int x0 = (int)(sm.sxp[li] - xbase), x1 = (int)(sm.sxp[li + 1] - xbase);
+    double sr = 0.0, si = 0.0;
+    for (int p = x0 + t; p < x1; p += 8 * IU) {
+      int j[IU];
+#pragma unroll
+      for (int k = 0; k < IU; ++k) j[k] = (p + 8 * k < x1) ? ldg(xcol + p + 8 * k) : -1;
+      double2 z[IU];
+#pragma unroll
+      for (int k = 0; k < IU; ++k) z[k] = (j[k] >= 0) ? ldz(z_in + j[k]) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < IU; ++k) {
+        sr += z[k].x;
+        si += z[k].y;
+      }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      sr += __shfl_xor_sync(gmask, sr, o);
+      si += __shfl_xor_sync(gmask, si, o);
+    }
+    if (t == 0) {
+      const double2 prev = sm.acc[r];
+      sm.acc[r] = make_double2(prev.x + sr, prev.y + si);
+    }
+  }
+}
+
+// Block-phased inter sweep (g.inter_blocks > 0; config 5): before its
+// segments, the CTA sums the inter entries of all its rows, column block by
+// column block, into xacc (one 8-lane group per row, IU independent gathers
+// per lane; block q adds onto block q-1's sum in a fixed order).  All CTAs
+// walk the blocks at about the same pace, so the random z gathers of the
+// whole GPU fall into one ~inter_block_nodes*16-byte slice of z that stays
+// L2-resident instead of thrashing HBM.
+template <int IU>
+__device__ __forceinline__ void inter_sweep(const StageArgs &a) {
+  const cdk_graph &g = a.g;
+  const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
+  if (segA == segB) return;
+  const int64_t rA = g.rblk_row0[g.seg_rblk[segA]], rB = g.rblk_row0[g.seg_rblk[segB]];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t = lane & 7, grp = tid >> 3;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  const double2 *__restrict__ z_in = a.z_in;
+  const int nb = g.inter_blocks;
+  for (int q = 0; q < nb; ++q) {
+    for (int64_t i = rA + grp; i < rB; i += NGROUPS) {
+      const int64_t xb = __ldg(g.inter_ptr + i), xe = __ldg(g.inter_ptr + i + 1);
+      const uint64_t sw = __ldg(g.inter_split + i);
+      const int64_t s0 = xb + (q ? (int64_t)((sw >> (16 * (q - 1))) & 0xFFFFu) : 0);
+      const int64_t s1 = (q + 1 < nb) ? xb + (int64_t)((sw >> (16 * q)) & 0xFFFFu) : xe;
+      double sr = 0.0, si = 0.0;
+      for (int64_t p = s0 + t; p < s1; p += 8 * IU) {
+        int j[IU];
+#pragma unroll
+        for (int k = 0; k < IU; ++k) j[k] = (p + 8 * k < s1) ? ldg(g.inter_col + p + 8 * k) : -1;
+        double2 z[IU];
+#pragma unroll
+        for (int k = 0; k < IU; ++k)
+          z[k] = (j[k] >= 0) ? ldz(z_in + j[k]) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < IU; ++k) {
+          sr += z[k].x;
+          si += z[k].y;
+        }
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(gmask, sr, o);
+        si += __shfl_xor_sync(gmask, si, o);
+      }
+      if (t == 0) {
+        if (q > 0) {
+          const double2 prev = ldcg2(a.xacc + i);
+          sr = prev.x + sr;
+          si = prev.y + si;
+        }
+        __stcg(a.xacc + i, make_double2(sr, si));
+      }
+    }
+  }
+  __syncthreads();
+}
+
 struct ProfAcc {
   unsigned long long t_stage = 0, t_gather = 0, t_epi = 0, t_mark = 0;
 };
@@ -363,6 +465,8 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
   const int wn = g.smem_nodes;
   // mbarrier phases: bar_seg completes once per pass, bar_epi once per segment
   uint32_t pseg = (parity >> 1) & 1u, pepi = parity & 1u;
+  const bool swept = g.inter_blocks > 0;
+  if (swept) inter_sweep<8>(a);
 #ifdef CDK_PROFILE
 #define PROF_MARK(acc)                           \
   do {                                           \
@@ -450,7 +554,9 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     const int64_t ebase = sm.sip[row0 - row0a], xbase = sm.sxp[row0 - row0a];
     const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col + ebase);
     const int32_t *__restrict__ xcol = g.inter_col + xbase;
-    const int lpr = g.seg_lpr[s];
+    const int lpr = g.seg_lpr[s] & 0xFF;
+    const bool inter_inline = !swept && (g.seg_lpr[s] & CDK_SEG_INTER_PHASE) == 0;
+    const bool inter_phased = !swept && !inter_inline;
 
     // ---- 2. gather: lanes per row chosen per segment (4 / 8 / 16 / 32); a
     //         community wider than the window is gathered in passes, each
@@ -474,22 +580,26 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
       switch (lpr) {
         case 32:
           gather_phase<32>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                           colv, xcol, pass, npass);
+                           colv, xcol, pass, npass, inter_inline);
           break;
         case 16:
           gather_phase<16>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                           colv, xcol, pass, npass);
+                           colv, xcol, pass, npass, inter_inline);
           break;
         case 4:
           gather_phase<4>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                          colv, xcol, pass, npass);
+                          colv, xcol, pass, npass, inter_inline);
           break;
         default:
           gather_phase<8>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                          colv, xcol, pass, npass);
+                          colv, xcol, pass, npass, inter_inline);
       }
     }
     __syncthreads();
+    if (inter_phased) {
+      inter_phase<8>(a, sm, nrows, row0, row0a, xbase, xcol);
+      __syncthreads();
+    }
     PROF_MARK(t_gather);
 
     // ---- 3. epilogue: warp per rblock, lane = row ---------------------------
@@ -505,7 +615,11 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
       if (lane < nr) {
         const int64_t i = rrow0 + lane;
         const int64_t li = i - row0a;
-        const double2 ac = sm.acc[i - row0];
+        double2 ac = sm.acc[i - row0];
+        if (swept) {
+          const double2 xa = ldcg2(a.xacc + i);
+          ac = make_double2(ac.x + xa.x, ac.y + xa.y);
+        }
         const double2 zi = (staged && npass == 1) ? sm.zs[i - w0] : ldz(z_in + i);
         const double2 R = (c >= 0) ? sR[c - cA] : make_double2(0.0, 0.0);
         double k = sm.som[li] + kn * (R.y * zi.x - R.x * zi.y);
@@ -705,6 +819,11 @@ static int check_graph(const cdk_graph *g) {
     set_error("cdk_graph: bad shared-memory capacities");
     return CDK_INPUT;
   }
+  if (g->inter_blocks != 0 &&
+      (g->inter_blocks < 2 || g->inter_blocks > 4 || !g->inter_split || g->inter_block_nodes <= 0)) {
+    set_error("cdk_graph: inter_blocks must be 0 or 2..4 with inter_split set");
+    return CDK_INPUT;
+  }
   return CDK_OK;
 }
 
@@ -757,6 +876,7 @@ static StageArgs base_args(const cdk_graph *g, const Workspace &w, double *theta
   a.theta = theta;
   a.omega = omega;
   a.ksum = w.ksum;
+  a.xacc = w.xacc;
   a.k_over_n = k_over_n;
   return a;
 }

@@ -333,15 +333,8 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
         cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
         delta[rows[0]: rows[-1]] = cstart - seg_base[seg_of_row]
+    seg_lpr = _seg_lanes(lay, rows[seg_rblk])
     if lay.intra_col is None:  # columns live on the device: caller rebases (cdk_gen_rebase)
-        import os
-
-        seg_rows = rows[seg_rblk]
-        lens = (lay.intra_ptr[seg_rows[1:]] - lay.intra_ptr[seg_rows[:-1]]) / np.maximum(
-            np.diff(seg_rows), 1)
-        forced = os.environ.get("CDK_LPR")
-        seg_lpr = (np.full(lens.shape[0], int(forced), dtype=np.int32) if forced
-                   else np.where(lens > 24, 8, 4).astype(np.int32))
         sch = Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
                        seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, None)
         sch.row_delta = delta.astype(np.int32)
@@ -355,20 +348,30 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
             raise InputError("rebased intra column out of uint16 range")
         col[m] = newc.astype(np.uint16)
     _bank_order(col, _sub_run_ptr(lay), smem_nodes)
-    # lanes per row: rows in flight matter more than lanes per row (measured:
-    # 16/32 lanes per row double the gather time); short rows use 4 lanes
-    seg_rows = rows[seg_rblk]
-    lens = (lay.intra_ptr[seg_rows[1:]] - lay.intra_ptr[seg_rows[:-1]]) / np.maximum(
-        np.diff(seg_rows), 1)
-    import os
-
-    forced = os.environ.get("CDK_LPR")
-    if forced:  # experiments: one width for every segment
-        seg_lpr = np.full(lens.shape[0], int(forced), dtype=np.int32)
-    else:
-        seg_lpr = np.where(lens > 24, 8, 4).astype(np.int32)
     return Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
                     seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, col)
+
+
+SEG_INTER_PHASE = 256  # include/commdyn_cuda.h CDK_SEG_INTER_PHASE
+INTER_PHASE_MIN = 16.0  # mean inter entries per row above which a segment runs the inter phase
+
+
+def _seg_lanes(lay: HostLayout, seg_rows: np.ndarray) -> np.ndarray:
+    """per-segment gather mode: lanes per row (rows in flight matter more than
+    lanes per row — measured: 16/32 lanes per row double the gather time;
+    short rows use 4) | SEG_INTER_PHASE for inter-heavy rows.  CDK_LPR and
+    CDK_INTER_PHASE (0/1) override for experiments."""
+    import os
+
+    nr = np.maximum(np.diff(seg_rows), 1)
+    lens = (lay.intra_ptr[seg_rows[1:]] - lay.intra_ptr[seg_rows[:-1]]) / nr
+    xl = (lay.inter_ptr[seg_rows[1:]] - lay.inter_ptr[seg_rows[:-1]]) / nr
+    forced = os.environ.get("CDK_LPR")
+    lpr = (np.full(lens.shape[0], int(forced), dtype=np.int32) if forced
+           else np.where(lens > 24, 8, 4).astype(np.int32))
+    fx = os.environ.get("CDK_INTER_PHASE")
+    sep = (np.full(lens.shape[0], fx == "1") if fx in ("0", "1") else xl > INTER_PHASE_MIN)
+    return (lpr | np.where(sep, SEG_INTER_PHASE, 0)).astype(np.int32)
 
 
 def _sub_run_ptr(lay: HostLayout) -> np.ndarray:
@@ -398,6 +401,47 @@ def _bank_order(col: np.ndarray, ptr: np.ndarray, smem_nodes: int) -> None:
                                  INTRA_PAD, int(smem_nodes) & 7)
     if rc != 0:
         raise InputError("cdk_host_bank_order failed")
+
+
+INTER_SWEEP_BYTES = 48 << 20  # z above this: block-phased inter sweep (cdk_graph.inter_blocks)
+INTER_BLOCK_BYTES = 40e6  # target z bytes per column block
+
+
+def inter_blocking(n_rows: int) -> tuple[int, int]:
+    """(inter_blocks, inter_block_nodes) for a graph of n_rows (CDK_INTER_BLOCKS
+    overrides the block count; 0 disables)."""
+    import os
+
+    forced = os.environ.get("CDK_INTER_BLOCKS")
+    if forced is not None:
+        nb = int(forced)
+    elif n_rows * 16 > INTER_SWEEP_BYTES:
+        nb = int(min(4, max(2, np.ceil(n_rows * 16 / INTER_BLOCK_BYTES))))
+    else:
+        nb = 0
+    if nb <= 1 or n_rows < 16:
+        return 0, 0
+    nb = min(nb, 4)
+    return nb, int((n_rows + nb - 1) // nb + 7) // 8 * 8
+
+
+def _attach_inter_split(self, lay_n_rows: int) -> None:
+    """compute cdk_graph.inter_split on the device when the sweep is on"""
+    import torch
+
+    from ._lib import check, load_library
+
+    nb, bn = inter_blocking(lay_n_rows)
+    self.inter_blocks, self.inter_block_nodes = nb, bn
+    if not nb:
+        return
+    t = self._t
+    t["inter_split"] = torch.zeros(lay_n_rows, dtype=torch.int64, device=self.device)
+    check(load_library().cdk_inter_split(lay_n_rows, t["inter_ptr"].data_ptr(),
+                                         t["inter_col"].data_ptr(), nb, bn,
+                                         t["inter_split"].data_ptr(),
+                                         torch.cuda.current_stream(self.device).cuda_stream),
+          "inter_split")
 
 
 class DeviceGraph:
@@ -451,6 +495,7 @@ class DeviceGraph:
             self._t["intra_col"] = torch.full((8,), -1, dtype=torch.int16, device=dev)
         if self._t["inter_col"].numel() == 0:
             self._t["inter_col"] = torch.zeros(4, dtype=torch.int32, device=dev)
+        _attach_inter_split(self, lay.n_rows)
         t = self._t
         self.struct = CdkGraph(
             n_rows=lay.n_rows, n_comm=lay.n_comm,
@@ -464,6 +509,8 @@ class DeviceGraph:
             seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
             cta_seg=t["cta_seg"].data_ptr(), seg_lpr=t["seg_lpr"].data_ptr(),
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
+            inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
+            inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
         )
 
     def device_bytes(self) -> int:
@@ -506,6 +553,7 @@ class DeviceGraph:
         }
         if split_dev is not None:
             self._t["intra_split"] = split_dev
+        _attach_inter_split(self, lay.n_rows)
         t = self._t
         delta = up(sch.row_delta)
         lib = load_library()
@@ -524,5 +572,7 @@ class DeviceGraph:
             seg_win=t["seg_win"].data_ptr(), seg_base=t["seg_base"].data_ptr(),
             cta_seg=t["cta_seg"].data_ptr(), seg_lpr=t["seg_lpr"].data_ptr(),
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
+            inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
+            inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
         )
         return self

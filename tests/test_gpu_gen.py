@@ -81,7 +81,8 @@ def _small_window_case():
     return c, budget, plan.window_nodes(plan.ROWS_CAP, budget)
 
 
-def test_multipass_generated_graph_vs_oracle():
+@pytest.mark.parametrize("blocks", ["0", "3"])
+def test_multipass_generated_graph_vs_oracle(blocks, monkeypatch):
     """Communities wider than the window, staged in passes (cdk_graph.intra_split):
     generator CSR bit-exact, RHS and 30 RK4 steps vs the oracle."""
     import torch
@@ -89,6 +90,7 @@ def test_multipass_generated_graph_vs_oracle():
     from paper_2203_16657_b200 import plan
     from paper_2203_16657_b200.engine import KuramotoEngine
 
+    monkeypatch.setenv("CDK_INTER_BLOCKS", blocks)
     c, budget, wn = _small_window_case()
     off, cdf, n_edges, thr = c.gen_inputs()
     npass = plan.community_passes(off, wn)
@@ -185,3 +187,37 @@ def test_full_size_row_regeneration():
     assert 0.8e10 < nnz_dir < 1.25e10, nnz_dir
     del csr
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "sweep2", "sweep4"])
+def test_inter_phase_modes_cfg1_golden(mode, monkeypatch, golden_dir):
+    """Every inter-entry path (inline in the row pipeline / separate phase per
+    segment / block-phased sweep, plan._seg_lanes and plan.inter_blocking)
+    reproduces the reference's config-1 trajectory."""
+    import os
+
+    import torch
+
+    from paper_2203_16657_b200 import configs
+    from paper_2203_16657_b200.engine import KuramotoEngine
+
+    if mode.startswith("sweep"):
+        monkeypatch.setenv("CDK_INTER_BLOCKS", mode[-1])
+    else:
+        monkeypatch.setenv("CDK_INTER_PHASE", mode)
+        monkeypatch.setenv("CDK_INTER_BLOCKS", "0")
+    c = configs.config1()
+    dec = c.decomposition()
+    omega, theta0 = c.state()
+    g = np.load(os.path.join(golden_dir, "cfg1.npz"))
+    eng = KuramotoEngine(dec, omega, coupling=c.coupling, norm=c.n)
+    if mode.startswith("sweep"):
+        assert eng.graph.inter_blocks == int(mode[-1])
+    else:
+        assert bool(eng.graph.schedule.seg_lpr[0] & 256) == (mode == "1")
+    k = eng.rhs(torch.from_numpy(theta0).cuda()).cpu().numpy()
+    assert np.abs(k - g["rhs0_cia"]).max() <= 1e-13
+    eng.set_state(theta0)
+    eng.rk4(c.dt, c.steps)
+    eng.check()
+    assert cia.circ_dist(eng.theta.cpu().numpy(), g["final_cia"]).max() <= 1e-9
