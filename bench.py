@@ -379,7 +379,7 @@ def run_ours(args):
     return 0
 
 
-def cpu_baseline_cfg5(case, csr, omega, theta0, rows: int = 20000):
+def cpu_baseline_cfg5(case, csr, dg, omega, theta0, rows: int = 20000):
     """Oracle C port on a bounded sample of config 5: one RHS with the full
     O(N) community terms and the directed corrections of the first ``rows``
     rows (as unordered pairs), extrapolated linearly in the pair count
@@ -390,13 +390,18 @@ def cpu_baseline_cfg5(case, csr, omega, theta0, rows: int = 20000):
     K.set_threads(1)
     off = case.offsets()
     iptr, xptr = csr.intra_ptr, csr.inter_ptr
-    icol = csr.intra_col[: int(iptr[rows])].cpu().numpy().view(np.uint16)
-    xcol = csr.inter_col[: int(xptr[rows])].cpu().numpy().astype(np.int64)
+    # device CSR: intra columns rebased to the segment windows (undo with the
+    # schedule's per-row delta) and bank-ordered within runs
+    icol = dg._t["intra_col"][: int(iptr[rows])].cpu().numpy().view(np.uint16)
+    xcol = dg._t["inter_col"][: int(xptr[rows])].cpu().numpy().astype(np.int64)
+    delta = dg.schedule.row_delta[:rows].astype(np.int64)
     ri = np.repeat(np.arange(rows), np.diff(iptr[: rows + 1]))
     keep = icol != 0xFFFF
     comm = np.searchsorted(off, np.arange(rows), side="right") - 1
     iu = np.concatenate([ri[keep], np.repeat(np.arange(rows), np.diff(xptr[: rows + 1]))])
-    iv = np.concatenate([icol[keep].astype(np.int64) + off[comm[ri[keep]]], xcol])
+    iv = np.concatenate([icol[keep].astype(np.int64) - delta[ri[keep]] + off[comm[ri[keep]]],
+                         xcol])
+    assert iv.min() >= 0 and iv.max() < case.n
     sg = np.concatenate([-np.ones(int(keep.sum())), np.ones(xcol.shape[0])])
     z = np.zeros(0, np.int64)
 
@@ -514,7 +519,7 @@ def run_cfg5(args):
         "clocks": clocks,
     }
     if not args.no_cpu_baseline:
-        rate, el, pairs, t_rhs = cpu_baseline_cfg5(case, csr, omega, theta0)
+        rate, el, pairs, t_rhs = cpu_baseline_cfg5(case, csr, dg, omega, theta0)
         res["cpu_baseline"] = {
             "value": rate, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"one RHS with the corrections of the first 20000 rows ({pairs} pairs, "

@@ -316,6 +316,11 @@ CDK_API int cdk_gen_inter_compact(int64_t n_rows, const int64_t *ptr_raw, const 
 /* add delta[row] to every non-padding intra column (segment-window rebasing) */
 CDK_API int cdk_gen_rebase(int64_t n_rows, const int64_t *ptr, const int32_t *delta,
                            uint16_t *col, void *stream);
+/* device twin of cdk_host_bank_order, out of place (src != dst): every row's
+ * intra run, or each pass sub-run when split != NULL, reordered for
+ * bank-conflict-free window gathers */
+CDK_API int cdk_bank_order(int64_t n_rows, const int64_t *ptr, const uint64_t *split,
+                           const uint16_t *src, uint16_t *dst, int pad_bank, void *stream);
 /* cdk_graph.inter_split of a row-sorted inter CSR (device arrays): block q
  * sub-run = columns in [q*block_nodes, (q+1)*block_nodes); rows longer than
  * 65535 entries are rejected */

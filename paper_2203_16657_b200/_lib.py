@@ -145,6 +145,7 @@ _SIGS = {
     "cdk_gen_inter_compact": [I64, P, P, P, P, P],
     "cdk_gen_rebase": [I64, P, P, P, P],
     "cdk_inter_split": [I64, P, P, ctypes.c_int, ctypes.c_int, P, P],
+    "cdk_bank_order": [I64, P, P, P, P, ctypes.c_int, P],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],

@@ -51,6 +51,49 @@ __device__ __forceinline__ T ldg(const T *p) { return __ldg(p); }
 
 __device__ __forceinline__ double2 ldcg2(const double2 *p) { return __ldcg(p); }
 
+// L2 eviction-priority hints: streamed-once data (CSR index runs, row
+// pointers, per-row scratch) is loaded evict-first so it does not push the
+// randomly gathered state out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *a, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+               : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_stream(const int64_t *a, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;"
+               : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t *a, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;"
+               : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_stream(const uint4 *a, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ldcg_stream(const double2 *a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stcg_stream(double2 *a, double2 v, uint64_t pol) {
+  asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
+               :: "l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 // --- warp reductions (xor butterfly: every lane ends with the same bits) ----
 __device__ __forceinline__ double warp_sum(double v, int width = 32) {
   for (int o = width >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);

@@ -385,3 +385,91 @@ extern "C" int cdk_inter_split(int64_t n_rows, const int64_t *ptr, const int32_t
   if (hbad) return set_error("inter_split: a row has more than 65535 inter entries"), CDK_INPUT;
   return CDK_OK;
 }
+
+namespace cdk {
+// Device twin of cdk_host_bank_order (csrc/host_plan.cpp), out of place: per
+// run (a row, or a pass sub-run of cdk_graph.intra_split) a stable counting
+// sort by bank group (column mod 8, pads -> pad_bank), then the sorted s-th
+// entry is dealt to phase j of round r in closed form (rounds 0..c-1 cover
+// all P = 8*nblk phases, later rounds only the full blocks' phases) and
+// written to position 64*(j/8) + 8*r + j%8 of the run.
+__global__ void bank_order_kernel(int64_t n_rows, const int64_t *ptr, const uint64_t *split,
+                                  const uint16_t *src, uint16_t *dst, int pad_bank) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows; i += warps) {
+    const int64_t a = ptr[i], e = ptr[i + 1];
+    const uint64_t sw = split ? split[i] : 0ull;
+    int64_t bnd[5];
+    int nr = 0;
+    bnd[nr++] = a;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int64_t o = (int64_t)((sw >> (16 * q)) & 0xFFFFu);
+      if (o) bnd[nr++] = a + 8 * o;
+    }
+    bnd[nr] = e;
+    for (int r = 0; r < nr; ++r) {
+      const int64_t rs = bnd[r], re = bnd[r + 1];
+      const int64_t L = re - rs;
+      if (L <= 8) {
+        for (int64_t q = rs + lane; q < re; q += 32) dst[q] = src[q];
+        continue;
+      }
+      int cnt[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) cnt[b] = 0;
+      for (int64_t q0 = rs; q0 < re; q0 += 32) {
+        const int64_t q = q0 + lane;
+        const uint16_t v = q < re ? src[q] : (uint16_t)0;
+        const int bank = q < re ? (v == (uint16_t)0xFFFF ? pad_bank : (v & 7)) : -1;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) cnt[b] += __popc(__ballot_sync(FULL, bank == b));
+      }
+      int base[8];
+      int acc = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        base[b] = acc;
+        acc += cnt[b];
+      }
+      const int64_t nblk = (L + 63) / 64, P = 8 * nblk, Pf = P - 8;
+      const int64_t c = (L % 64 == 0) ? 8 : (L % 64) / 8;
+      for (int64_t q0 = rs; q0 < re; q0 += 32) {
+        const int64_t q = q0 + lane;
+        const uint16_t v = q < re ? src[q] : (uint16_t)0;
+        const int bank = q < re ? (v == (uint16_t)0xFFFF ? pad_bank : (v & 7)) : -1;
+        int64_t sidx = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const unsigned m = __ballot_sync(FULL, bank == b);
+          if (bank == b) sidx = base[b] + __popc(m & lt);
+          base[b] += __popc(m);
+        }
+        if (q < re) {
+          int64_t rd, j;
+          if (sidx < c * P) {
+            rd = sidx / P;
+            j = sidx % P;
+          } else {
+            const int64_t s2 = sidx - c * P;
+            rd = c + s2 / Pf;
+            j = s2 % Pf;
+          }
+          dst[rs + 64 * (j >> 3) + 8 * rd + (j & 7)] = v;
+        }
+      }
+    }
+  }
+}
+}  // namespace cdk
+
+extern "C" int cdk_bank_order(int64_t n_rows, const int64_t *ptr, const uint64_t *split,
+                              const uint16_t *src, uint16_t *dst, int pad_bank, void *stream) {
+  if (n_rows < 0 || !ptr || !src || !dst || src == dst) return set_error("bank_order: bad args"), CDK_INPUT;
+  cdk::bank_order_kernel<<<cdk::gen_grid(n_rows, 8), 256, 0, as_stream(stream)>>>(
+      n_rows, ptr, split, src, dst, pad_bank & 7);
+  CDK_CHECK_LAUNCH("bank_order_kernel");
+  return CDK_OK;
+}

@@ -84,6 +84,9 @@ struct StageArgs {
   double *ksum;
   double *out;  // MODE 0
   double2 *xacc;  // block-phased inter sums (g.inter_blocks > 0)
+  int sweep_mode;  // inter sweep lanes/unroll variant (CDK_SWEEP, experiments)
+  int debug_flags; // CDK_DEBUG_FLAGS (timing experiments only; results invalid):
+                   // 1 = skip the inter sweep, 2 = skip the segments
   double k_over_n;
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
@@ -394,28 +397,34 @@ __device__ __forceinline__ void inter_phase(const StageArgs &a, const SegSmem &s
 // walk the blocks at about the same pace, so the random z gathers of the
 // whole GPU fall into one ~inter_block_nodes*16-byte slice of z that stays
 // L2-resident instead of thrashing HBM.
-template <int IU>
+template <int LPR, int IU, bool HINT = false>
 __device__ __forceinline__ void inter_sweep(const StageArgs &a) {
   const cdk_graph &g = a.g;
   const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
   if (segA == segB) return;
   const int64_t rA = g.rblk_row0[g.seg_rblk[segA]], rB = g.rblk_row0[g.seg_rblk[segB]];
+  constexpr int NG = NTHREADS / LPR;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int t = lane & 7, grp = tid >> 3;
-  const unsigned gmask = 0xFFu << (lane & 24);
+  const int t = lane & (LPR - 1), grp = tid / LPR;
+  const unsigned gmask = (LPR == 32) ? FULL : (((1u << LPR) - 1u) << (lane & ~(LPR - 1)));
   const double2 *__restrict__ z_in = a.z_in;
   const int nb = g.inter_blocks;
+  const uint64_t pol = l2_evict_first();
   for (int q = 0; q < nb; ++q) {
-    for (int64_t i = rA + grp; i < rB; i += NGROUPS) {
-      const int64_t xb = __ldg(g.inter_ptr + i), xe = __ldg(g.inter_ptr + i + 1);
-      const uint64_t sw = __ldg(g.inter_split + i);
+    for (int64_t i = rA + grp; i < rB; i += NG) {
+      const int64_t xb = HINT ? ld_stream(g.inter_ptr + i, pol) : __ldg(g.inter_ptr + i);
+      const int64_t xe = HINT ? ld_stream(g.inter_ptr + i + 1, pol) : __ldg(g.inter_ptr + i + 1);
+      const uint64_t sw = HINT ? ld_stream(g.inter_split + i, pol) : __ldg(g.inter_split + i);
       const int64_t s0 = xb + (q ? (int64_t)((sw >> (16 * (q - 1))) & 0xFFFFu) : 0);
       const int64_t s1 = (q + 1 < nb) ? xb + (int64_t)((sw >> (16 * q)) & 0xFFFFu) : xe;
       double sr = 0.0, si = 0.0;
-      for (int64_t p = s0 + t; p < s1; p += 8 * IU) {
+      for (int64_t p = s0 + t; p < s1; p += LPR * IU) {
         int j[IU];
 #pragma unroll
-        for (int k = 0; k < IU; ++k) j[k] = (p + 8 * k < s1) ? ldg(g.inter_col + p + 8 * k) : -1;
+        for (int k = 0; k < IU; ++k)
+          j[k] = (p + LPR * k < s1)
+                     ? (HINT ? ld_stream(g.inter_col + p + LPR * k, pol) : ldg(g.inter_col + p + LPR * k))
+                     : -1;
         double2 z[IU];
 #pragma unroll
         for (int k = 0; k < IU; ++k)
@@ -427,21 +436,123 @@ __device__ __forceinline__ void inter_sweep(const StageArgs &a) {
         }
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
+      for (int o = LPR / 2; o > 0; o >>= 1) {
         sr += __shfl_xor_sync(gmask, sr, o);
         si += __shfl_xor_sync(gmask, si, o);
       }
       if (t == 0) {
         if (q > 0) {
-          const double2 prev = ldcg2(a.xacc + i);
+          const double2 prev = HINT ? ldcg_stream(a.xacc + i, pol) : ldcg2(a.xacc + i);
+          sr = prev.x + sr;
+          si = prev.y + si;
+        }
+        if (HINT) stcg_stream(a.xacc + i, make_double2(sr, si), pol);
+        else __stcg(a.xacc + i, make_double2(sr, si));
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Software-pipelined variant: the next row's pointers, split word, first
+// index batch and previous-block sum are loaded while the current row's
+// gathers are in flight, so a group always has gathers or index loads
+// outstanding instead of serialising pointer -> index -> gather per row.
+template <int IU>
+__device__ __forceinline__ void inter_sweep_pipe(const StageArgs &a) {
+  constexpr int LPR = 8;
+  const cdk_graph &g = a.g;
+  const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
+  if (segA == segB) return;
+  const int64_t rA = g.rblk_row0[g.seg_rblk[segA]], rB = g.rblk_row0[g.seg_rblk[segB]];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int t = lane & (LPR - 1), grp = tid / LPR;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  const double2 *__restrict__ z_in = a.z_in;
+  const int32_t *__restrict__ xc = g.inter_col;
+  const int nb = g.inter_blocks;
+  auto span = [&](int64_t i, int q, int64_t &s0, int64_t &s1) {
+    const int64_t xb = __ldg(g.inter_ptr + i), xe = __ldg(g.inter_ptr + i + 1);
+    const uint64_t sw = __ldg(g.inter_split + i);
+    s0 = xb + (q ? (int64_t)((sw >> (16 * (q - 1))) & 0xFFFFu) : 0);
+    s1 = (q + 1 < nb) ? xb + (int64_t)((sw >> (16 * q)) & 0xFFFFu) : xe;
+  };
+  for (int q = 0; q < nb; ++q) {
+    int64_t i = rA + grp;
+    if (i >= rB) continue;
+    int64_t c0, c1;
+    span(i, q, c0, c1);
+    int jn[IU];
+#pragma unroll
+    for (int k = 0; k < IU; ++k) jn[k] = (c0 + t + LPR * k < c1) ? ldg(xc + c0 + t + LPR * k) : -1;
+    while (i < rB) {
+      const int64_t i2 = i + NGROUPS;
+      int64_t n0 = 0, n1 = 0;
+      if (i2 < rB) span(i2, q, n0, n1);  // next row's span: in flight with this row's gathers
+      double2 prev = make_double2(0.0, 0.0);
+      if (q > 0 && t == 0) prev = ldcg2(a.xacc + i);
+      double sr = 0.0, si = 0.0;
+      int j[IU];
+#pragma unroll
+      for (int k = 0; k < IU; ++k) j[k] = jn[k];
+      for (int64_t p = c0 + t;;) {
+        double2 z[IU];
+#pragma unroll
+        for (int k = 0; k < IU; ++k)
+          z[k] = (j[k] >= 0) ? ldz(z_in + j[k]) : make_double2(0.0, 0.0);
+        p += LPR * IU;
+        const bool more = p < c1;
+        if (more) {
+#pragma unroll
+          for (int k = 0; k < IU; ++k) j[k] = (p + LPR * k < c1) ? ldg(xc + p + LPR * k) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < IU; ++k) {
+          sr += z[k].x;
+          si += z[k].y;
+        }
+        if (!more) break;
+      }
+      // next row's first index batch (its span has landed by now)
+      if (i2 < rB) {
+#pragma unroll
+        for (int k = 0; k < IU; ++k) jn[k] = (n0 + t + LPR * k < n1) ? ldg(xc + n0 + t + LPR * k) : -1;
+      }
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(gmask, sr, o);
+        si += __shfl_xor_sync(gmask, si, o);
+      }
+      if (t == 0) {
+        if (q > 0) {
           sr = prev.x + sr;
           si = prev.y + si;
         }
         __stcg(a.xacc + i, make_double2(sr, si));
       }
+      i = i2;
+      c0 = n0;
+      c1 = n1;
     }
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void inter_sweep_dispatch(const StageArgs &a) {
+  switch (a.sweep_mode) {
+    case 1: inter_sweep<8, 8>(a); break;
+    case 2: inter_sweep<8, 16>(a); break;
+    case 3: inter_sweep<4, 16>(a); break;
+    case 4: inter_sweep<8, 4>(a); break;
+    case 5: inter_sweep<2, 16>(a); break;
+    case 6: inter_sweep<16, 8>(a); break;
+    case 7: inter_sweep_pipe<8>(a); break;
+    case 8: inter_sweep_pipe<4>(a); break;
+    case 9: inter_sweep_pipe<12>(a); break;
+    case 10: inter_sweep<8, 8, true>(a); break;
+    case 11: inter_sweep<8, 16, true>(a); break;
+    default: inter_sweep<4, 8>(a);  // measured best on config 5 (tools/sweep_modes.sh)
+  }
 }
 
 struct ProfAcc {
@@ -465,8 +576,8 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
   const int wn = g.smem_nodes;
   // mbarrier phases: bar_seg completes once per pass, bar_epi once per segment
   uint32_t pseg = (parity >> 1) & 1u, pepi = parity & 1u;
-  const bool swept = g.inter_blocks > 0;
-  if (swept) inter_sweep<8>(a);
+  const bool swept = g.inter_blocks > 0;  // inter sums precomputed (inter_sweep_kernel)
+  const int segEnd = (a.debug_flags & 2) ? segA : segB;
 #ifdef CDK_PROFILE
 #define PROF_MARK(acc)                           \
   do {                                           \
@@ -479,7 +590,7 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
   do {                 \
   } while (0)
 #endif
-  for (int s = segA; s < segB; ++s) {
+  for (int s = segA; s < segEnd; ++s) {
     const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
     const int64_t row0 = g.rblk_row0[rbA];
     const int64_t row1 = g.rblk_row0[rbB];
@@ -680,6 +791,15 @@ __device__ __forceinline__ void init_cta(const cdk_graph &g, const SegSmem &sm, 
   __syncthreads();
 }
 
+// Block-phased inter sweep as its own launch: it must run with (almost) no
+// shared memory — measured on B200, a 200+ KB shared-memory carve-out halves
+// the random-gather rate (124 vs 240 Ggathers/s, tools/sweep_bench.cu), the
+// L1 left for in-flight misses being too small.  Same CTA row ranges as the
+// stage kernel (cta_seg).
+__global__ void __launch_bounds__(NTHREADS, 1) inter_sweep_kernel(const StageArgs a) {
+  inter_sweep_dispatch(a);
+}
+
 // single stage launch (MODE 0: RHS, 1..4: RK4 stage, 5: Euler)
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
@@ -849,6 +969,10 @@ static int launch_stage(const StageArgs &a, cudaStream_t st) {
     set_error("community state does not fit the shared-memory opt-in limit");
     return CDK_INPUT;
   }
+  if (a.g.inter_blocks > 0 && !(a.debug_flags & 1)) {
+    inter_sweep_kernel<<<a.g.n_cta, a.g.cta_threads, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("inter_sweep_kernel");
+  }
   kuramoto_stage_kernel<MODE><<<a.g.n_cta, a.g.cta_threads, smem, st>>>(a);
   CDK_CHECK_LAUNCH("kuramoto_stage_kernel");
   return CDK_OK;
@@ -877,6 +1001,12 @@ static StageArgs base_args(const cdk_graph *g, const Workspace &w, double *theta
   a.omega = omega;
   a.ksum = w.ksum;
   a.xacc = w.xacc;
+  {
+    const char *e = getenv("CDK_SWEEP");
+    a.sweep_mode = e ? atoi(e) : 0;
+    const char *f = getenv("CDK_DEBUG_FLAGS");
+    a.debug_flags = f ? atoi(f) : 0;
+  }
   a.k_over_n = k_over_n;
   return a;
 }
@@ -969,7 +1099,26 @@ extern "C" int cdk_kuramoto_rk4(const cdk_graph *g, double *theta, const double 
   cudaStream_t st = as_stream(stream);
   Workspace w = carve(g, workspace, nullptr);
   StageArgs a = base_args(g, w, theta, omega, k_over_n);
-  if ((rc = launch_rk4_persistent(a, w, n_steps, dt, st))) return rc;
+  if (g->inter_blocks > 0) {
+    // large graphs: per-stage launches (sweep + stage); launch gaps are
+    // negligible against ~10 ms stages and the sweep needs its own smem config
+    for (int64_t s = 0; s < n_steps; ++s) {
+      a.step_rel = s;
+      a.z_in = w.z[0]; a.z_out = w.z[1]; a.part_in = w.part[0]; a.part_out = w.part[1];
+      a.h = dt / 2.0;
+      if ((rc = launch_stage<1>(a, st))) return rc;
+      a.z_in = w.z[1]; a.z_out = w.z[0]; a.part_in = w.part[1]; a.part_out = w.part[0];
+      if ((rc = launch_stage<2>(a, st))) return rc;
+      a.z_in = w.z[0]; a.z_out = w.z[1]; a.part_in = w.part[0]; a.part_out = w.part[1];
+      a.h = dt;
+      if ((rc = launch_stage<3>(a, st))) return rc;
+      a.z_in = w.z[1]; a.z_out = w.z[0]; a.part_in = w.part[1]; a.part_out = w.part[0];
+      a.h = dt / 6.0;
+      if ((rc = launch_stage<4>(a, st))) return rc;
+    }
+  } else if ((rc = launch_rk4_persistent(a, w, n_steps, dt, st))) {
+    return rc;
+  }
   advance_kernel<<<1, 1, 0, st>>>(w.status, n_steps);
   CDK_CHECK_LAUNCH("advance_kernel");
   return CDK_OK;

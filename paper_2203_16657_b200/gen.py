@@ -230,6 +230,7 @@ def device_graph(case: LfrCase, device=None, sm_count: int | None = None,
     dg = DeviceGraph.from_device_csr(csr.layout(), csr.intra_col, csr.inter_col,
                                      csr.intra_col.device, sm_count=sm_count,
                                      split_dev=csr.intra_split, smem_budget=budget)
+    csr.intra_col = None  # rebased + bank-ordered copy lives in dg (the original is freed)
     return dg, csr
 
 

@@ -519,7 +519,7 @@ class DeviceGraph:
     @classmethod
     def from_device_csr(cls, lay: "HostLayout", intra_col_dev, inter_col_dev, device,
                         sm_count: int | None = None, split_dev=None,
-                        smem_budget: int = SMEM_OPTIN - 2048):
+                        smem_budget: int = SMEM_OPTIN - 2048, bank_order: bool = True):
         """Graph whose columns were generated on the device (config 5): the
         schedule is planned from the host copies of the row pointers and the
         intra columns are rebased in place on the device."""
@@ -557,9 +557,18 @@ class DeviceGraph:
         t = self._t
         delta = up(sch.row_delta)
         lib = load_library()
+        stream = torch.cuda.current_stream().cuda_stream
         check(lib.cdk_gen_rebase(lay.n_rows, t["intra_ptr"].data_ptr(), delta.data_ptr(),
-                                 t["intra_col"].data_ptr(), torch.cuda.current_stream().cuda_stream),
-              "gen_rebase")
+                                 t["intra_col"].data_ptr(), stream), "gen_rebase")
+        del delta
+        if bank_order:  # device twin of the host path's _bank_order (out of place)
+            ordered = torch.empty_like(t["intra_col"])
+            ordered[-8:].fill_(-1)
+            check(lib.cdk_bank_order(lay.n_rows, t["intra_ptr"].data_ptr(),
+                                     t["intra_split"].data_ptr() if "intra_split" in t else None,
+                                     t["intra_col"].data_ptr(), ordered.data_ptr(),
+                                     int(sch.smem_nodes) & 7, stream), "bank_order")
+            t["intra_col"] = ordered
         self.struct = CdkGraph(
             n_rows=lay.n_rows, n_comm=lay.n_comm,
             comm_off=t["comm_off"].data_ptr(), intra_ptr=t["intra_ptr"].data_ptr(),

@@ -221,3 +221,22 @@ def test_inter_phase_modes_cfg1_golden(mode, monkeypatch, golden_dir):
     eng.rk4(c.dt, c.steps)
     eng.check()
     assert cia.circ_dist(eng.theta.cpu().numpy(), g["final_cia"]).max() <= 1e-9
+
+
+def test_device_bank_order_matches_host():
+    """cdk_bank_order (device, out of place) == cdk_host_bank_order on the same
+    rebased runs, including pass sub-runs (192-node window)."""
+    from paper_2203_16657_b200 import plan
+
+    c, budget, wn = _small_window_case()
+    csr = gen.generate(c, "cuda", pass_nodes=wn)
+    iptr, icol, _, _ = csr.to_host()
+    lay = csr.layout()
+    dg, _ = gen.device_graph(c, "cuda", smem_budget=budget)
+    delta = np.repeat(dg.schedule.row_delta.astype(np.int64), np.diff(iptr))
+    col = icol.copy()
+    m = col != 0xFFFF
+    col[m] = (col[m].astype(np.int64) + delta[m]).astype(np.uint16)
+    plan._bank_order(col, plan._sub_run_ptr(lay), dg.schedule.smem_nodes)
+    got = dg._t["intra_col"][: col.shape[0]].cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, col)
