@@ -140,9 +140,9 @@ typedef struct cdk_graph {
    * block 0, then block 1, ...), so the random z gathers of the whole GPU hit
    * one L2-resident block at a time; inter_split[row] packs the block
    * sub-run starts like intra_split (entries from the row start).  0 = off. */
-  int32_t inter_blocks;         /* 0 or 2..4 */
+  int32_t inter_blocks;         /* 0 (off) or 1..4 (1: no column split) */
   int32_t inter_block_nodes;
-  const uint64_t *inter_split;  /* [n_rows] or NULL (see cdk_inter_split) */
+  const uint64_t *inter_split;  /* [n_rows] (inter_blocks >= 2) or NULL (cdk_inter_split) */
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */
@@ -152,6 +152,9 @@ typedef struct cdk_run_status {
   int64_t steps_done;     /* steps advanced since the last prepare */
   int64_t reserved;
 } cdk_run_status;
+
+/* threads per CTA of the stage kernels (cdk_graph.cta_threads must match) */
+CDK_API int cdk_kuramoto_stage_threads(void);
 
 /* bytes of device workspace the fused Kuramoto path needs for graph g */
 CDK_API size_t cdk_kuramoto_workspace_bytes(const cdk_graph *g);

@@ -108,6 +108,7 @@ class CdkRunStatus(ctypes.Structure):
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
 _SIGS = {
+    "cdk_kuramoto_stage_threads": [],
     "cdk_order_params_blocks": [P, P, I64, I, D, D, P, P],
     "cdk_dense_complex": [P, P, I64, P, I, D, P, P, P],
     "cdk_dense_real": [P, P, I64, P, P, I, D, P, P],

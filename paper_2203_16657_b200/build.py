@@ -49,10 +49,14 @@ def _stale() -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False,
-                  debug: bool = False) -> str:
+                  debug: bool = False, defines: dict | None = None, tag: str = "") -> str:
+    """Build libcommdyn_cuda.so (or a variant: debug/profile builds, or
+    experiment builds with extra -D defines written to _<tag>.so)."""
     out = LIB if not debug else LIB.replace(".so", "_profile.so" if debug == "profile"
                                             else "_debug.so")
-    if not debug and not force and not _stale():
+    if tag:
+        out = out.replace(".so", f"_{tag}.so")
+    if not debug and not tag and not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     tmp = out + ".tmp"
@@ -63,6 +67,8 @@ def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: boo
         cmd.insert(1, "-DCDK_DEBUG")
     if ptxas_verbose:
         cmd.insert(1, "-Xptxas=-v")
+    for k, v in (defines or {}).items():
+        cmd.insert(1, f"-D{k}={v}")
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -75,5 +81,8 @@ def build_library(force: bool = False, verbose: bool = False, ptxas_verbose: boo
 
 
 if __name__ == "__main__":
+    defs = dict(a[2:].split("=", 1) for a in sys.argv[1:] if a.startswith("-D"))
+    tag = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--tag=")), "")
     print(build_library(force=True, verbose=True, ptxas_verbose="-v" in sys.argv,
-                        debug="profile" if "--profile" in sys.argv else ("--debug" in sys.argv)))
+                        debug="profile" if "--profile" in sys.argv else ("--debug" in sys.argv),
+                        defines=defs, tag=tag))

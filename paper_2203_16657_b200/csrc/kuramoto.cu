@@ -86,7 +86,8 @@ struct StageArgs {
   double2 *xacc;  // block-phased inter sums (g.inter_blocks > 0)
   int sweep_mode;  // inter sweep lanes/unroll variant (CDK_SWEEP, experiments)
   int debug_flags; // CDK_DEBUG_FLAGS (timing experiments only; results invalid):
-                   // 1 = skip the inter sweep, 2 = skip the segments
+                   // 1 = skip the inter sweep, 2 = skip the segments,
+                   // 4 = drop inline inter entries, 8 = drop intra gathers
   double k_over_n;
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
@@ -207,7 +208,10 @@ __device__ __forceinline__ void gather8_global(const uint4 w, const double2 *__r
 // Communities above the window capacity (and the NONE pool) gather intra
 // neighbours from global memory; everything else is identical.
 // ---------------------------------------------------------------------------
-constexpr int NTHREADS = 1024;
+#ifndef CDK_STAGE_THREADS
+#define CDK_STAGE_THREADS 1024
+#endif
+constexpr int NTHREADS = CDK_STAGE_THREADS;
 constexpr int NWARPS = NTHREADS / 32;
 constexpr int NGROUPS = NTHREADS / 8;
 
@@ -264,14 +268,17 @@ __device__ __forceinline__ double2 ldz(const double2 *p) { return __ldcg(p); }
 // so for LPR >= 8 one quarter-warp phase (8 lanes) covers one 64-entry block
 // and the host bank ordering (cdk_host_bank_order) is conflict-free; for
 // LPR = 4 a phase spans two rows (distinct within each row).
-template <int LPR>
+// MULTI: the segment is staged in window passes (sub-runs per row); INLINE:
+// inter entries ride in the row pipeline (else: separate phase / sweep).
+// Compile-time so the common single-pass inline path carries no extra state.
+template <int LPR, bool MULTI, bool INLINE>
 __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &sm, int nrows,
                                              int64_t row0, int64_t row0a, int64_t ebase,
                                              int64_t xbase, bool staged, uint32_t zs_addr,
                                              uint32_t zero_slot, const double2 *zglob,
                                              const uint4 *__restrict__ colv,
                                              const int32_t *__restrict__ xcol, int pass,
-                                             int npass, bool inter_inline) {
+                                             int npass) {
   constexpr int NG = NTHREADS / LPR;
   constexpr int STRIDE = 8 * LPR;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -285,14 +292,17 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
       const int64_t li = row0 + r - row0a;
       int e0 = (int)(sm.sip[li] - ebase);
       R.e1 = (int)(sm.sip[li + 1] - ebase);
-      if (npass > 1) {  // this pass's sub-run (cdk_graph.intra_split)
+      if (MULTI) {  // this pass's sub-run (cdk_graph.intra_split)
         const uint64_t sw = __ldg(a.g.intra_split + row0 + r);
         if (pass + 1 < npass) R.e1 = e0 + 8 * (int)((sw >> (16 * pass)) & 0xFFFFu);
         if (pass > 0) e0 += 8 * (int)((sw >> (16 * (pass - 1))) & 0xFFFFu);
       }
-      R.x0 = (int)(sm.sxp[li] - xbase);
-      // inter entries: in pass 0, unless the segment runs a separate inter phase
-      R.x1 = (pass == 0 && inter_inline) ? (int)(sm.sxp[li + 1] - xbase) : R.x0;
+      if (INLINE) {  // inter entries: in pass 0
+        R.x0 = (int)(sm.sxp[li] - xbase);
+        R.x1 = (!MULTI || pass == 0) ? (int)(sm.sxp[li + 1] - xbase) : R.x0;
+      } else {
+        R.x0 = R.x1 = 0;
+      }
       R.p = e0 + 8 * t;
       R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
     }
@@ -337,7 +347,7 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
       si += __shfl_xor_sync(gmask, si, o);
     }
     if (t == 0) {
-      if (pass == 0) {
+      if (!MULTI || pass == 0) {
         sm.acc[r] = make_double2(sr, si);
       } else {
         const double2 prev = sm.acc[r];
@@ -414,7 +424,8 @@ __device__ __forceinline__ void inter_sweep(const StageArgs &a) {
     for (int64_t i = rA + grp; i < rB; i += NG) {
       const int64_t xb = HINT ? ld_stream(g.inter_ptr + i, pol) : __ldg(g.inter_ptr + i);
       const int64_t xe = HINT ? ld_stream(g.inter_ptr + i + 1, pol) : __ldg(g.inter_ptr + i + 1);
-      const uint64_t sw = HINT ? ld_stream(g.inter_split + i, pol) : __ldg(g.inter_split + i);
+      const uint64_t sw =
+          nb > 1 ? (HINT ? ld_stream(g.inter_split + i, pol) : __ldg(g.inter_split + i)) : 0ull;
       const int64_t s0 = xb + (q ? (int64_t)((sw >> (16 * (q - 1))) & 0xFFFFu) : 0);
       const int64_t s1 = (q + 1 < nb) ? xb + (int64_t)((sw >> (16 * q)) & 0xFFFFu) : xe;
       double sr = 0.0, si = 0.0;
@@ -473,7 +484,7 @@ __device__ __forceinline__ void inter_sweep_pipe(const StageArgs &a) {
   const int nb = g.inter_blocks;
   auto span = [&](int64_t i, int q, int64_t &s0, int64_t &s1) {
     const int64_t xb = __ldg(g.inter_ptr + i), xe = __ldg(g.inter_ptr + i + 1);
-    const uint64_t sw = __ldg(g.inter_split + i);
+    const uint64_t sw = nb > 1 ? __ldg(g.inter_split + i) : 0ull;
     s0 = xb + (q ? (int64_t)((sw >> (16 * (q - 1))) & 0xFFFFu) : 0);
     s1 = (q + 1 < nb) ? xb + (int64_t)((sw >> (16 * q)) & 0xFFFFu) : xe;
   };
@@ -600,6 +611,9 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     const int npass = staged ? (int)((w1 - w0 + wn - 1) / wn) : 1;  // window passes (<= 4)
     const int nrows = (int)(row1 - row0);
     const int cA = g.rblk_comm[rbA];
+    const bool inter_inline0 = !swept && (g.seg_lpr[s] & CDK_SEG_INTER_PHASE) == 0;
+    const bool inter_inline = inter_inline0 && !(a.debug_flags & 4);
+    const bool inter_phased = !swept && !inter_inline0 && !(a.debug_flags & 4);
 
     // ---- 1. stage window, pointer slices, epilogue inputs (async) ----------
     if (tid == 0) {
@@ -666,8 +680,6 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col + ebase);
     const int32_t *__restrict__ xcol = g.inter_col + xbase;
     const int lpr = g.seg_lpr[s] & 0xFF;
-    const bool inter_inline = !swept && (g.seg_lpr[s] & CDK_SEG_INTER_PHASE) == 0;
-    const bool inter_phased = !swept && !inter_inline;
 
     // ---- 2. gather: lanes per row chosen per segment (4 / 8 / 16 / 32); a
     //         community wider than the window is gathered in passes, each
@@ -688,23 +700,26 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
       }
       const uint32_t zs_p = zs_addr - (uint32_t)pass * (uint32_t)wn * 16u;
       const uint32_t zero_p = zero_slot + (uint32_t)pass * (uint32_t)wn;
-      switch (lpr) {
-        case 32:
-          gather_phase<32>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                           colv, xcol, pass, npass, inter_inline);
-          break;
-        case 16:
-          gather_phase<16>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                           colv, xcol, pass, npass, inter_inline);
-          break;
-        case 4:
-          gather_phase<4>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                          colv, xcol, pass, npass, inter_inline);
-          break;
-        default:
-          gather_phase<8>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob,
-                          colv, xcol, pass, npass, inter_inline);
+#define CDK_GATHER(L, M, I)                                                                  \
+  gather_phase<L, M, I>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob, \
+                        colv, xcol, pass, npass)
+      const bool multi = npass > 1;
+      if (a.debug_flags & 8) {
+        for (int r = tid; r < nrows; r += NTHREADS) sm.acc[r] = make_double2(0.0, 0.0);
+      } else if (lpr == 4) {
+        if (multi) {
+          if (inter_inline) CDK_GATHER(4, true, true); else CDK_GATHER(4, true, false);
+        } else {
+          if (inter_inline) CDK_GATHER(4, false, true); else CDK_GATHER(4, false, false);
+        }
+      } else {
+        if (multi) {
+          if (inter_inline) CDK_GATHER(8, true, true); else CDK_GATHER(8, true, false);
+        } else {
+          if (inter_inline) CDK_GATHER(8, false, true); else CDK_GATHER(8, false, false);
+        }
       }
+#undef CDK_GATHER
     }
     __syncthreads();
     if (inter_phased) {
@@ -932,16 +947,16 @@ static int check_graph(const cdk_graph *g) {
     return CDK_INPUT;
   }
   if (g->cta_threads != NTHREADS) {
-    set_error("cdk_graph: cta_threads must be 1024");
+    set_error("cdk_graph: cta_threads must equal cdk_kuramoto_stage_threads()");
     return CDK_INPUT;
   }
   if (g->smem_nodes < 0 || (g->smem_nodes & 7) || g->seg_rows_cap <= 0) {
     set_error("cdk_graph: bad shared-memory capacities");
     return CDK_INPUT;
   }
-  if (g->inter_blocks != 0 &&
-      (g->inter_blocks < 2 || g->inter_blocks > 4 || !g->inter_split || g->inter_block_nodes <= 0)) {
-    set_error("cdk_graph: inter_blocks must be 0 or 2..4 with inter_split set");
+  if (g->inter_blocks < 0 || g->inter_blocks > 4 ||
+      (g->inter_blocks >= 2 && (!g->inter_split || g->inter_block_nodes <= 0))) {
+    set_error("cdk_graph: inter_blocks must be 0..4 (inter_split set when >= 2)");
     return CDK_INPUT;
   }
   return CDK_OK;
@@ -1226,3 +1241,5 @@ extern "C" int cdk_kuramoto_advance(const cdk_graph *g, void *workspace, int64_t
   CDK_CHECK_LAUNCH("advance_kernel");
   return CDK_OK;
 }
+
+extern "C" int cdk_kuramoto_stage_threads(void) { return cdk::NTHREADS; }

@@ -123,7 +123,14 @@ def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
 
 
 WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
-CTA_THREADS = 1024
+CTA_THREADS = 1024  # default; the library's value wins (stage_threads())
+
+
+def stage_threads() -> int:
+    """threads per CTA the stage kernels were built for (cdk_kuramoto_stage_threads)"""
+    from ._lib import load_library
+
+    return int(load_library().cdk_kuramoto_stage_threads())
 ROWS_CAP = 1536  # rows per segment (shared-memory row buffers; multiple of 8)
 SEG_MAX_COMM = 64  # communities per staged segment (csrc/kuramoto.cu SEG_MAX_COMM)
 MAX_PASS = 4  # window passes per community (cdk_graph.intra_split packs 3 sub-run starts)
@@ -335,7 +342,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         delta[rows[0]: rows[-1]] = cstart - seg_base[seg_of_row]
     seg_lpr = _seg_lanes(lay, rows[seg_rblk])
     if lay.intra_col is None:  # columns live on the device: caller rebases (cdk_gen_rebase)
-        sch = Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
+        sch = Schedule(n_cta, stage_threads(), int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
                        seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, None)
         sch.row_delta = delta.astype(np.int32)
         return sch
@@ -348,7 +355,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
             raise InputError("rebased intra column out of uint16 range")
         col[m] = newc.astype(np.uint16)
     _bank_order(col, _sub_run_ptr(lay), smem_nodes)
-    return Schedule(n_cta, CTA_THREADS, int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
+    return Schedule(n_cta, stage_threads(), int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
                     seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, col)
 
 
@@ -419,7 +426,7 @@ def inter_blocking(n_rows: int) -> tuple[int, int]:
         nb = int(min(4, max(2, np.ceil(n_rows * 16 / INTER_BLOCK_BYTES))))
     else:
         nb = 0
-    if nb <= 1 or n_rows < 16:
+    if nb <= 0 or n_rows < 16:
         return 0, 0
     nb = min(nb, 4)
     return nb, int((n_rows + nb - 1) // nb + 7) // 8 * 8
@@ -433,7 +440,7 @@ def _attach_inter_split(self, lay_n_rows: int) -> None:
 
     nb, bn = inter_blocking(lay_n_rows)
     self.inter_blocks, self.inter_block_nodes = nb, bn
-    if not nb:
+    if nb < 2:  # 0: off; 1: one block (separate inter launch, no split needed)
         return
     t = self._t
     t["inter_split"] = torch.zeros(lay_n_rows, dtype=torch.int64, device=self.device)

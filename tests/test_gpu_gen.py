@@ -189,7 +189,7 @@ def test_full_size_row_regeneration():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "sweep2", "sweep4"])
+@pytest.mark.parametrize("mode", ["0", "1", "sweep1", "sweep2", "sweep4"])
 def test_inter_phase_modes_cfg1_golden(mode, monkeypatch, golden_dir):
     """Every inter-entry path (inline in the row pipeline / separate phase per
     segment / block-phased sweep, plan._seg_lanes and plan.inter_blocking)

@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(1024, 1) smem_gather(const uint4 *idx, size_t 
 }
 
 int main() {
+  const bool only_gather = getenv("ONLY_GATHER") != nullptr;
   int dev = 0; CK(cudaSetDevice(dev));
   int sms = 0; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const size_t total = (size_t)1 << 30;  // 1 GiB stream
@@ -113,12 +114,12 @@ int main() {
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
     printf("TMA stream S=%d B=%6d: %.1f GB/s\n", S, B, 5.0 * per_cta * sms / (ms * 1e-3) / 1e9);
   };
-  for (int B : {4096, 8192, 16384, 32768}) {
+  if (!only_gather) for (int B : {4096, 8192, 16384, 32768}) {
     run_tma(tma_stream<2>, 2, B);
     run_tma(tma_stream<4>, 4, B);
     if (B <= 16384) run_tma(tma_stream<8>, 8, B);
   }
-  {
+  if (!only_gather) {
     const size_t n4 = per_cta / 16;
     ldg_stream<<<sms, 1024>>>((const int4 *)src, n4, sink);
     CK(cudaDeviceSynchronize());
@@ -128,9 +129,9 @@ int main() {
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
     printf("LDG stream 1024thr: %.1f GB/s\n", 5.0 * per_cta * sms / (ms * 1e-3) / 1e9);
   }
-  // C) gathers: 64 MB of indices (32M entries), window 6000 nodes
+  // C) gathers: 64 MB of indices (32M entries), window W nodes (WIN env, default 6000)
   {
-    const int W = 6000;
+    const int W = getenv("WIN") ? atoi(getenv("WIN")) : 6000;
     const size_t n_idx = (size_t)32 << 20;
     std::vector<uint16_t> h(n_idx);
     uint64_t x = 88172645463325252ull;
