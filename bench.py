@@ -218,7 +218,7 @@ def run_ours(args):
     import torch
 
     rank, world, local = _dist_env()
-    if world > 1:
+    if world > 1 or os.environ.get("CDK_BENCH_SHARDED") == "1":  # (1-rank: path check)
         from paper_2203_16657_b200 import multi
 
         return multi.bench_main(args)
@@ -425,8 +425,10 @@ def run_cfg5(args):
     import torch
 
     rank, world, local = _dist_env()
-    if world > 1:
-        raise SystemExit("--config cfg5 runs on one GPU (multi-GPU: see DESIGN.md §5)")
+    if world > 1 or os.environ.get("CDK_BENCH_SHARDED") == "1":
+        from paper_2203_16657_b200 import multi
+
+        return multi.bench_main(args)
     torch.cuda.set_device(local)
     from paper_2203_16657_b200 import _lib, gen
     from paper_2203_16657_b200.engine import KuramotoEngine
@@ -542,6 +544,9 @@ def main():
                          "config (steps default 200)")
     args = ap.parse_args()
     if args.config == "cfg5":
+        if args.impl != "reference" and (int(os.environ.get("WORLD_SIZE", "1")) > 1
+                                         or os.environ.get("CDK_BENCH_SHARDED") == "1"):
+            return run_ours(args)
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "cfg5 reference arm not run: "
                               "~4 CPU-minutes per RHS; see cpu_baseline of the cfg5 line"}))

@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 8
+#define CDK_ABI_VERSION 9
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -297,6 +297,8 @@ typedef struct cdk_gen_params {
   uint32_t miss_thr;         /* intra pair missing iff hash < miss_thr (q * 2^32) */
   uint32_t pass_nodes;       /* window capacity of the stage kernel (cdk_graph.smem_nodes):
                                 rows of communities wider than it get per-pass sub-runs */
+  int64_t row_lo, row_hi;    /* rows generated: [row_lo, row_hi) (a rank's shard; other
+                                rows stay empty, columns stay global) */
 } cdk_gen_params;
 
 /* intra: per-row padded run lengths (int64[n_rows], sub-runs per pass each

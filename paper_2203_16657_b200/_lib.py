@@ -98,6 +98,8 @@ class CdkGenParams(ctypes.Structure):
         ("n_inter_edges", I64),
         ("miss_thr", ctypes.c_uint32),
         ("pass_nodes", ctypes.c_uint32),
+        ("row_lo", I64),
+        ("row_hi", I64),
     ]
 
 
@@ -163,7 +165,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 _lock = threading.Lock()
 _lib = None

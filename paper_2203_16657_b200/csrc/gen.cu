@@ -92,7 +92,9 @@ __global__ void gen_intra_count_kernel(cdk_gen_params p, int64_t *padded, int64_
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_in = p.comm_off[p.n_comm];
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_in; i += warps) {
+  const int64_t i_lo = p.row_lo, i_hi = min(p.row_hi, n_in);
+  for (int64_t i = i_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < i_hi;
+       i += warps) {
     const int c = find_comm64(p.comm_off, p.n_comm, i);
     const PassGeom G = pass_geom(p, c);
     const uint32_t a = (uint32_t)(i - G.c0);
@@ -124,7 +126,9 @@ __global__ void gen_intra_fill_kernel(cdk_gen_params p, const int64_t *ptr, cons
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_in = p.comm_off[p.n_comm];
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_in; i += warps) {
+  const int64_t i_lo = p.row_lo, i_hi = min(p.row_hi, n_in);
+  for (int64_t i = i_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < i_hi;
+       i += warps) {
     const int c = find_comm64(p.comm_off, p.n_comm, i);
     const PassGeom G = pass_geom(p, c);
     const uint32_t a = (uint32_t)(i - G.c0);
@@ -168,8 +172,8 @@ __global__ void gen_inter_count_kernel(cdk_gen_params p, unsigned long long *cnt
     int cu, cv;
     const int64_t u = edge_end(p, e, 0, &cu), v = edge_end(p, e, 1, &cv);
     if (cu == cv) continue;
-    atomicAdd(cnt + u, 1ull);
-    atomicAdd(cnt + v, 1ull);
+    if (u >= p.row_lo && u < p.row_hi) atomicAdd(cnt + u, 1ull);
+    if (v >= p.row_lo && v < p.row_hi) atomicAdd(cnt + v, 1ull);
   }
 }
 
@@ -179,8 +183,8 @@ __global__ void gen_inter_fill_kernel(cdk_gen_params p, unsigned long long *curs
     int cu, cv;
     const int64_t u = edge_end(p, e, 0, &cu), v = edge_end(p, e, 1, &cv);
     if (cu == cv) continue;
-    col[atomicAdd(cursor + u, 1ull)] = (int32_t)v;
-    col[atomicAdd(cursor + v, 1ull)] = (int32_t)u;
+    if (u >= p.row_lo && u < p.row_hi) col[atomicAdd(cursor + u, 1ull)] = (int32_t)v;
+    if (v >= p.row_lo && v < p.row_hi) col[atomicAdd(cursor + v, 1ull)] = (int32_t)u;
   }
 }
 
@@ -262,7 +266,9 @@ using namespace cdk;
 
 extern "C" int cdk_gen_intra_count(const cdk_gen_params *p, int64_t *padded, int64_t *raw,
                                    uint64_t *split, void *stream) {
-  if (!p || p->n_comm < 0 || !padded) return set_error("gen: bad params"), CDK_INPUT;
+  if (!p || p->n_comm < 0 || !padded || p->row_lo < 0 || p->row_hi > p->n_rows ||
+      p->row_lo > p->row_hi)
+    return set_error("gen: bad params"), CDK_INPUT;
   gen_intra_count_kernel<<<gen_grid(p->n_rows, 8), 256, 0, as_stream(stream)>>>(*p, padded, raw,
                                                                                  split);
   CDK_CHECK_LAUNCH("gen_intra_count_kernel");

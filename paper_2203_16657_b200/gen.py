@@ -98,6 +98,14 @@ class LfrCase:
         thr = int(min(round((1.0 - self.p_in) * 2.0 ** 32), 2 ** 32 - 1))
         return off, cdf, n_edges, thr
 
+    def row_costs(self) -> np.ndarray:
+        """Expected per-row cost in the planner's model (padded missing-intra
+        entries + INTER_COST x expected inter degree + ROW_COST), for sharding."""
+        off = self.offsets()
+        lam = np.diff(off).astype(np.float64)
+        intra = np.repeat(np.ceil((1.0 - self.p_in) * (lam - 1.0) / 8.0) * 8.0, np.diff(off))
+        return intra + INTER_COST * self.propensities(off) + ROW_COST
+
     def state(self):
         """(omega, theta0): omega ~ Cauchy(0, 0.5), theta0 ~ U[0, 2 pi) (BASELINE configs[4])."""
         rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(self.state_seed)))
@@ -132,11 +140,13 @@ class GeneratedCsr:
     nnz_intra: int
     intra_split: object = None  # device int64 (uint64 bits) or None
     pass_nodes: int = 0
+    row_range: tuple | None = None
 
     def layout(self) -> HostLayout:
         n = self.n_rows
         off = self.comm_off
-        rblk_row0, rblk_comm, comm_rblk_off = _rblocks(off, n, self.intra_ptr, self.inter_ptr)
+        rblk_row0, rblk_comm, comm_rblk_off = _rblocks(off, n, self.intra_ptr, self.inter_ptr,
+                                                       self.row_range)
         padded = np.diff(self.intra_ptr)
         xcounts = np.diff(self.inter_ptr)
         row_cost = padded.astype(np.float64) + INTER_COST * xcounts + ROW_COST
@@ -158,13 +168,18 @@ class GeneratedCsr:
                 self.inter_ptr, self.inter_col[:nx].cpu().numpy())
 
 
-def generate(case: LfrCase, device=None, stream=None, pass_nodes: int | None = None) -> GeneratedCsr:
+def generate(case: LfrCase, device=None, stream=None, pass_nodes: int | None = None,
+             row_range=None) -> GeneratedCsr:
     """Run the device generator for ``case``; returns the CSR on ``device``.
     Rows of communities wider than ``pass_nodes`` (default: the stage
-    kernel's window) get one sub-run per window pass (cdk_graph.intra_split)."""
+    kernel's window) get one sub-run per window pass (cdk_graph.intra_split).
+    ``row_range=(lo, hi)``: generate only those rows (a rank's shard, cut at
+    community boundaries); other rows are empty, columns stay global, and the
+    shard's rows are identical to the same rows of the full graph."""
     import torch
 
     pass_nodes = window_nodes() if pass_nodes is None else int(pass_nodes)
+    lo, hi = (0, case.n) if row_range is None else (int(row_range[0]), int(row_range[1]))
     dev = torch.device(device if device is not None else "cuda")
     lib = _lib.lib()
     off, cdf, n_edges, thr = case.gen_inputs()
@@ -173,7 +188,8 @@ def generate(case: LfrCase, device=None, stream=None, pass_nodes: int | None = N
     d_cdf = torch.from_numpy(cdf).to(dev)
     p = _lib.CdkGenParams(seed=int(case.graph_seed), n_rows=n, n_comm=m,
                           comm_off=d_off.data_ptr(), node_cdf=d_cdf.data_ptr(),
-                          n_inter_edges=n_edges, miss_thr=thr, pass_nodes=pass_nodes)
+                          n_inter_edges=n_edges, miss_thr=thr, pass_nodes=pass_nodes,
+                          row_lo=lo, row_hi=hi)
     pp = ctypes.byref(p)
     sp = _lib.stream_ptr(stream)
 
@@ -215,21 +231,22 @@ def generate(case: LfrCase, device=None, stream=None, pass_nodes: int | None = N
                                          xcol.data_ptr(), sp), "gen_inter_compact")
     del raw
     return GeneratedCsr(n, m, off, iptr.cpu().numpy(), xptr.cpu().numpy(), icol, xcol, n_edges,
-                        nnz_intra, split, pass_nodes)
+                        nnz_intra, split, pass_nodes, None if row_range is None else (lo, hi))
 
 
 def device_graph(case: LfrCase, device=None, sm_count: int | None = None,
-                 smem_budget: int | None = None):
+                 smem_budget: int | None = None, row_range=None):
     """(DeviceGraph, GeneratedCsr) for ``case``: generate, plan, rebase in place.
     ``smem_budget`` shrinks the stage kernel's window (tests: multi-pass paths
-    at small sizes)."""
+    at small sizes); ``row_range`` generates one rank's shard."""
     from .plan import ROWS_CAP, SMEM_OPTIN, DeviceGraph
 
     budget = SMEM_OPTIN - 2048 if smem_budget is None else int(smem_budget)
-    csr = generate(case, device, pass_nodes=window_nodes(ROWS_CAP, budget))
+    csr = generate(case, device, pass_nodes=window_nodes(ROWS_CAP, budget), row_range=row_range)
     dg = DeviceGraph.from_device_csr(csr.layout(), csr.intra_col, csr.inter_col,
                                      csr.intra_col.device, sm_count=sm_count,
-                                     split_dev=csr.intra_split, smem_budget=budget)
+                                     split_dev=csr.intra_split, smem_budget=budget,
+                                     row_range=row_range)
     csr.intra_col = None  # rebased + bank-ordered copy lives in dg (the original is freed)
     return dg, csr
 

@@ -45,13 +45,18 @@ def row_costs(dec: Decomposition) -> np.ndarray:
 def partition_rows(dec: Decomposition, world: int) -> list[tuple[int, int]]:
     """Contiguous row ranges, one per rank, cut at community starts (or in the
     NONE pool at 32-row granularity), balanced on cumulative cost."""
+    return partition_by_cost(dec.offsets, dec.n_nodes, row_costs(dec), world)
+
+
+def partition_by_cost(off, n: int, cost, world: int) -> list[tuple[int, int]]:
+    """partition_rows on explicit community offsets and per-row costs (also
+    used for device-generated graphs, whose rows never exist on the host)."""
     if world < 1:
         raise InputError("world must be >= 1")
-    n = dec.n_nodes
-    off = dec.offsets
+    off = np.asarray(off, dtype=np.int64)
     cand = list(off[:-1].tolist()) + list(range(int(off[-1]), n, POOL_GRAIN)) + [n]
     cand = np.unique(np.asarray(cand, dtype=np.int64))
-    cum = np.concatenate([[0.0], np.cumsum(row_costs(dec))])
+    cum = np.concatenate([[0.0], np.cumsum(np.asarray(cost, dtype=np.float64))])
     total = cum[-1]
     cuts = [0]
     for r in range(1, world):
@@ -92,14 +97,26 @@ def workspace_views(engine: KuramotoEngine):
 class ShardedKuramotoEngine:
     """One rank of a community-sharded Kuramoto CIA trajectory (NCCL exchange)."""
 
-    def __init__(self, dec: Decomposition, omega, coupling: float, norm: float | None, rank: int,
-                 world: int, group=None, device=None, ranges=None):
+    def __init__(self, dec: Decomposition | None, omega, coupling: float, norm: float | None,
+                 rank: int, world: int, group=None, device=None, ranges=None, graph=None):
         self.rank, self.world, self.group = rank, world, group
         self.ranges = ranges if ranges is not None else partition_rows(dec, world)
         lo, hi = self.ranges[rank]
-        self.graph = DeviceGraph(dec, device=device, row_range=(lo, hi))
+        self.graph = graph if graph is not None else DeviceGraph(dec, device=device,
+                                                                 row_range=(lo, hi))
         self.eng = KuramotoEngine(dec, omega, coupling=coupling, norm=norm, graph=self.graph)
         self.z = workspace_views(self.eng)
+
+    @classmethod
+    def generated(cls, case, rank: int, world: int, group=None, device=None):
+        """One rank of a device-generated graph (config 5): the rank generates
+        only its own rows (gen.generate(row_range=...))."""
+        from . import gen
+
+        ranges = partition_by_cost(case.offsets(), case.n, case.row_costs(), world)
+        dg, _ = gen.device_graph(case, device, row_range=ranges[rank])
+        omega, _ = case.state()
+        return cls(None, omega, case.coupling, case.n, rank, world, group, device, ranges, dg)
 
     def _exchange(self, k: int, stream=None) -> None:
         exchange_slices(self.z[k], self.ranges, self.rank, self.group)
@@ -132,14 +149,26 @@ class VirtualCluster:
     Exercises exactly the per-rank layouts/schedules/kernels of the multi-GPU
     path (for bitwise-equality tests without several GPUs)."""
 
-    def __init__(self, dec: Decomposition, omega, coupling: float, norm: float | None,
-                 world: int, device=None):
-        self.ranges = partition_rows(dec, world)
+    def __init__(self, dec: Decomposition | None, omega, coupling: float, norm: float | None,
+                 world: int, device=None, graphs=None, ranges=None):
+        self.ranges = ranges if ranges is not None else partition_rows(dec, world)
         self.ranks = []
         for r in range(world):
-            g = DeviceGraph(dec, device=device, row_range=self.ranges[r])
+            g = (graphs[r] if graphs is not None
+                 else DeviceGraph(dec, device=device, row_range=self.ranges[r]))
             e = KuramotoEngine(dec, omega, coupling=coupling, norm=norm, graph=g)
             self.ranks.append((e, workspace_views(e)))
+
+    @classmethod
+    def generated(cls, case, world: int, device=None, smem_budget=None):
+        """Every rank of a sharded device-generated graph on one device."""
+        from . import gen
+
+        ranges = partition_by_cost(case.offsets(), case.n, case.row_costs(), world)
+        graphs = [gen.device_graph(case, device, smem_budget=smem_budget, row_range=rr)[0]
+                  for rr in ranges]
+        omega, _ = case.state()
+        return cls(None, omega, case.coupling, case.n, world, device, graphs, ranges)
 
     def _exchange(self, k: int) -> None:
         for r, (lo, hi) in enumerate(self.ranges):
@@ -176,28 +205,50 @@ class VirtualCluster:
 
 
 def bench_main(args):
-    """bench.py --gpus N under torchrun: config 2 sharded over N ranks."""
+    """bench.py --gpus N under torchrun: config 2 (default) or config 5
+    (--config cfg5, each rank generating its own rows) sharded by community
+    over N ranks; timed on the device, max over ranks."""
     import json
     import os
+    import sys
     import time
 
     import torch
     import torch.distributed as dist
 
-    from . import configs
+    from . import configs, gen
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    case = configs.config2()
-    dec = case.decomposition()
-    omega, theta0 = case.state()
-    eng = ShardedKuramotoEngine(dec, omega, case.coupling, case.n, rank, world)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import METRIC, UNIT, ClockSampler, _peaks, algorithmic_bytes_per_rhs  # noqa: E402
+
+    cfg = getattr(args, "config", "cfg2")
+    if cfg == "cfg5":
+        case = gen.config5()
+        omega, theta0 = case.state()
+        eng = ShardedKuramotoEngine.generated(case, rank, world)
+        nnz_local = eng.graph.layout.nnz_dir
+        workload = ("cfg5 Kuramoto CIA RK4, LFR-style N=8000000 (device-generated, each rank its "
+                    "own rows), sharded by community")
+        flush = None
+    else:
+        case = configs.config2()
+        dec = case.decomposition()
+        omega, theta0 = case.state()
+        eng = ShardedKuramotoEngine(dec, omega, case.coupling, case.n, rank, world)
+        nnz_local = eng.graph.layout.nnz_dir
+        workload = "cfg2 Kuramoto CIA RK4, SBM N=200000, sharded by community"
+        flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    lib = eng.eng.lib
+    nnz_t = torch.tensor([nnz_local], dtype=torch.int64, device="cuda")
+    dist.all_reduce(nnz_t)
+    nnz = int(nnz_t.item())
     eng.set_state(theta0)
     W, K = max(3, args.warmup), args.steps
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     for _ in range(W):
         eng.rk4(case.dt, 1)
     eng.set_state(theta0)
@@ -205,31 +256,57 @@ def bench_main(args):
     dist.barrier()
     cur = torch.cuda.current_stream()
     tot = 0.0
-    for _ in range(K):
-        flush.fill_(1.0)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(cur)
-        eng.rk4(case.dt, 1)
-        b.record(cur)
-        b.synchronize()
-        tot += a.elapsed_time(b)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+    sampler = ClockSampler(local)
+    l0 = int(lib.cdk_launch_count())
+    with sampler:
+        for _ in range(K):
+            if flush is not None:
+                flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cur)
+            eng.rk4(case.dt, 1)
+            b.record(cur)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        torch.cuda.synchronize()
+        dist.barrier()
+        launches = int(lib.cdk_launch_count()) - l0
+        # e2e: host theta0 in, K steps, full theta back on rank 0
+        th_h = torch.from_numpy(theta0).pin_memory()
+        dist.barrier()
+        t0 = time.perf_counter()
+        eng.set_state(th_h)
+        eng.rk4(case.dt, K)
+        final = eng.gather_theta().cpu()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+    t = torch.tensor([tot, e2e_s * 1e3], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     eng.check()
-    ms = float(t.item())
+    ms, e2e_ms = float(t[0].item()), float(t[1].item())
     if rank == 0:
+        peak, peak_kind = _peaks()
+        b_rhs = algorithmic_bytes_per_rhs(case.n, nnz)
+        stage_ms = ms / K / 4.0
         print(json.dumps({
-            "metric": "node-updates/sec (CIA Kuramoto RK4 RHS)", "value": case.n * K / (ms / 1e3),
-            "unit": "node-updates/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2 Kuramoto CIA RK4 sharded by community",
-                       "n_nodes": case.n, "parallelism": f"community shards x{world}",
-                       "l2": "flushed before every timed step",
-                       "ranges": eng.ranges},
-            "gpu_launches": 9 * K,
+            "metric": METRIC, "value": case.n * K / (ms / 1e3), "unit": UNIT,
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "n_nodes": case.n, "nnz_dir": nnz,
+                       "parallelism": f"community shards x{world} (NCCL all-gather of z per stage)",
+                       "l2": "flushed before every timed step" if flush is not None
+                       else "inputs >> L2", "ranges": eng.ranges},
+            "roofline": {"bound": "hbm", "achieved": b_rhs / world / (stage_ms / 1e3) / 1e9,
+                         "peak": peak, "unit": "GB/s", "peak_kind": peak_kind,
+                         "frac": b_rhs / world / (stage_ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "note": "per GPU: canonical bytes / world over the whole stage "
+                                 "(kernels + exchange)"},
+            "e2e": {"value": case.n * K / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(8 * case.n / K),
+                    "d2h_bytes_per_step": int(8 * case.n / K)},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
         }), flush=True)
     dist.destroy_process_group()
     time.sleep(0.1)

@@ -298,7 +298,8 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         npass_c = np.where(npass_c == 1, 1, 0)
     stageable = npass_c >= 1
     multi = npass_c > 1
-    seg_rblk, seg_win, seg_base, cta_seg = [0], [], [], [0]
+    mode_c, mode_pool = _comm_modes(lay)
+    seg_rblk, seg_win, seg_base, cta_seg, seg_lpr = [0], [], [], [0], []
     for b in range(n_cta):
         rb, rb_end = int(cta_bounds[b]), int(cta_bounds[b + 1])
         while rb < rb_end:
@@ -314,11 +315,12 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
                 else:  # unstaged: global gathers
                     seg_win.append((0, 0))
                     seg_base.append(int(off[c]) if c >= 0 else 0)
+                seg_lpr.append(int(mode_c[c]) if c >= 0 else mode_pool)
             else:  # staged window over whole communities, 128-byte aligned
                 w0 = int(win_lo[c])
                 while rb < rb_end:
                     cc = int(lay.rblk_comm[rb])
-                    if cc < 0 or not stageable[cc] or multi[cc]:
+                    if cc < 0 or not stageable[cc] or multi[cc] or mode_c[cc] != mode_c[c]:
                         break
                     if (int(win_hi[cc]) - w0 > smem_nodes or rows[rb + 1] - rows[start] > rows_cap
                             or cc - c >= SEG_MAX_COMM):
@@ -326,9 +328,11 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
                     rb += 1
                 seg_win.append((w0, int(win_hi[int(lay.rblk_comm[rb - 1])])))
                 seg_base.append(w0)
+                seg_lpr.append(int(mode_c[c]))
             seg_rblk.append(rb)
         cta_seg.append(len(seg_rblk) - 1)
     seg_rblk = np.asarray(seg_rblk, dtype=np.int32)
+    seg_lpr = np.asarray(seg_lpr, dtype=np.int32)
     seg_win = np.asarray(seg_win, dtype=np.int64).reshape(-1, 2)
     seg_base = np.asarray(seg_base, dtype=np.int64)
 
@@ -340,7 +344,6 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
         cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
         delta[rows[0]: rows[-1]] = cstart - seg_base[seg_of_row]
-    seg_lpr = _seg_lanes(lay, rows[seg_rblk])
     if lay.intra_col is None:  # columns live on the device: caller rebases (cdk_gen_rebase)
         sch = Schedule(n_cta, stage_threads(), int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
                        seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, None)
@@ -363,22 +366,28 @@ SEG_INTER_PHASE = 256  # include/commdyn_cuda.h CDK_SEG_INTER_PHASE
 INTER_PHASE_MIN = 16.0  # mean inter entries per row above which a segment runs the inter phase
 
 
-def _seg_lanes(lay: HostLayout, seg_rows: np.ndarray) -> np.ndarray:
-    """per-segment gather mode: lanes per row (rows in flight matter more than
-    lanes per row — measured: 16/32 lanes per row double the gather time;
-    short rows use 4) | SEG_INTER_PHASE for inter-heavy rows.  CDK_LPR and
+def _comm_modes(lay: HostLayout):
+    """Gather mode per community (and for the NONE pool): lanes per row (rows
+    in flight matter more than lanes per row — measured: 16/32 lanes per row
+    double the gather time; short rows use 4) | SEG_INTER_PHASE for
+    inter-heavy rows.  Decided per community from its own rows, so every
+    shard of a multi-GPU run picks the same mode for the same rows (bitwise
+    equal trajectories); segments never mix modes.  CDK_LPR and
     CDK_INTER_PHASE (0/1) override for experiments."""
     import os
 
-    nr = np.maximum(np.diff(seg_rows), 1)
-    lens = (lay.intra_ptr[seg_rows[1:]] - lay.intra_ptr[seg_rows[:-1]]) / nr
-    xl = (lay.inter_ptr[seg_rows[1:]] - lay.inter_ptr[seg_rows[:-1]]) / nr
+    off = lay.comm_off
+    lam = np.maximum(np.diff(off), 1)
+    lens = (lay.intra_ptr[off[1:]] - lay.intra_ptr[off[:-1]]) / lam
+    xl = (lay.inter_ptr[off[1:]] - lay.inter_ptr[off[:-1]]) / lam
     forced = os.environ.get("CDK_LPR")
     lpr = (np.full(lens.shape[0], int(forced), dtype=np.int32) if forced
            else np.where(lens > 24, 8, 4).astype(np.int32))
     fx = os.environ.get("CDK_INTER_PHASE")
     sep = (np.full(lens.shape[0], fx == "1") if fx in ("0", "1") else xl > INTER_PHASE_MIN)
-    return (lpr | np.where(sep, SEG_INTER_PHASE, 0)).astype(np.int32)
+    mode = (lpr | np.where(sep, SEG_INTER_PHASE, 0)).astype(np.int32)
+    pool = (int(forced) if forced else 4) | (SEG_INTER_PHASE if fx == "1" else 0)
+    return mode, int(pool)
 
 
 def _sub_run_ptr(lay: HostLayout) -> np.ndarray:
@@ -526,7 +535,8 @@ class DeviceGraph:
     @classmethod
     def from_device_csr(cls, lay: "HostLayout", intra_col_dev, inter_col_dev, device,
                         sm_count: int | None = None, split_dev=None,
-                        smem_budget: int = SMEM_OPTIN - 2048, bank_order: bool = True):
+                        smem_budget: int = SMEM_OPTIN - 2048, bank_order: bool = True,
+                        row_range=None):
         """Graph whose columns were generated on the device (config 5): the
         schedule is planned from the host copies of the row pointers and the
         intra columns are rebased in place on the device."""
@@ -541,7 +551,7 @@ class DeviceGraph:
         sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget)
         self.layout, self.schedule = lay, sch
         self.n_rows, self.n_comm, self.device = lay.n_rows, lay.n_comm, dev
-        self.row_range = (0, lay.n_rows)
+        self.row_range = (0, lay.n_rows) if row_range is None else tuple(int(x) for x in row_range)
 
         def up(a):
             return torch.from_numpy(np.ascontiguousarray(a)).to(dev)

@@ -53,3 +53,31 @@ def test_virtual_cluster_with_pool_and_tiny_communities():
     vc.set_state(theta)
     vc.rk4(0.01, 10)
     assert np.array_equal(vc.theta().cpu().numpy(), single.theta.cpu().numpy())
+
+
+@pytest.mark.parametrize("world,blocks", [(2, "0"), (3, "3")])
+def test_virtual_cluster_generated_graph_bitwise(world, blocks, monkeypatch):
+    """Config-5 family, every rank generating only its own rows (gen.generate
+    row_range) with multi-pass windows and (blocks=3) the block-phased inter
+    sweep: bitwise equal to the single-rank trajectory."""
+    from paper_2203_16657_b200 import gen, plan
+    from paper_2203_16657_b200.engine import KuramotoEngine
+    from paper_2203_16657_b200.multi import VirtualCluster
+
+    monkeypatch.setenv("CDK_INTER_BLOCKS", blocks)
+    c = gen.scaled_config5(n=5000, lo=100, hi=1400, seed=58)
+    budget = plan.stage_smem_bytes(192) - 128
+    omega, theta0 = c.state()
+    omega = np.clip(omega, -20, 20)
+    dg, _ = gen.device_graph(c, "cuda", smem_budget=budget)
+    single = KuramotoEngine(None, omega, coupling=c.coupling, norm=c.n, graph=dg)
+    single.set_state(theta0)
+    single.rk4(c.dt, 12)
+    vc = VirtualCluster.generated(c, world, "cuda", smem_budget=budget)
+    for e, _ in vc.ranks:
+        e.omega.copy_(single.omega)
+    vc.set_state(theta0)
+    vc.rk4(c.dt, 12)
+    vc.check()
+    assert len({tuple(r) for r in vc.ranges}) == world
+    assert np.array_equal(vc.theta().cpu().numpy(), single.theta.cpu().numpy())

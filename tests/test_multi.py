@@ -143,3 +143,20 @@ def test_gloo_two_ranks_exchange_and_sharded_rk4():
     for rank, ok1, err in res:
         assert ok1, f"rank {rank}: uneven all-gather wrong"
         assert err <= 1e-13, f"rank {rank}: sharded trajectory differs by {err}"
+
+
+def test_partition_by_cost_generated_case():
+    from paper_2203_16657_b200 import gen
+    from paper_2203_16657_b200.multi import partition_by_cost
+
+    c = gen.config5()
+    off = c.offsets()
+    cost = c.row_costs()
+    for world in (2, 4, 8):
+        ranges = partition_by_cost(off, c.n, cost, world)
+        assert ranges[0][0] == 0 and ranges[-1][1] == c.n
+        assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+        assert all(lo in set(off.tolist()) for lo, _ in ranges)  # community boundaries
+        cum = np.concatenate([[0.0], np.cumsum(cost)])
+        share = np.array([cum[hi] - cum[lo] for lo, hi in ranges]) / cum[-1]
+        assert share.max() < 1.0 / world * 1.05
