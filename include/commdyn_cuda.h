@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 9
+#define CDK_ABI_VERSION 10
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -143,6 +143,13 @@ typedef struct cdk_graph {
   int32_t inter_blocks;         /* 0 (off) or 1..4 (1: no column split) */
   int32_t inter_block_nodes;
   const uint64_t *inter_split;  /* [n_rows] (inter_blocks >= 2) or NULL (cdk_inter_split) */
+  /* Staged inter indices: segments whose inter run (seg_xr[2s]..seg_xr[2s+1],
+   * 4-entry aligned) fits xs_cap int32 entries have it bulk-copied into
+   * shared memory with the window, so the row pipeline reads inter columns
+   * from shared memory and issues the z gathers two rows ahead.  0 = off. */
+  int32_t xs_cap;               /* multiple of 16 */
+  int32_t reserved0;
+  const int64_t *seg_xr;        /* [2*n_seg] inter_ptr at the segment's first/last row, or NULL */
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */

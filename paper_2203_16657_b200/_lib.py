@@ -49,6 +49,9 @@ class CdkGraph(ctypes.Structure):
         ("inter_blocks", I32),
         ("inter_block_nodes", I32),
         ("inter_split", P),
+        ("xs_cap", I32),
+        ("reserved0", I32),
+        ("seg_xr", P),
     ]
 
 
@@ -165,7 +168,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 _lock = threading.Lock()
 _lib = None

@@ -87,7 +87,8 @@ struct StageArgs {
   int sweep_mode;  // inter sweep lanes/unroll variant (CDK_SWEEP, experiments)
   int debug_flags; // CDK_DEBUG_FLAGS (timing experiments only; results invalid):
                    // 1 = skip the inter sweep, 2 = skip the segments,
-                   // 4 = drop inline inter entries, 8 = drop intra gathers
+                   // 4 = drop inline inter entries, 8 = drop intra gathers,
+                   // 32 = intra column chunks re-read from one cached line
   double k_over_n;
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
@@ -156,20 +157,33 @@ __device__ __forceinline__ double2 lds_d2(uint32_t addr) {
 // Staged: explicit ld.shared from the window (32-bit shared address),
 // branch-free, padding (0xFFFF) clamped onto a zero slot one past the window
 // capacity.  Unstaged (global, huge communities / NONE pool): predicated loads.
+#ifndef CDK_LDS_BATCH
+#define CDK_LDS_BATCH 8
+#endif
 __device__ __forceinline__ void gather8_smem(const uint4 w, uint32_t zs_addr, uint32_t zero_slot,
                                              double &sr, double &si) {
-  // two independent accumulation chains (even / odd entries), fixed combine
+  // all loads of a batch issued before any add: the shared-memory latency is
+  // paid once per batch, not once per pair of entries (measured: with two
+  // loads in flight per warp the gather was latency-bound at ~0.45
+  // cycles/entry/SM); fixed combine order
   const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  constexpr int B = CDK_LDS_BATCH;
   double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
 #pragma unroll
-  for (int k = 0; k < 8; k += 2) {
-    const uint32_t u0 = wv[k >> 1] & 0xFFFFu, u1 = wv[k >> 1] >> 16;
-    const double2 z0 = lds_d2(zs_addr + (min(u0, zero_slot) << 4));
-    const double2 z1 = lds_d2(zs_addr + (min(u1, zero_slot) << 4));
-    ar += z0.x;
-    ai += z0.y;
-    br += z1.x;
-    bi += z1.y;
+  for (int k0 = 0; k0 < 8; k0 += B) {
+    double2 z[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const uint32_t u = (wv[(k0 + k) >> 1] >> (((k0 + k) & 1) * 16)) & 0xFFFFu;
+      z[k] = lds_d2(zs_addr + (min(u, zero_slot) << 4));
+    }
+#pragma unroll
+    for (int k = 0; k < B; k += 2) {
+      ar += z[k].x;
+      ai += z[k].y;
+      br += z[k + 1].x;
+      bi += z[k + 1].y;
+    }
   }
   sr -= ar + br;
   si -= ai + bi;
@@ -209,11 +223,12 @@ __device__ __forceinline__ void gather8_global(const uint4 w, const double2 *__r
 // neighbours from global memory; everything else is identical.
 // ---------------------------------------------------------------------------
 #ifndef CDK_STAGE_THREADS
-#define CDK_STAGE_THREADS 1024
+#define CDK_STAGE_THREADS 896  // measured: 896 ~ 768 > 640 > 1024 threads (register room)
 #endif
 constexpr int NTHREADS = CDK_STAGE_THREADS;
 constexpr int NWARPS = NTHREADS / 32;
 constexpr int NGROUPS = NTHREADS / 8;
+constexpr int SWEEP_THREADS = 1024;  // inter sweep launch (no shared memory, own config)
 
 struct SegSmem {  // carve-up of dynamic shared memory (all 16-byte aligned)
   double2 *acc;     // [cap4]   row sums, index i - row0
@@ -223,12 +238,14 @@ struct SegSmem {  // carve-up of dynamic shared memory (all 16-byte aligned)
   double *som;      // [cap4]   omega[row0a ..]
   double *sks;      // [cap4]   ksum[row0a ..]
   double2 *zs;      // [smem_nodes + 8] window + zero slot
+  int32_t *sxc;     // [xs_cap + 4] staged inter columns of the segment (xs_cap > 0)
 };
 
 __host__ __device__ inline size_t cap4_of(int cap) { return (size_t)cap + 4; }
 
-__host__ __device__ inline size_t stage_smem_bytes(int cap, int smem_nodes) {
-  return cap4_of(cap) * (16 + 5 * 8) + ((size_t)smem_nodes + 8) * 16;
+__host__ __device__ inline size_t stage_smem_bytes(int cap, int smem_nodes, int xs_cap = 0) {
+  return cap4_of(cap) * (16 + 5 * 8) + ((size_t)smem_nodes + 8) * 16 +
+         (xs_cap > 0 ? ((size_t)xs_cap + 4) * 4 : 0);
 }
 
 __device__ __forceinline__ SegSmem carve_smem(unsigned char *base, int cap, int smem_nodes) {
@@ -241,6 +258,7 @@ __device__ __forceinline__ SegSmem carve_smem(unsigned char *base, int cap, int 
   m.som = m.sth + c4;
   m.sks = m.som + c4;
   m.zs = reinterpret_cast<double2 *>(m.sks + c4);
+  m.sxc = reinterpret_cast<int32_t *>(m.zs + smem_nodes + 8);
   return m;
 }
 
@@ -278,7 +296,7 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
                                              uint32_t zero_slot, const double2 *zglob,
                                              const uint4 *__restrict__ colv,
                                              const int32_t *__restrict__ xcol, int pass,
-                                             int npass) {
+                                             int npass, const int32_t *sxc) {
   constexpr int NG = NTHREADS / LPR;
   constexpr int STRIDE = 8 * LPR;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -304,14 +322,20 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
         R.x0 = R.x1 = 0;
       }
       R.p = e0 + 8 * t;
-      R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
+      if (sxc) {  // staged inter columns: the z gather goes out two rows ahead
+        R.j = (R.x0 + t < R.x1) ? sxc[R.x0 + t] : -1;
+        R.z = (R.j >= 0) ? ldz(z_in + R.j) : make_double2(0.0, 0.0);
+      } else {
+        R.j = (R.x0 + t < R.x1) ? ldg(xcol + R.x0 + t) : -1;
+      }
     }
   };
+  const int cmask = (a.debug_flags & 32) ? 7 : 0x7FFFFFFF;  // timing experiment only
   auto stage_data = [&](int r, RowPipe &R) {
     if (r < nrows) {
-      R.c0 = (R.p < R.e1) ? ldg(colv + (R.p >> 3)) : padv;
-      R.c1 = (R.p + STRIDE < R.e1) ? ldg(colv + ((R.p + STRIDE) >> 3)) : padv;
-      R.z = (R.j >= 0) ? ldz(z_in + R.j) : make_double2(0.0, 0.0);
+      R.c0 = (R.p < R.e1) ? ldg(colv + ((R.p >> 3) & cmask)) : padv;
+      R.c1 = (R.p + STRIDE < R.e1) ? ldg(colv + (((R.p + STRIDE) >> 3) & cmask)) : padv;
+      if (!sxc) R.z = (R.j >= 0) ? ldz(z_in + R.j) : make_double2(0.0, 0.0);
     }
   };
   RowPipe A{}, B{}, C{};
@@ -327,7 +351,7 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
       if (A.p < A.e1) gather8_smem(A.c0, zs_addr, zero_slot, sr, si);  // skip all-pad chunks
       if (A.p + STRIDE < A.e1) gather8_smem(A.c1, zs_addr, zero_slot, sr, si);
       for (int p = A.p + 2 * STRIDE; p < A.e1; p += STRIDE)
-        gather8_smem(ldg(colv + (p >> 3)), zs_addr, zero_slot, sr, si);
+        gather8_smem(ldg(colv + ((p >> 3) & cmask)), zs_addr, zero_slot, sr, si);
     } else {
       gather8_global(A.c0, zglob, sr, si);
       gather8_global(A.c1, zglob, sr, si);
@@ -337,21 +361,24 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
     sr += A.z.x;
     si += A.z.y;
     for (int p = A.x0 + LPR + t; p < A.x1; p += LPR) {
-      const double2 z = ldz(z_in + ldg(xcol + p));
+      const double2 z = ldz(z_in + (sxc ? sxc[p] : ldg(xcol + p)));
       sr += z.x;
       si += z.y;
     }
+    // group reduction with a transposed first level: lanes of the low half
+    // keep the real part, the high half the imaginary part, so every level
+    // moves ONE double (2 SHFL) instead of two (fixed order, deterministic)
+    const bool hi_half = (t & (LPR / 2)) != 0;
+    double v = hi_half ? si : sr;
+    v += __shfl_xor_sync(gmask, hi_half ? sr : si, LPR / 2);
 #pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) {
-      sr += __shfl_xor_sync(gmask, sr, o);
-      si += __shfl_xor_sync(gmask, si, o);
-    }
-    if (t == 0) {
+    for (int o = LPR / 4; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+    if (t == 0 || t == LPR / 2) {  // t = 0 owns .x, t = LPR/2 owns .y
+      double *dst = reinterpret_cast<double *>(sm.acc + r) + (t ? 1 : 0);
       if (!MULTI || pass == 0) {
-        sm.acc[r] = make_double2(sr, si);
+        *dst = v;
       } else {
-        const double2 prev = sm.acc[r];
-        sm.acc[r] = make_double2(prev.x + sr, prev.y + si);
+        *dst = *dst + v;
       }
     }
     A = B;
@@ -413,7 +440,7 @@ __device__ __forceinline__ void inter_sweep(const StageArgs &a) {
   const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
   if (segA == segB) return;
   const int64_t rA = g.rblk_row0[g.seg_rblk[segA]], rB = g.rblk_row0[g.seg_rblk[segB]];
-  constexpr int NG = NTHREADS / LPR;
+  constexpr int NG = SWEEP_THREADS / LPR;
   const int tid = threadIdx.x, lane = tid & 31;
   const int t = lane & (LPR - 1), grp = tid / LPR;
   const unsigned gmask = (LPR == 32) ? FULL : (((1u << LPR) - 1u) << (lane & ~(LPR - 1)));
@@ -497,7 +524,7 @@ __device__ __forceinline__ void inter_sweep_pipe(const StageArgs &a) {
 #pragma unroll
     for (int k = 0; k < IU; ++k) jn[k] = (c0 + t + LPR * k < c1) ? ldg(xc + c0 + t + LPR * k) : -1;
     while (i < rB) {
-      const int64_t i2 = i + NGROUPS;
+      const int64_t i2 = i + SWEEP_THREADS / LPR;
       int64_t n0 = 0, n1 = 0;
       if (i2 < rB) span(i2, q, n0, n1);  // next row's span: in flight with this row's gathers
       double2 prev = make_double2(0.0, 0.0);
@@ -615,14 +642,24 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     const bool inter_inline = inter_inline0 && !(a.debug_flags & 4);
     const bool inter_phased = !swept && !inter_inline0 && !(a.debug_flags & 4);
 
+    // staged inter columns (xs): the segment's inter run, 4-entry aligned
+    int64_t xs_beg = 0;
+    bool xs_ok = false;
+    if (g.xs_cap > 0 && g.seg_xr != nullptr && inter_inline) {
+      xs_beg = g.seg_xr[2 * s] & ~(int64_t)3;
+      xs_ok = g.seg_xr[2 * s + 1] - xs_beg <= (int64_t)g.xs_cap;
+    }
     // ---- 1. stage window, pointer slices, epilogue inputs (async) ----------
     if (tid == 0) {
       fence_proxy_async_smem();  // earlier generic accesses before the async overwrite
       const uint32_t bw = staged ? (uint32_t)(min(w1 - w0, (int64_t)wn) * 16) : 0u;
       const uint32_t bp = (uint32_t)((((row1 + 2) & ~(int64_t)1) - row0a) * 8);
       const uint32_t br = (uint32_t)((((row1 + 1) & ~(int64_t)1) - row0a) * 8);
+      const uint32_t bx =
+          xs_ok ? (uint32_t)(((g.seg_xr[2 * s + 1] - xs_beg + 3) & ~(int64_t)3) * 4) : 0u;
       const int nr_in = (MODE == 0) ? 1 : ((MODE == 1 || MODE == 5) ? 2 : 3);
-      mbar_expect_tx(&bar_seg, bw + 2 * bp);
+      mbar_expect_tx(&bar_seg, bw + 2 * bp + bx);
+      if (bx) bulk_g2s(sm.sxc, g.inter_col + xs_beg, bx, &bar_seg);
       if (bw) bulk_g2s(sm.zs, z_in + w0, bw, &bar_seg);
       bulk_g2s(sm.sip, g.intra_ptr + row0a, bp, &bar_seg);
       bulk_g2s(sm.sxp, g.inter_ptr + row0a, bp, &bar_seg);
@@ -680,6 +717,8 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     const uint4 *__restrict__ colv = reinterpret_cast<const uint4 *>(g.intra_col + ebase);
     const int32_t *__restrict__ xcol = g.inter_col + xbase;
     const int lpr = g.seg_lpr[s] & 0xFF;
+    // inter column p of the segment (relative to xbase) lives at sxc[p + xbase - xs_beg]
+    const int32_t *sxc_rel = xs_ok ? sm.sxc + (xbase - xs_beg) : nullptr;
 
     // ---- 2. gather: lanes per row chosen per segment (4 / 8 / 16 / 32); a
     //         community wider than the window is gathered in passes, each
@@ -702,7 +741,7 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
       const uint32_t zero_p = zero_slot + (uint32_t)pass * (uint32_t)wn;
 #define CDK_GATHER(L, M, I)                                                                  \
   gather_phase<L, M, I>(a, sm, nrows, row0, row0a, ebase, xbase, staged, zs_p, zero_p, zglob, \
-                        colv, xcol, pass, npass)
+                        colv, xcol, pass, npass, sxc_rel)
       const bool multi = npass > 1;
       if (a.debug_flags & 8) {
         for (int r = tid; r < nrows; r += NTHREADS) sm.acc[r] = make_double2(0.0, 0.0);
@@ -811,7 +850,7 @@ __device__ __forceinline__ void init_cta(const cdk_graph &g, const SegSmem &sm, 
 // the random-gather rate (124 vs 240 Ggathers/s, tools/sweep_bench.cu), the
 // L1 left for in-flight misses being too small.  Same CTA row ranges as the
 // stage kernel (cta_seg).
-__global__ void __launch_bounds__(NTHREADS, 1) inter_sweep_kernel(const StageArgs a) {
+__global__ void __launch_bounds__(SWEEP_THREADS, 1) inter_sweep_kernel(const StageArgs a) {
   inter_sweep_dispatch(a);
 }
 
@@ -963,7 +1002,7 @@ static int check_graph(const cdk_graph *g) {
 }
 
 static size_t stage_smem(const cdk_graph *g) {
-  return stage_smem_bytes(g->seg_rows_cap, g->smem_nodes);
+  return stage_smem_bytes(g->seg_rows_cap, g->smem_nodes, g->xs_cap);
 }
 
 template <int MODE>
@@ -985,7 +1024,7 @@ static int launch_stage(const StageArgs &a, cudaStream_t st) {
     return CDK_INPUT;
   }
   if (a.g.inter_blocks > 0 && !(a.debug_flags & 1)) {
-    inter_sweep_kernel<<<a.g.n_cta, a.g.cta_threads, 0, st>>>(a);
+    inter_sweep_kernel<<<a.g.n_cta, SWEEP_THREADS, 0, st>>>(a);
     CDK_CHECK_LAUNCH("inter_sweep_kernel");
   }
   kuramoto_stage_kernel<MODE><<<a.g.n_cta, a.g.cta_threads, smem, st>>>(a);

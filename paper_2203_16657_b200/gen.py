@@ -239,9 +239,9 @@ def device_graph(case: LfrCase, device=None, sm_count: int | None = None,
     """(DeviceGraph, GeneratedCsr) for ``case``: generate, plan, rebase in place.
     ``smem_budget`` shrinks the stage kernel's window (tests: multi-pass paths
     at small sizes); ``row_range`` generates one rank's shard."""
-    from .plan import ROWS_CAP, SMEM_OPTIN, DeviceGraph
+    from .plan import ROWS_CAP, SMEM_BUDGET, DeviceGraph
 
-    budget = SMEM_OPTIN - 2048 if smem_budget is None else int(smem_budget)
+    budget = SMEM_BUDGET if smem_budget is None else int(smem_budget)
     csr = generate(case, device, pass_nodes=window_nodes(ROWS_CAP, budget), row_range=row_range)
     dg = DeviceGraph.from_device_csr(csr.layout(), csr.intra_col, csr.inter_col,
                                      csr.intra_col.device, sm_count=sm_count,

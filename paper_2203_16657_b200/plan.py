@@ -79,13 +79,15 @@ class Schedule:
     cta_seg: np.ndarray  # int32[n_cta+1]
     seg_lpr: np.ndarray  # int32[n_seg] lanes per row (4 | 8 | 16 | 32)
     intra_col: np.ndarray  # uint16, rebased to each row's segment base, bank-ordered
+    xs_cap: int = 0  # staged inter-column capacity (cdk_graph.xs_cap)
+    seg_xr: np.ndarray | None = None  # int64[2*n_seg] inter_ptr at segment bounds
 
     @property
     def n_seg(self) -> int:
         return int(self.seg_rblk.shape[0] - 1)
 
     def smem_bytes(self) -> int:
-        return stage_smem_bytes(self.smem_nodes, self.seg_rows_cap)
+        return stage_smem_bytes(self.smem_nodes, self.seg_rows_cap, self.xs_cap)
 
 
 def _row_runs(rows_sorted: np.ndarray, n_rows: int):
@@ -123,7 +125,7 @@ def _split_heavy_rblocks(row0, row_end, intra_ptr, inter_ptr):
 
 
 WIN_ALIGN = 8  # staged windows start/end on 8-node (128-byte) boundaries (bulk-copy alignment)
-CTA_THREADS = 1024  # default; the library's value wins (stage_threads())
+CTA_THREADS = 896  # default; the library's value wins (stage_threads())
 
 
 def stage_threads() -> int:
@@ -131,18 +133,27 @@ def stage_threads() -> int:
     from ._lib import load_library
 
     return int(load_library().cdk_kuramoto_stage_threads())
-ROWS_CAP = 1536  # rows per segment (shared-memory row buffers; multiple of 8)
+import os as _os
+
+ROWS_CAP = int(_os.environ.get("CDK_ROWS_CAP", 1536))  # rows per segment (multiple of 8)
+# shared-memory budget of the stage kernel (CDK_SMEM_BUDGET: experiments with
+# a smaller carve-out, which leaves more L1 for in-flight global loads)
+SMEM_BUDGET = int(_os.environ.get("CDK_SMEM_BUDGET", 232448 - 2048))
 SEG_MAX_COMM = 64  # communities per staged segment (csrc/kuramoto.cu SEG_MAX_COMM)
 MAX_PASS = 4  # window passes per community (cdk_graph.intra_split packs 3 sub-run starts)
+XS_MAX = 16384  # staged inter columns per segment (cdk_graph.xs_cap), upper bound
+XS_MIN = 1024
 
 
-def stage_smem_bytes(smem_nodes: int, rows_cap: int = ROWS_CAP) -> int:
+def stage_smem_bytes(smem_nodes: int, rows_cap: int = ROWS_CAP, xs_cap: int = 0) -> int:
     """dynamic shared memory of the stage kernel (csrc/kuramoto.cu:stage_smem_bytes):
-    row accumulators + pointer slices + epilogue inputs + window (+8 spare)"""
-    return (rows_cap + 4) * (16 + 5 * 8) + 16 * (smem_nodes + 8)
+    row accumulators + pointer slices + epilogue inputs + window (+8 spare)
+    + staged inter columns (+4 spare)"""
+    return ((rows_cap + 4) * (16 + 5 * 8) + 16 * (smem_nodes + 8)
+            + (4 * (xs_cap + 4) if xs_cap > 0 else 0))
 
 
-def window_nodes(rows_cap: int = ROWS_CAP, smem_budget: int = SMEM_OPTIN - 2048) -> int:
+def window_nodes(rows_cap: int = ROWS_CAP, smem_budget: int = SMEM_BUDGET) -> int:
     """staged window capacity (nodes, multiple of 8) of the stage kernel"""
     rows_cap = int(rows_cap) // 8 * 8
     return max(0, (smem_budget - stage_smem_bytes(0, rows_cap)) // 16) // WIN_ALIGN * WIN_ALIGN
@@ -271,7 +282,7 @@ def _rblk_rows(lay: HostLayout) -> np.ndarray:
 
 
 def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int = ROWS_CAP,
-                   smem_budget: int = SMEM_OPTIN - 2048) -> Schedule:
+                   smem_budget: int = SMEM_BUDGET) -> Schedule:
     """Cost-balanced contiguous CTA ranges of rblocks (one CTA per SM), split
     into segments of <= rows_cap rows whose intra neighbours fit one
     shared-memory window (or, for communities above the window capacity and
@@ -298,6 +309,17 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         npass_c = np.where(npass_c == 1, 1, 0)
     stageable = npass_c >= 1
     multi = npass_c > 1
+    # staged inter columns: when no community needs window passes, shrink the
+    # window to the widest staged community and give the rest of the budget
+    # to the segment's inter-column slice (row pipeline reads them from smem)
+    xs_cap = 0
+    if (_os.environ.get("CDK_XS", "1") != "0" and not multi.any()
+            and lay.nnz_inter > 0 and stageable.any()):
+        need = int((win_hi - win_lo)[stageable].max())
+        rem = smem_budget - stage_smem_bytes(need, rows_cap)
+        cap = min(rem // 4 - 4, XS_MAX) // 16 * 16
+        if cap >= XS_MIN:
+            xs_cap, smem_nodes = int(cap), need
     mode_c, mode_pool = _comm_modes(lay)
     seg_rblk, seg_win, seg_base, cta_seg, seg_lpr = [0], [], [], [0], []
     for b in range(n_cta):
@@ -344,9 +366,13 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         comm_row = np.repeat(lay.rblk_comm.astype(np.int64), np.diff(rows))
         cstart = np.where(comm_row >= 0, off[np.maximum(comm_row, 0)], 0)
         delta[rows[0]: rows[-1]] = cstart - seg_base[seg_of_row]
+    seg_rows = rows[seg_rblk]
+    seg_xr = np.stack([lay.inter_ptr[seg_rows[:-1]], lay.inter_ptr[seg_rows[1:]]], 1).reshape(-1)
+    seg_xr = seg_xr.astype(np.int64)
     if lay.intra_col is None:  # columns live on the device: caller rebases (cdk_gen_rebase)
         sch = Schedule(n_cta, stage_threads(), int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
-                       seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, None)
+                       seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, None, xs_cap,
+                       seg_xr)
         sch.row_delta = delta.astype(np.int32)
         return sch
     col = lay.intra_col.copy()
@@ -359,7 +385,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         col[m] = newc.astype(np.uint16)
     _bank_order(col, _sub_run_ptr(lay), smem_nodes)
     return Schedule(n_cta, stage_threads(), int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
-                    seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, col)
+                    seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, col, xs_cap, seg_xr)
 
 
 SEG_INTER_PHASE = 256  # include/commdyn_cuda.h CDK_SEG_INTER_PHASE
@@ -369,8 +395,7 @@ INTER_PHASE_MIN = 16.0  # mean inter entries per row above which a segment runs 
 def _comm_modes(lay: HostLayout):
     """Gather mode per community (and for the NONE pool): lanes per row (rows
     in flight matter more than lanes per row — measured: 16/32 lanes per row
-    double the gather time; short rows use 4) | SEG_INTER_PHASE for
-    inter-heavy rows.  Decided per community from its own rows, so every
+    double the gather time) | SEG_INTER_PHASE for inter-heavy rows.  Decided per community from its own rows, so every
     shard of a multi-GPU run picks the same mode for the same rows (bitwise
     equal trajectories); segments never mix modes.  CDK_LPR and
     CDK_INTER_PHASE (0/1) override for experiments."""
@@ -380,13 +405,13 @@ def _comm_modes(lay: HostLayout):
     lam = np.maximum(np.diff(off), 1)
     lens = (lay.intra_ptr[off[1:]] - lay.intra_ptr[off[:-1]]) / lam
     xl = (lay.inter_ptr[off[1:]] - lay.inter_ptr[off[:-1]]) / lam
-    forced = os.environ.get("CDK_LPR")
-    lpr = (np.full(lens.shape[0], int(forced), dtype=np.int32) if forced
-           else np.where(lens > 24, 8, 4).astype(np.int32))
+    # 8 lanes everywhere: a per-community 4/8 choice split config 2 into 24%
+    # more segments and cost 15% (segments cannot mix lane counts)
+    lpr = np.full(lens.shape[0], int(os.environ.get("CDK_LPR", 8)), dtype=np.int32)
     fx = os.environ.get("CDK_INTER_PHASE")
     sep = (np.full(lens.shape[0], fx == "1") if fx in ("0", "1") else xl > INTER_PHASE_MIN)
     mode = (lpr | np.where(sep, SEG_INTER_PHASE, 0)).astype(np.int32)
-    pool = (int(forced) if forced else 4) | (SEG_INTER_PHASE if fx == "1" else 0)
+    pool = int(os.environ.get("CDK_LPR", 8)) | (SEG_INTER_PHASE if fx == "1" else 0)
     return mode, int(pool)
 
 
@@ -465,7 +490,7 @@ class DeviceGraph:
     cdk_graph struct handed to the C ABI."""
 
     def __init__(self, dec: Decomposition, device=None, sm_count: int | None = None,
-                 row_range=None, smem_budget: int = SMEM_OPTIN - 2048):
+                 row_range=None, smem_budget: int = SMEM_BUDGET):
         import torch
 
         from ._lib import CdkGraph
@@ -503,6 +528,7 @@ class DeviceGraph:
             "seg_base": up(sch.seg_base),
             "cta_seg": up(sch.cta_seg),
             "seg_lpr": up(sch.seg_lpr if sch.n_seg else np.zeros(1, np.int32)),
+            "seg_xr": up(sch.seg_xr if sch.n_seg else np.zeros(2, np.int64)),
         }
         if lay.intra_split is not None:
             self._t["intra_split"] = up(lay.intra_split.view(np.int64))
@@ -527,6 +553,7 @@ class DeviceGraph:
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
             inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
             inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
+            xs_cap=sch.xs_cap, reserved0=0, seg_xr=t["seg_xr"].data_ptr(),
         )
 
     def device_bytes(self) -> int:
@@ -535,7 +562,7 @@ class DeviceGraph:
     @classmethod
     def from_device_csr(cls, lay: "HostLayout", intra_col_dev, inter_col_dev, device,
                         sm_count: int | None = None, split_dev=None,
-                        smem_budget: int = SMEM_OPTIN - 2048, bank_order: bool = True,
+                        smem_budget: int = SMEM_BUDGET, bank_order: bool = True,
                         row_range=None):
         """Graph whose columns were generated on the device (config 5): the
         schedule is planned from the host copies of the row pointers and the
@@ -567,6 +594,7 @@ class DeviceGraph:
             "comm_rblk_off": up(lay.comm_rblk_off), "seg_rblk": up(sch.seg_rblk),
             "seg_win": up(sch.seg_win.reshape(-1)), "seg_base": up(sch.seg_base),
             "cta_seg": up(sch.cta_seg), "seg_lpr": up(sch.seg_lpr),
+            "seg_xr": up(sch.seg_xr),
         }
         if split_dev is not None:
             self._t["intra_split"] = split_dev
@@ -600,5 +628,6 @@ class DeviceGraph:
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
             inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
             inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
+            xs_cap=sch.xs_cap, reserved0=0, seg_xr=t["seg_xr"].data_ptr(),
         )
         return self
