@@ -142,6 +142,10 @@ SMEM_BUDGET = int(_os.environ.get("CDK_SMEM_BUDGET", 232448 - 2048))
 SEG_MAX_COMM = 64  # communities per staged segment (csrc/kuramoto.cu SEG_MAX_COMM)
 MAX_PASS = 4  # window passes per community (cdk_graph.intra_split packs 3 sub-run starts)
 XS_MAX = 16384  # staged inter columns per segment (cdk_graph.xs_cap), upper bound
+# fixed cost of a segment in cost-model units (~9k cycles per segment in the
+# per-CTA profile fit at ~0.22 cycles per unit); SCHED_ITERS re-cuts with it
+SEG_COST = float(_os.environ.get("CDK_SEG_COST", 40000))
+SCHED_ITERS = 6
 XS_MIN = 1024
 
 
@@ -294,10 +298,6 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
     rows = _rblk_rows(lay)
     cum = np.concatenate([[0.0], np.cumsum(lay.row_cost)])
     rb_cost = cum[rows[1:]] - cum[rows[:-1]]
-    cum_rb = np.concatenate([[0.0], np.cumsum(rb_cost)])
-    targets = cum_rb[-1] * np.arange(1, n_cta) / n_cta
-    cuts = np.clip(np.searchsorted(cum_rb, targets, side="left"), 0, nrb)
-    cta_bounds = np.maximum.accumulate(np.concatenate([[0], cuts, [nrb]]).astype(np.int64))
 
     off = lay.comm_off
     win_lo = off[:-1] // WIN_ALIGN * WIN_ALIGN
@@ -321,6 +321,50 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         if cap >= XS_MIN:
             xs_cap, smem_nodes = int(cap), need
     mode_c, mode_pool = _comm_modes(lay)
+
+    def segments(cta_bounds):
+        return _build_segments(lay, rows, cta_bounds, n_cta, rows_cap, smem_nodes, win_lo, win_hi,
+                               stageable, multi, mode_c, mode_pool)
+
+    # CTA cuts balanced on row cost plus SEG_COST per segment: a segment's
+    # fixed cost (staging, community sums, pipeline ramp, barriers) is only
+    # known once the cuts are placed, so iterate (damped) and keep the best
+    targets_frac = np.arange(1, n_cta) / n_cta
+    extra = np.zeros(nrb)
+    best = None
+    iters = SCHED_ITERS if n_cta > 1 and nrb > n_cta else 1
+    if nrb > 50000:  # huge graphs (config 5): segments are long, the fixed cost matters less
+        iters = min(iters, 2)
+    for _ in range(iters):
+        cum_rb = np.concatenate([[0.0], np.cumsum(rb_cost + extra)])
+        cuts = np.clip(np.searchsorted(cum_rb, cum_rb[-1] * targets_frac, side="left"), 0, nrb)
+        bounds = np.maximum.accumulate(np.concatenate([[0], cuts, [nrb]]).astype(np.int64))
+        segs = segments(bounds)
+        nseg_b = np.diff(np.asarray(segs[3]))
+        cum0 = np.concatenate([[0.0], np.cumsum(rb_cost)])
+        cta_cost = cum0[bounds[1:]] - cum0[bounds[:-1]] + SEG_COST * nseg_b
+        if best is None or cta_cost.max() < best[0]:
+            best = (cta_cost.max(), segs)
+        share = np.zeros(nrb)
+        for b in range(n_cta):
+            lo, hi = int(bounds[b]), int(bounds[b + 1])
+            if hi > lo:
+                w = rb_cost[lo:hi]
+                share[lo:hi] = SEG_COST * nseg_b[b] * w / max(w.sum(), 1e-9)
+        extra = 0.5 * extra + 0.5 * share
+    seg_rblk, seg_win, seg_base, cta_seg, seg_lpr = best[1]
+    seg_rblk = np.asarray(seg_rblk, dtype=np.int32)
+    seg_lpr = np.asarray(seg_lpr, dtype=np.int32)
+    seg_win = np.asarray(seg_win, dtype=np.int64).reshape(-1, 2)
+    seg_base = np.asarray(seg_base, dtype=np.int64)
+    return _finish_schedule(lay, rows, n_cta, rows_cap, smem_nodes, xs_cap, seg_rblk, seg_win,
+                            seg_base, cta_seg, seg_lpr, off)
+
+
+def _build_segments(lay, rows, cta_bounds, n_cta, rows_cap, smem_nodes, win_lo, win_hi,
+                    stageable, multi, mode_c, mode_pool):
+    """segments of every CTA's rblock range (see build_schedule)"""
+    off = lay.comm_off
     seg_rblk, seg_win, seg_base, cta_seg, seg_lpr = [0], [], [], [0], []
     for b in range(n_cta):
         rb, rb_end = int(cta_bounds[b]), int(cta_bounds[b + 1])
@@ -353,10 +397,13 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
                 seg_lpr.append(int(mode_c[c]))
             seg_rblk.append(rb)
         cta_seg.append(len(seg_rblk) - 1)
-    seg_rblk = np.asarray(seg_rblk, dtype=np.int32)
-    seg_lpr = np.asarray(seg_lpr, dtype=np.int32)
-    seg_win = np.asarray(seg_win, dtype=np.int64).reshape(-1, 2)
-    seg_base = np.asarray(seg_base, dtype=np.int64)
+    return seg_rblk, seg_win, seg_base, cta_seg, seg_lpr
+
+
+def _finish_schedule(lay, rows, n_cta, rows_cap, smem_nodes, xs_cap, seg_rblk, seg_win, seg_base,
+                     cta_seg, seg_lpr, off):
+    """rebasing, bank ordering, segment inter ranges -> Schedule"""
+    nrb = lay.n_rblk
 
     # rebase intra columns (community-local in the layout) to each row's segment base
     n = lay.n_rows
