@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 10
+#define CDK_ABI_VERSION 11
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -160,6 +160,36 @@ typedef struct cdk_run_status {
   int64_t reserved;
 } cdk_run_status;
 
+/* ------------------------------------------------------------------------ */
+/* Fused multi-GPU exchange (community-sharded runs): each rank's */
+/* stage epilogue stores its new z rows straight into every peer's z buffer  */
+/* over NVLink (P2P stores), then the ranks meet at a system-scope counter   */
+/* barrier — replacing the per-stage NCCL all-gather.                        */
+/* ------------------------------------------------------------------------ */
+typedef struct cdk_peers {
+  int32_t n_ranks;             /* 1 = no peers */
+  int32_t rank;
+  void *const *z0;             /* [n_ranks] device array: every rank's z[0] (own included) */
+  void *const *z1;             /* [n_ranks] device array: every rank's z[1] */
+  unsigned int *const *bar;    /* [n_ranks] device array: every rank's peer-barrier counter */
+  unsigned int bar_base;       /* this rank's counter value before the call (host-tracked) */
+  int32_t wait;                /* 1: wait at the barrier; 0: signal only (single-device tests) */
+} cdk_peers;
+
+/* cdk_kuramoto_rk4 / cdk_kuramoto_rk4_stage with the fused exchange; the
+ * counter advances by n_ranks per stage (bar_base += 4*n_steps*n_ranks) */
+CDK_API int cdk_kuramoto_rk4_peers(const cdk_graph *g, double *theta, const double *omega,
+                                   double k_over_n, double dt, int64_t n_steps, void *workspace,
+                                   const cdk_peers *peers, void *stream);
+CDK_API int cdk_kuramoto_rk4_stage_peers(const cdk_graph *g, double *theta, const double *omega,
+                                         double k_over_n, double dt, int stage, void *workspace,
+                                         const cdk_peers *peers, void *stream);
+/* CUDA IPC helpers for the peer tables: export a device pointer (64-byte
+ * handle of its allocation + byte offset), import it in another process */
+CDK_API int cdk_ipc_export(const void *ptr, void *handle64, uint64_t *offset);
+CDK_API int cdk_ipc_import(const void *handle64, uint64_t offset, void **ptr);
+CDK_API int cdk_ipc_close(void *ptr, uint64_t offset);
+
 /* threads per CTA of the stage kernels (cdk_graph.cta_threads must match) */
 CDK_API int cdk_kuramoto_stage_threads(void);
 
@@ -192,7 +222,7 @@ CDK_API int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const doub
                                    void *stream);
 
 /* byte offsets inside the workspace of [z0, z1, ksum, part0, part1, status]
- * (offsets: [host] int64[6]); z_s buffers hold exp(i theta) of the stage state,
+ * (offsets: [host] int64[7]: z0 z1 ksum part0 part1 status peer_bar); z_s buffers hold exp(i theta) of the stage state,
  * stage k (1..4) reads z[(k-1)&1] and writes z[k&1].  Used by multi-rank
  * drivers to exchange each rank's freshly written rows after a stage. */
 CDK_API int cdk_kuramoto_workspace_layout(const cdk_graph *g, int64_t *offsets);

@@ -55,6 +55,18 @@ class CdkGraph(ctypes.Structure):
     ]
 
 
+class CdkPeers(ctypes.Structure):
+    _fields_ = [
+        ("n_ranks", I32),
+        ("rank", I32),
+        ("z0", P),
+        ("z1", P),
+        ("bar", P),
+        ("bar_base", ctypes.c_uint32),
+        ("wait", I32),
+    ]
+
+
 class CdkHoGraph(ctypes.Structure):
     _fields_ = [
         ("n_rows", I64),
@@ -152,6 +164,14 @@ _SIGS = {
     "cdk_gen_rebase": [I64, P, P, P, P],
     "cdk_inter_split": [I64, P, P, ctypes.c_int, ctypes.c_int, P, P],
     "cdk_bank_order": [I64, P, P, P, P, ctypes.c_int, P],
+    "cdk_kuramoto_rk4_peers": [ctypes.POINTER(CdkGraph), P, P, ctypes.c_double, ctypes.c_double,
+                               I64, P, ctypes.POINTER(CdkPeers), P],
+    "cdk_kuramoto_rk4_stage_peers": [ctypes.POINTER(CdkGraph), P, P, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_int, P, ctypes.POINTER(CdkPeers),
+                                     P],
+    "cdk_ipc_export": [P, P, ctypes.POINTER(ctypes.c_uint64)],
+    "cdk_ipc_import": [P, ctypes.c_uint64, ctypes.POINTER(P)],
+    "cdk_ipc_close": [P, ctypes.c_uint64],
     "cdk_abi_version": [],
     "cdk_last_error": [],
     "cdk_launch_count": [],
@@ -168,7 +188,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 _lock = threading.Lock()
 _lib = None

@@ -45,6 +45,7 @@ struct Workspace {
   cdk_run_status *status;
   unsigned int *bar;  // grid-barrier counter of the persistent kernel
   double2 *xacc;      // per-row inter sums (block-phased inter sweep only)
+  unsigned int *peer_bar;  // fused multi-GPU exchange: this rank's barrier counter
 };
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -68,6 +69,7 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
   w.status = (cdk_run_status *)take(sizeof(cdk_run_status));
   w.bar = (unsigned int *)take(256);
   w.xacc = g->inter_blocks > 0 ? (double2 *)take(n * sizeof(double2)) : nullptr;
+  w.peer_bar = (unsigned int *)take(256);
   if (total) *total = off;
   return w;
 }
@@ -84,6 +86,10 @@ struct StageArgs {
   double *ksum;
   double *out;  // MODE 0
   double2 *xacc;  // block-phased inter sums (g.inter_blocks > 0)
+  // fused multi-GPU exchange: the epilogue also stores z_out rows into every
+  // peer's buffer (peer_out[q], q != rank)
+  double2 *const *peer_out;
+  int n_peers, rank;
   int sweep_mode;  // inter sweep lanes/unroll variant (CDK_SWEEP, experiments)
   int debug_flags; // CDK_DEBUG_FLAGS (timing experiments only; results invalid):
                    // 1 = skip the inter sweep, 2 = skip the segments,
@@ -811,7 +817,10 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
             }
           }
           sincos(thn, &zim, &zr);
-          a.z_out[i] = make_double2(zr, zim);
+          const double2 zn = make_double2(zr, zim);
+          a.z_out[i] = zn;
+          for (int q = 0; q < a.n_peers; ++q)  // NVLink P2P stores (fused all-gather)
+            if (q != a.rank) a.peer_out[q][i] = zn;
         }
       }
       if (MODE != 0) {
@@ -832,6 +841,7 @@ __device__ __forceinline__ void stage_body(const StageArgs &a, const SegSmem &sm
     __syncthreads();  // shared segment buffers reused by the next segment
     PROF_MARK(t_epi);
   }
+  if (a.n_peers > 1) __threadfence_system();  // peer stores before the barrier signal
   parity = (pseg << 1) | pepi;
 }
 
@@ -897,15 +907,55 @@ __device__ __forceinline__ void grid_sync(unsigned int *counter, unsigned int ta
   __syncthreads();
 }
 
+// System-scope counter barrier of the fused exchange: signal every rank
+// (its counter gets +1 from each rank per stage), then wait until this
+// rank's counter reaches `target`.  A 20 s watchdog turns a lost peer into a
+// status error instead of a hang.
+struct PeerBar {
+  unsigned int *const *bar;
+  unsigned int *mine;
+  int n, wait;
+};
+
+__device__ __forceinline__ void peer_barrier(const PeerBar &pb, unsigned int target,
+                                             cdk_run_status *st) {
+  __threadfence_system();
+  for (int q = 0; q < pb.n; ++q) atomicAdd_system(pb.bar[q], 1u);
+  if (!pb.wait) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pb.mine) : "memory");
+    if ((int)(v - target) >= 0) break;
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 20000000000ull) {
+      atomicOr(reinterpret_cast<unsigned long long *>(&st->reserved), 1ull);
+      break;
+    }
+    __nanosleep(100);
+  }
+  __threadfence_system();
+}
+
+__global__ void peer_barrier_kernel(PeerBar pb, unsigned int target, cdk_run_status *st) {
+  peer_barrier(pb, target, st);
+}
+
 struct StepPtrs {
   double2 *z[2];
   double2 *part[2];
   unsigned int *bar;
+  double2 *const *peer_z[2];  // fused exchange: every rank's z[0] / z[1] (n_peers > 1)
+  PeerBar pb;
+  unsigned int pb_base;
 };
 
 // Persistent RK4: n_steps x 4 stages in ONE cooperative launch, grid barrier
 // between stages (no launch gaps; the CSR slices and window reloads are the
 // only per-stage traffic).
+template <bool PEERS>
 __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_rk4_kernel(StageArgs a, StepPtrs ptr,
                                                                    int64_t n_steps, double dt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -917,24 +967,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_rk4_kernel(StageArgs a, 
   ProfAcc pa;
   unsigned int sync_idx = 0;
   const double h2 = dt / 2.0, h6 = dt / 6.0;
+  unsigned int peer_target = ptr.pb_base;
+  // after a stage: grid barrier, and with peers the cross-GPU barrier (one
+  // thread) followed by a second grid barrier that releases every CTA
+#define CDK_STAGE_SYNC(last)                                                           \
+  do {                                                                                 \
+    if (PEERS) {                                                                       \
+      grid_sync(ptr.bar, ++sync_idx * gridDim.x);                                      \
+      peer_target += (unsigned int)a.n_peers;                                          \
+      if (blockIdx.x == 0 && threadIdx.x == 0) peer_barrier(ptr.pb, peer_target, a.status); \
+      if (!(last)) grid_sync(ptr.bar, ++sync_idx * gridDim.x);                         \
+    } else if (!(last)) {                                                              \
+      grid_sync(ptr.bar, ++sync_idx * gridDim.x);                                      \
+    }                                                                                  \
+  } while (0)
   for (int64_t step = 0; step < n_steps; ++step) {
     a.step_rel = step;
     a.z_in = ptr.z[0]; a.z_out = ptr.z[1]; a.part_in = ptr.part[0]; a.part_out = ptr.part[1];
+    a.peer_out = ptr.peer_z[1];
     a.h = h2;
     stage_body<1>(a, sm, bar_seg, bar_epi, sR, parity, pa);
-    grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+    CDK_STAGE_SYNC(false);
     a.z_in = ptr.z[1]; a.z_out = ptr.z[0]; a.part_in = ptr.part[1]; a.part_out = ptr.part[0];
+    a.peer_out = ptr.peer_z[0];
     stage_body<2>(a, sm, bar_seg, bar_epi, sR, parity, pa);
-    grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+    CDK_STAGE_SYNC(false);
     a.z_in = ptr.z[0]; a.z_out = ptr.z[1]; a.part_in = ptr.part[0]; a.part_out = ptr.part[1];
+    a.peer_out = ptr.peer_z[1];
     a.h = dt;
     stage_body<3>(a, sm, bar_seg, bar_epi, sR, parity, pa);
-    grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+    CDK_STAGE_SYNC(false);
     a.z_in = ptr.z[1]; a.z_out = ptr.z[0]; a.part_in = ptr.part[1]; a.part_out = ptr.part[0];
+    a.peer_out = ptr.peer_z[0];
     a.h = h6;
     stage_body<4>(a, sm, bar_seg, bar_epi, sR, parity, pa);
-    if (step + 1 < n_steps) grid_sync(ptr.bar, ++sync_idx * gridDim.x);
+    CDK_STAGE_SYNC(step + 1 == n_steps);
   }
+#undef CDK_STAGE_SYNC
 }
 
 // z = exp(i theta) and the canonical rblock partials (prepare).  One 8-lane
@@ -1055,6 +1124,9 @@ static StageArgs base_args(const cdk_graph *g, const Workspace &w, double *theta
   a.omega = omega;
   a.ksum = w.ksum;
   a.xacc = w.xacc;
+  a.peer_out = nullptr;
+  a.n_peers = 1;
+  a.rank = 0;
   {
     const char *e = getenv("CDK_SWEEP");
     a.sweep_mode = e ? atoi(e) : 0;
@@ -1099,16 +1171,19 @@ extern "C" int cdk_kuramoto_rhs(const cdk_graph *g, const double *theta, const d
 }
 
 static int launch_rk4_persistent(const StageArgs &a, const Workspace &w, int64_t n_steps,
-                                 double dt, cudaStream_t st) {
+                                 double dt, cudaStream_t st, const cdk_peers *peers = nullptr) {
   static int attr_bytes = -1;
   const size_t smem = stage_smem(&a.g);
   if (attr_bytes < 0) {
     cudaFuncAttributes fa{};
-    cudaError_t e = cudaFuncGetAttributes(&fa, kuramoto_rk4_kernel);
+    cudaError_t e = cudaFuncGetAttributes(&fa, kuramoto_rk4_kernel<false>);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncGetAttributes(rk4)");
     const int dyn_max = cdk_max_smem_optin() - (int)fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(kuramoto_rk4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dyn_max);
+    e = cudaFuncSetAttribute(kuramoto_rk4_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kuramoto_rk4_kernel<true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(rk4)");
     attr_bytes = dyn_max;
   }
@@ -1122,6 +1197,15 @@ static int launch_rk4_persistent(const StageArgs &a, const Workspace &w, int64_t
   ptr.part[0] = w.part[0];
   ptr.part[1] = w.part[1];
   ptr.bar = w.bar;
+  if (peers && peers->n_ranks > 1) {
+    ptr.peer_z[0] = reinterpret_cast<double2 *const *>(peers->z0);
+    ptr.peer_z[1] = reinterpret_cast<double2 *const *>(peers->z1);
+    ptr.pb.bar = peers->bar;
+    ptr.pb.mine = w.peer_bar;
+    ptr.pb.n = peers->n_ranks;
+    ptr.pb.wait = peers->wait;
+    ptr.pb_base = peers->bar_base;
+  }
   cudaError_t e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(grid barrier)");
   cudaLaunchConfig_t cfg{};
@@ -1134,7 +1218,10 @@ static int launch_rk4_persistent(const StageArgs &a, const Workspace &w, int64_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel, a, ptr, n_steps, dt);
+  if (peers && peers->n_ranks > 1)
+    e = cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel<true>, a, ptr, n_steps, dt);
+  else
+    e = cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel<false>, a, ptr, n_steps, dt);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(kuramoto_rk4_kernel)");
   return CDK_OK;
@@ -1267,6 +1354,7 @@ extern "C" int cdk_kuramoto_workspace_layout(const cdk_graph *g, int64_t *offset
   offsets[3] = reinterpret_cast<char *>(w.part[0]) - base;
   offsets[4] = reinterpret_cast<char *>(w.part[1]) - base;
   offsets[5] = reinterpret_cast<char *>(w.status) - base;
+  offsets[6] = reinterpret_cast<char *>(w.peer_bar) - base;
   return CDK_OK;
 }
 
@@ -1282,3 +1370,93 @@ extern "C" int cdk_kuramoto_advance(const cdk_graph *g, void *workspace, int64_t
 }
 
 extern "C" int cdk_kuramoto_stage_threads(void) { return cdk::NTHREADS; }
+
+static int check_peers(const cdk_peers *p) {
+  if (!p || p->n_ranks < 1 || p->rank < 0 || p->rank >= p->n_ranks ||
+      (p->n_ranks > 1 && (!p->z0 || !p->z1 || !p->bar))) {
+    set_error("cdk_peers: invalid table");
+    return CDK_INPUT;
+  }
+  return CDK_OK;
+}
+
+static void apply_peers(StageArgs &a, const cdk_peers *p) {
+  a.n_peers = p->n_ranks;
+  a.rank = p->rank;
+}
+
+extern "C" int cdk_kuramoto_rk4_peers(const cdk_graph *g, double *theta, const double *omega,
+                                      double k_over_n, double dt, int64_t n_steps,
+                                      void *workspace, const cdk_peers *peers, void *stream) {
+  int rc = check_graph(g);
+  if (rc || (rc = check_peers(peers))) return rc;
+  if (n_steps < 0) return set_error("n_steps < 0"), CDK_INPUT;
+  if (n_steps == 0) return CDK_OK;
+  cudaStream_t st = as_stream(stream);
+  Workspace w = carve(g, workspace, nullptr);
+  StageArgs a = base_args(g, w, theta, omega, k_over_n);
+  apply_peers(a, peers);
+  if (g->inter_blocks > 0) {  // per-stage launches: stage kernel, then the peer barrier
+    PeerBar pb{peers->bar, w.peer_bar, peers->n_ranks, peers->wait};
+    unsigned int target = peers->bar_base;
+    auto z = [&](int k) { return k ? peers->z1 : peers->z0; };
+    for (int64_t s = 0; s < n_steps; ++s) {
+      a.step_rel = s;
+      for (int stg = 1; stg <= 4; ++stg) {
+        const int src = (stg - 1) & 1;
+        a.z_in = w.z[src]; a.z_out = w.z[src ^ 1];
+        a.part_in = w.part[src]; a.part_out = w.part[src ^ 1];
+        a.peer_out = reinterpret_cast<double2 *const *>(z(src ^ 1));
+        a.h = (stg == 3) ? dt : (stg == 4 ? dt / 6.0 : dt / 2.0);
+        switch (stg) {
+          case 1: rc = launch_stage<1>(a, st); break;
+          case 2: rc = launch_stage<2>(a, st); break;
+          case 3: rc = launch_stage<3>(a, st); break;
+          default: rc = launch_stage<4>(a, st);
+        }
+        if (rc) return rc;
+        if (peers->n_ranks > 1) {
+          target += (unsigned int)peers->n_ranks;
+          peer_barrier_kernel<<<1, 1, 0, st>>>(pb, target, w.status);
+          CDK_CHECK_LAUNCH("peer_barrier_kernel");
+        }
+      }
+    }
+  } else if ((rc = launch_rk4_persistent(a, w, n_steps, dt, st, peers))) {
+    return rc;
+  }
+  advance_kernel<<<1, 1, 0, st>>>(w.status, n_steps);
+  CDK_CHECK_LAUNCH("advance_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_kuramoto_rk4_stage_peers(const cdk_graph *g, double *theta, const double *omega,
+                                            double k_over_n, double dt, int stage, void *workspace,
+                                            const cdk_peers *peers, void *stream) {
+  int rc = check_graph(g);
+  if (rc || (rc = check_peers(peers))) return rc;
+  if (stage < 1 || stage > 4) return set_error("stage must be 1..4"), CDK_INPUT;
+  cudaStream_t st = as_stream(stream);
+  Workspace w = carve(g, workspace, nullptr);
+  StageArgs a = base_args(g, w, theta, omega, k_over_n);
+  apply_peers(a, peers);
+  const int src = (stage - 1) & 1;
+  a.z_in = w.z[src]; a.z_out = w.z[src ^ 1];
+  a.part_in = w.part[src]; a.part_out = w.part[src ^ 1];
+  a.peer_out = reinterpret_cast<double2 *const *>(src ^ 1 ? peers->z1 : peers->z0);
+  a.step_rel = 0;
+  switch (stage) {
+    case 1: a.h = dt / 2.0; rc = launch_stage<1>(a, st); break;
+    case 2: a.h = dt / 2.0; rc = launch_stage<2>(a, st); break;
+    case 3: a.h = dt; rc = launch_stage<3>(a, st); break;
+    default: a.h = dt / 6.0; rc = launch_stage<4>(a, st);
+  }
+  if (rc) return rc;
+  if (peers->n_ranks > 1) {
+    PeerBar pb{peers->bar, w.peer_bar, peers->n_ranks, peers->wait};
+    peer_barrier_kernel<<<1, 1, 0, st>>>(pb, peers->bar_base + (unsigned int)peers->n_ranks,
+                                         w.status);
+    CDK_CHECK_LAUNCH("peer_barrier_kernel");
+  }
+  return CDK_OK;
+}

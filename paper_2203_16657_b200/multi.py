@@ -80,11 +80,47 @@ def exchange_slices(buf, ranges, rank: int, group=None) -> None:
         w.wait()
 
 
-def workspace_views(engine: KuramotoEngine):
-    """torch views [z0, z1] (float64 [n, 2]) of an engine's workspace."""
-    offs = (ctypes.c_int64 * 6)()
+def workspace_offsets(engine: KuramotoEngine) -> list[int]:
+    """byte offsets in an engine's workspace: z0 z1 ksum part0 part1 status peer_bar"""
+    offs = (ctypes.c_int64 * 7)()
     _lib.check(engine.lib.cdk_kuramoto_workspace_layout(ctypes.byref(engine.graph.struct), offs),
                "workspace_layout")
+    return [int(x) for x in offs]
+
+
+class PeerTable:
+    """Device pointer tables of the fused exchange (include/commdyn_cuda.h
+    cdk_peers): every rank's z[0], z[1] and peer-barrier counter.  ``bases``
+    are the workspace base addresses of all ranks as seen from this device
+    (own workspace, IPC-imported peers, or same-device virtual ranks)."""
+
+    def __init__(self, bases, offsets, rank: int, device, wait: bool):
+        """offsets[q]: rank q's workspace_offsets (layouts differ per rank:
+        the rblock partial arrays are sized by the rank's own rblocks)."""
+        import torch
+
+        n = len(bases)
+        z0 = [b + o[0] for b, o in zip(bases, offsets)]
+        z1 = [b + o[1] for b, o in zip(bases, offsets)]
+        bar = [b + o[6] for b, o in zip(bases, offsets)]
+        self._t = [torch.tensor(v, dtype=torch.int64, device=device) for v in (z0, z1, bar)]
+        self.struct = _lib.CdkPeers(n_ranks=n, rank=rank, z0=self._t[0].data_ptr(),
+                                    z1=self._t[1].data_ptr(), bar=self._t[2].data_ptr(),
+                                    bar_base=0, wait=1 if wait else 0)
+
+    def advance(self, n_stages: int) -> None:
+        """host-side counter bookkeeping: every stage adds n_ranks to each counter"""
+        self.struct.bar_base = (self.struct.bar_base + n_stages * self.struct.n_ranks) & 0xFFFFFFFF
+
+
+def zero_peer_counter(engine: KuramotoEngine) -> None:
+    o = workspace_offsets(engine)[6]
+    engine.workspace[o: o + 4].zero_()
+
+
+def workspace_views(engine: KuramotoEngine):
+    """torch views [z0, z1] (float64 [n, 2]) of an engine's workspace."""
+    offs = workspace_offsets(engine)
     n = engine.n
     ws = engine.workspace
     views = []
@@ -98,7 +134,8 @@ class ShardedKuramotoEngine:
     """One rank of a community-sharded Kuramoto CIA trajectory (NCCL exchange)."""
 
     def __init__(self, dec: Decomposition | None, omega, coupling: float, norm: float | None,
-                 rank: int, world: int, group=None, device=None, ranges=None, graph=None):
+                 rank: int, world: int, group=None, device=None, ranges=None, graph=None,
+                 p2p: bool = False):
         self.rank, self.world, self.group = rank, world, group
         self.ranges = ranges if ranges is not None else partition_rows(dec, world)
         lo, hi = self.ranges[rank]
@@ -106,9 +143,59 @@ class ShardedKuramotoEngine:
                                                                  row_range=(lo, hi))
         self.eng = KuramotoEngine(dec, omega, coupling=coupling, norm=norm, graph=self.graph)
         self.z = workspace_views(self.eng)
+        self.peers = None
+        if p2p and world > 1:
+            self.peers = self._open_peers_or_fallback()
+
+    def _open_peers_or_fallback(self):
+        """all ranks agree: fused exchange if every rank opened its peers,
+        otherwise the NCCL all-gather path for everyone"""
+        import torch
+        import torch.distributed as dist
+
+        try:
+            pt, ok = self._open_peers(), 1
+        except Exception as exc:  # noqa: BLE001 - any IPC/peer failure -> fallback
+            import sys
+
+            print(f"[rank {self.rank}] fused exchange unavailable: {exc}", file=sys.stderr)
+            pt, ok = None, 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.eng.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        return pt if int(flag.item()) == 1 else None
+
+    def _open_peers(self) -> PeerTable:
+        """Exchange CUDA IPC handles of every rank's workspace (one
+        all_gather_object), open the peers' and build the pointer tables of the
+        fused exchange (stage epilogues store into peers over NVLink)."""
+        import torch.distributed as dist
+
+        lib = self.eng.lib
+        ws = self.eng.workspace.data_ptr()
+        h = (ctypes.c_ubyte * 64)()
+        off = ctypes.c_uint64()
+        _lib.check(lib.cdk_ipc_export(ws, h, ctypes.byref(off)), "ipc_export")
+        mine = (bytes(h), int(off.value), workspace_offsets(self.eng))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=self.group)
+        bases, self._imported = [], []
+        for q, (hq, oq, _) in enumerate(allh):
+            if q == self.rank:
+                bases.append(ws)
+                continue
+            buf = (ctypes.c_ubyte * 64).from_buffer_copy(hq)
+            ptr = ctypes.c_void_p()
+            _lib.check(lib.cdk_ipc_import(buf, oq, ctypes.byref(ptr)), "ipc_import")
+            self._imported.append((ptr.value, oq))
+            bases.append(int(ptr.value))
+        zero_peer_counter(self.eng)
+        import torch
+
+        torch.cuda.synchronize()  # counter zeroed before the agreement all_reduce
+        return PeerTable(bases, [a[2] for a in allh], self.rank, self.eng.device, True)
 
     @classmethod
-    def generated(cls, case, rank: int, world: int, group=None, device=None):
+    def generated(cls, case, rank: int, world: int, group=None, device=None, p2p: bool = False):
         """One rank of a device-generated graph (config 5): the rank generates
         only its own rows (gen.generate(row_range=...))."""
         from . import gen
@@ -116,7 +203,8 @@ class ShardedKuramotoEngine:
         ranges = partition_by_cost(case.offsets(), case.n, case.row_costs(), world)
         dg, _ = gen.device_graph(case, device, row_range=ranges[rank])
         omega, _ = case.state()
-        return cls(None, omega, case.coupling, case.n, rank, world, group, device, ranges, dg)
+        return cls(None, omega, case.coupling, case.n, rank, world, group, device, ranges, dg,
+                   p2p=p2p)
 
     def _exchange(self, k: int, stream=None) -> None:
         exchange_slices(self.z[k], self.ranges, self.rank, self.group)
@@ -126,6 +214,14 @@ class ShardedKuramotoEngine:
         self._exchange(0)
 
     def rk4(self, dt: float, n_steps: int, stream=None) -> None:
+        if self.peers is not None:  # fused exchange: one persistent launch, NVLink stores
+            e = self.eng
+            _lib.check(e.lib.cdk_kuramoto_rk4_peers(
+                ctypes.byref(self.graph.struct), e.theta.data_ptr(), e.omega.data_ptr(),
+                e.k_over_n, float(dt), int(n_steps), e.workspace.data_ptr(),
+                ctypes.byref(self.peers.struct), _lib.stream_ptr(stream)), "rk4_peers")
+            self.peers.advance(4 * int(n_steps))
+            return
         for _ in range(int(n_steps)):
             for s in range(1, 5):
                 self.eng.rk4_stage(dt, s, stream=stream)
@@ -142,6 +238,9 @@ class ShardedKuramotoEngine:
 
     def check(self) -> None:
         self.eng.check()
+        if self.peers is not None and self.eng.status().reserved:
+            raise RuntimeError("fused exchange: peer barrier watchdog fired "
+                               "(a rank stopped responding)")
 
 
 class VirtualCluster:
@@ -150,7 +249,7 @@ class VirtualCluster:
     path (for bitwise-equality tests without several GPUs)."""
 
     def __init__(self, dec: Decomposition | None, omega, coupling: float, norm: float | None,
-                 world: int, device=None, graphs=None, ranges=None):
+                 world: int, device=None, graphs=None, ranges=None, p2p: bool = False):
         self.ranges = ranges if ranges is not None else partition_rows(dec, world)
         self.ranks = []
         for r in range(world):
@@ -158,9 +257,19 @@ class VirtualCluster:
                  else DeviceGraph(dec, device=device, row_range=self.ranges[r]))
             e = KuramotoEngine(dec, omega, coupling=coupling, norm=norm, graph=g)
             self.ranks.append((e, workspace_views(e)))
+        # fused exchange on one device: every virtual rank's epilogue stores into
+        # the others' workspaces (signal-only barrier: ranks run one after another)
+        self.peers = None
+        if p2p and world > 1:
+            bases = [e.workspace.data_ptr() for e, _ in self.ranks]
+            offs = [workspace_offsets(e) for e, _ in self.ranks]
+            for e, _ in self.ranks:
+                zero_peer_counter(e)
+            self.peers = [PeerTable(bases, offs, r, self.ranks[r][0].device, False)
+                          for r in range(world)]
 
     @classmethod
-    def generated(cls, case, world: int, device=None, smem_budget=None):
+    def generated(cls, case, world: int, device=None, smem_budget=None, p2p: bool = False):
         """Every rank of a sharded device-generated graph on one device."""
         from . import gen
 
@@ -168,7 +277,7 @@ class VirtualCluster:
         graphs = [gen.device_graph(case, device, smem_budget=smem_budget, row_range=rr)[0]
                   for rr in ranges]
         omega, _ = case.state()
-        return cls(None, omega, case.coupling, case.n, world, device, graphs, ranges)
+        return cls(None, omega, case.coupling, case.n, world, device, graphs, ranges, p2p=p2p)
 
     def _exchange(self, k: int) -> None:
         for r, (lo, hi) in enumerate(self.ranges):
@@ -185,9 +294,17 @@ class VirtualCluster:
     def rk4(self, dt: float, n_steps: int) -> None:
         for _ in range(int(n_steps)):
             for s in range(1, 5):
-                for e, _ in self.ranks:
-                    e.rk4_stage(dt, s)
-                self._exchange(s & 1)
+                if self.peers is not None:
+                    for (e, _), pt in zip(self.ranks, self.peers):
+                        _lib.check(e.lib.cdk_kuramoto_rk4_stage_peers(
+                            ctypes.byref(e.graph.struct), e.theta.data_ptr(), e.omega.data_ptr(),
+                            e.k_over_n, float(dt), s, e.workspace.data_ptr(),
+                            ctypes.byref(pt.struct), None), "rk4_stage_peers")
+                        pt.advance(1)
+                else:
+                    for e, _ in self.ranks:
+                        e.rk4_stage(dt, s)
+                    self._exchange(s & 1)
 
     def theta(self):
         import torch
@@ -227,10 +344,15 @@ def bench_main(args):
     from bench import METRIC, UNIT, ClockSampler, _peaks, algorithmic_bytes_per_rhs  # noqa: E402
 
     cfg = getattr(args, "config", "cfg2")
+    # fused exchange (NVLink P2P stores + peer barrier) when every peer is
+    # reachable; CDK_P2P=0 falls back to the NCCL all-gather after each stage
+    p2p = os.environ.get("CDK_P2P", "1") != "0" and world > 1 and all(
+        torch.cuda.can_device_access_peer(local, q) for q in range(torch.cuda.device_count())
+        if q != local)
     if cfg == "cfg5":
         case = gen.config5()
         omega, theta0 = case.state()
-        eng = ShardedKuramotoEngine.generated(case, rank, world)
+        eng = ShardedKuramotoEngine.generated(case, rank, world, p2p=p2p)
         nnz_local = eng.graph.layout.nnz_dir
         workload = ("cfg5 Kuramoto CIA RK4, LFR-style N=8000000 (device-generated, each rank its "
                     "own rows), sharded by community")
@@ -239,7 +361,7 @@ def bench_main(args):
         case = configs.config2()
         dec = case.decomposition()
         omega, theta0 = case.state()
-        eng = ShardedKuramotoEngine(dec, omega, case.coupling, case.n, rank, world)
+        eng = ShardedKuramotoEngine(dec, omega, case.coupling, case.n, rank, world, p2p=p2p)
         nnz_local = eng.graph.layout.nnz_dir
         workload = "cfg2 Kuramoto CIA RK4, SBM N=200000, sharded by community"
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -294,7 +416,9 @@ def bench_main(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "n_nodes": case.n, "nnz_dir": nnz,
-                       "parallelism": f"community shards x{world} (NCCL all-gather of z per stage)",
+                       "parallelism": f"community shards x{world} " + (
+                           "(fused exchange: epilogue NVLink P2P stores + peer barrier)"
+                           if eng.peers is not None else "(NCCL all-gather of z per stage)"),
                        "l2": "flushed before every timed step" if flush is not None
                        else "inputs >> L2", "ranges": eng.ranges},
             "roofline": {"bound": "hbm", "achieved": b_rhs / world / (stage_ms / 1e3) / 1e9,
