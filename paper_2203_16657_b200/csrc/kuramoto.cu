@@ -93,8 +93,7 @@ struct StageArgs {
   int sweep_mode;  // inter sweep lanes/unroll variant (CDK_SWEEP, experiments)
   int debug_flags; // CDK_DEBUG_FLAGS (timing experiments only; results invalid):
                    // 1 = skip the inter sweep, 2 = skip the segments,
-                   // 4 = drop inline inter entries, 8 = drop intra gathers,
-                   // 32 = intra column chunks re-read from one cached line
+                   // 4 = drop inline inter entries, 8 = drop intra gathers
   double k_over_n;
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
@@ -336,11 +335,10 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
       }
     }
   };
-  const int cmask = (a.debug_flags & 32) ? 7 : 0x7FFFFFFF;  // timing experiment only
   auto stage_data = [&](int r, RowPipe &R) {
     if (r < nrows) {
-      R.c0 = (R.p < R.e1) ? ldg(colv + ((R.p >> 3) & cmask)) : padv;
-      R.c1 = (R.p + STRIDE < R.e1) ? ldg(colv + (((R.p + STRIDE) >> 3) & cmask)) : padv;
+      R.c0 = (R.p < R.e1) ? ldg(colv + (R.p >> 3)) : padv;
+      R.c1 = (R.p + STRIDE < R.e1) ? ldg(colv + ((R.p + STRIDE) >> 3)) : padv;
       if (!sxc) R.z = (R.j >= 0) ? ldz(z_in + R.j) : make_double2(0.0, 0.0);
     }
   };
@@ -357,7 +355,7 @@ __device__ __forceinline__ void gather_phase(const StageArgs &a, const SegSmem &
       if (A.p < A.e1) gather8_smem(A.c0, zs_addr, zero_slot, sr, si);  // skip all-pad chunks
       if (A.p + STRIDE < A.e1) gather8_smem(A.c1, zs_addr, zero_slot, sr, si);
       for (int p = A.p + 2 * STRIDE; p < A.e1; p += STRIDE)
-        gather8_smem(ldg(colv + ((p >> 3) & cmask)), zs_addr, zero_slot, sr, si);
+        gather8_smem(ldg(colv + (p >> 3)), zs_addr, zero_slot, sr, si);
     } else {
       gather8_global(A.c0, zglob, sr, si);
       gather8_global(A.c1, zglob, sr, si);
