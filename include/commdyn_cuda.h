@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 11
+#define CDK_ABI_VERSION 12
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -148,8 +148,31 @@ typedef struct cdk_graph {
    * shared memory with the window, so the row pipeline reads inter columns
    * from shared memory and issues the z gathers two rows ahead.  0 = off. */
   int32_t xs_cap;               /* multiple of 16 */
-  int32_t reserved0;
+  int32_t n_ell_parts;          /* ELL split rblocks: partial-sum slots (see ell_units) */
   const int64_t *seg_xr;        /* [2*n_seg] inter_ptr at the segment's first/last row, or NULL */
+  /* Lane-per-row sliced layout ("ELL"; cdk_host_ell_intra).  When ell_off is
+   * set the stage kernels run one warp per rblock, lane = row: the rblock's
+   * intra chunks are ell_col[(ell_off[b] + 32 c + lane) * 8 .. +8) for
+   * c < (ell_off[b+1] - ell_off[b]) / 32 (columns relative to seg_base, as
+   * intra_col; staged pads point at zero slots smem_nodes + g), its inter
+   * columns xell_col[xell_off[b] + 32 k + lane] for k < (xell_off[b+1] -
+   * xell_off[b]) / 32 (global, -1 = none).  cta_threads must then equal
+   * cdk_kuramoto_ell_threads(); requires inter_blocks == 0 and no
+   * intra_split (communities wider than the window gather from global). */
+  const int64_t *ell_off;       /* [n_rblk+1] uint4 units, or NULL */
+  const uint16_t *ell_col;
+  const int64_t *xell_off;      /* [n_rblk+1] int32 units */
+  const int32_t *xell_col;
+  /* ELL work units: warps of segment s claim units seg_unit[s] ..
+   * seg_unit[s+1]-1 in order; unit u = rblock ell_units[2u], part
+   * q = ell_units[2u+1] & 0xFFFF of P = ell_units[2u+1] >> 16 (chunks
+   * [q nch / P, (q+1) nch / P); inter entries in part 0).  Parts of a split
+   * rblock (P > 1) meet in partial-sum slots ell_part_base[b] + q of the
+   * workspace; the last to arrive adds them in part order and runs the
+   * epilogue.  P depends on the rblock only (deterministic on every shard). */
+  const int32_t *ell_units;     /* [2 * n_units] */
+  const int32_t *seg_unit;      /* [n_seg+1] */
+  const int32_t *ell_part_base; /* [n_rblk], -1 = not split */
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */
@@ -192,6 +215,13 @@ CDK_API int cdk_ipc_close(void *ptr, uint64_t offset);
 
 /* threads per CTA of the stage kernels (cdk_graph.cta_threads must match) */
 CDK_API int cdk_kuramoto_stage_threads(void);
+/* resident stage CTAs per SM the library was built for (the planner launches
+ * SMs x this many persistent CTAs and sizes their shared memory to match) */
+CDK_API int cdk_kuramoto_stage_ctas_per_sm(void);
+/* threads per CTA of the ELL stage kernels (graphs with ell_off set) */
+CDK_API int cdk_kuramoto_ell_threads(void);
+/* node capacity of the ELL kernels' shared-memory window (zero slots follow) */
+CDK_API int cdk_kuramoto_ell_window_nodes(void);
 
 /* bytes of device workspace the fused Kuramoto path needs for graph g */
 CDK_API size_t cdk_kuramoto_workspace_bytes(const cdk_graph *g);
@@ -378,6 +408,18 @@ CDK_API int cdk_inter_split(int64_t n_rows, const int64_t *ptr, const int32_t *c
  * groups (column mod 8); pads (pad_value) count as bank pad_bank. */
 CDK_API int cdk_host_bank_order(uint16_t *cols, const int64_t *ptr, int64_t n_rows,
                                 int32_t pad_value, int32_t pad_bank);
+
+/* [host] ELL intra layout (cdk_graph.ell_off/ell_col): per rblock, the rows'
+ * runs (ptr/cols as intra_ptr/intra_col, pads skipped) scheduled so each
+ * quarter-warp step hits 8 distinct bank groups.  staged[b] != 0: pads point
+ * at zero slot zero_slot + bank group; else CDK_INTRA_PAD.  Bank group of a
+ * column v of rblock b: (v + bank_shift[b]) mod 8 (NULL: 0).  ell == NULL:
+ * writes ell_off only (sizes); then call again with ell sized
+ * 8 * ell_off[n_rblk] uint16. */
+CDK_API int cdk_host_ell_intra(const int64_t *rblk_row0, int32_t n_rblk, const int64_t *ptr,
+                               const uint16_t *cols, const uint8_t *staged,
+                               const uint8_t *bank_shift, int32_t zero_slot, int64_t *ell_off,
+                               uint16_t *ell);
 
 /* [host] triangles {i<j<k} of a symmetric CSR (sorted global columns, no
  * self loops); writes <= cap int32 triples to out (NULL ok), returns the count

@@ -50,8 +50,15 @@ class CdkGraph(ctypes.Structure):
         ("inter_block_nodes", I32),
         ("inter_split", P),
         ("xs_cap", I32),
-        ("reserved0", I32),
+        ("n_ell_parts", I32),
         ("seg_xr", P),
+        ("ell_off", P),
+        ("ell_col", P),
+        ("xell_off", P),
+        ("xell_col", P),
+        ("ell_units", P),
+        ("seg_unit", P),
+        ("ell_part_base", P),
     ]
 
 
@@ -126,6 +133,7 @@ class CdkRunStatus(ctypes.Structure):
 # name -> argtypes (restype int unless listed in _RESTYPES)
 _SIGS = {
     "cdk_kuramoto_stage_threads": [],
+    "cdk_kuramoto_stage_ctas_per_sm": [],
     "cdk_order_params_blocks": [P, P, I64, I, D, D, P, P],
     "cdk_dense_complex": [P, P, I64, P, I, D, P, P, P],
     "cdk_dense_real": [P, P, I64, P, P, I, D, P, P],
@@ -143,6 +151,9 @@ _SIGS = {
     "cdk_kuramoto_euler": [ctypes.POINTER(CdkGraph), P, P, D, D, I64, P, P],
     "cdk_kuramoto_status": [ctypes.POINTER(CdkGraph), P, ctypes.POINTER(CdkRunStatus), P],
     "cdk_host_bank_order": [P, P, I64, I32, I32],
+    "cdk_host_ell_intra": [P, I32, P, P, P, P, I32, P, P],
+    "cdk_kuramoto_ell_threads": [],
+    "cdk_kuramoto_ell_window_nodes": [],
     "cdk_debug_set_profile_buffer": [P],
     "cdk_host_triangles": [P, P, I64, P, I64],
     "cdk_ho_workspace_bytes": [ctypes.POINTER(CdkHoGraph)],
@@ -188,7 +199,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 _lock = threading.Lock()
 _lib = None

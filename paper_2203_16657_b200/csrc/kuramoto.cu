@@ -46,6 +46,8 @@ struct Workspace {
   unsigned int *bar;  // grid-barrier counter of the persistent kernel
   double2 *xacc;      // per-row inter sums (block-phased inter sweep only)
   unsigned int *peer_bar;  // fused multi-GPU exchange: this rank's barrier counter
+  double2 *ell_part;  // ELL split rblocks: partial sums [n_ell_parts][32]
+  int *ell_cnt;       // ELL split rblocks: arrival counters [n_rblk] (zero between stages)
 };
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -70,6 +72,9 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
   w.bar = (unsigned int *)take(256);
   w.xacc = g->inter_blocks > 0 ? (double2 *)take(n * sizeof(double2)) : nullptr;
   w.peer_bar = (unsigned int *)take(256);
+  w.ell_part = g->n_ell_parts > 0 ? (double2 *)take((size_t)g->n_ell_parts * 32 * sizeof(double2))
+                                  : nullptr;
+  w.ell_cnt = g->n_ell_parts > 0 ? (int *)take(((size_t)g->n_rblk + 1) * sizeof(int)) : nullptr;
   if (total) *total = off;
   return w;
 }
@@ -98,6 +103,8 @@ struct StageArgs {
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
   unsigned long long *prof;  // CDK_PROFILE builds: per-CTA phase cycles
+  double2 *ell_part;  // Workspace::ell_part / ell_cnt
+  int *ell_cnt;
 };
 
 // Canonical community sum R_c of the rblock partials: 8 lanes, lane t sums
@@ -229,6 +236,9 @@ __device__ __forceinline__ void gather8_global(const uint4 w, const double2 *__r
 // ---------------------------------------------------------------------------
 #ifndef CDK_STAGE_THREADS
 #define CDK_STAGE_THREADS 896  // measured: 896 ~ 768 > 640 > 1024 threads (register room)
+#endif
+#ifndef CDK_STAGE_MINBLOCKS
+#define CDK_STAGE_MINBLOCKS 1  // resident stage CTAs per SM the build targets
 #endif
 constexpr int NTHREADS = CDK_STAGE_THREADS;
 constexpr int NWARPS = NTHREADS / 32;
@@ -864,7 +874,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) inter_sweep_kernel(const Sta
 
 // single stage launch (MODE 0: RHS, 1..4: RK4 stage, 5: Euler)
 template <int MODE>
-__global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const StageArgs a) {
+__global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_stage_kernel(const StageArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar_seg, bar_epi;
   __shared__ double2 sR[SEG_MAX_COMM];
@@ -875,15 +885,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_stage_kernel(const Stage
 #ifdef CDK_PROFILE
   pa.t_mark = clock64();
   const unsigned long long t_begin = pa.t_mark;
+  unsigned long long g_begin;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_begin));
 #endif
   stage_body<MODE>(a, sm, bar_seg, bar_epi, sR, parity, pa);
 #ifdef CDK_PROFILE
   if (threadIdx.x == 0 && a.prof) {
-    unsigned long long *p = a.prof + 4 * blockIdx.x;
+    unsigned long long *p = a.prof + 6 * blockIdx.x;
     p[0] = clock64() - t_begin;
     p[1] = pa.t_stage;
     p[2] = pa.t_gather;
     p[3] = pa.t_epi;
+    unsigned long long g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    p[4] = g_begin;  // ns: launch skew and tail across CTAs
+    p[5] = g_end;
   }
 #endif
 }
@@ -954,7 +970,7 @@ struct StepPtrs {
 // between stages (no launch gaps; the CSR slices and window reloads are the
 // only per-stage traffic).
 template <bool PEERS>
-__global__ void __launch_bounds__(NTHREADS, 1) kuramoto_rk4_kernel(StageArgs a, StepPtrs ptr,
+__global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_kernel(StageArgs a, StepPtrs ptr,
                                                                    int64_t n_steps, double dt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar_seg, bar_epi;
@@ -1000,6 +1016,467 @@ __global__ void __launch_bounds__(NTHREADS, 1) kuramoto_rk4_kernel(StageArgs a, 
     a.h = h6;
     stage_body<4>(a, sm, bar_seg, bar_epi, sR, parity, pa);
     CDK_STAGE_SYNC(step + 1 == n_steps);
+  }
+#undef CDK_STAGE_SYNC
+}
+
+// ===========================================================================
+// ELL stage kernels (cdk_graph.ell_off set; layout: cdk_host_ell_intra).
+// One warp per rblock, lane = row, persistent CTAs over the same segments as
+// the kernels above.  Per segment: one bulk copy (TMA engine) stages the
+// window of z_in, the segment's chunk and inter-column ranges are prefetched
+// into L2, and each 8-lane group reduces one community's R_c from the
+// previous stage's rblock partials.  Warps then claim rblocks (shared
+// counter); per rblock every lane streams its row's 16-byte chunks (8 uint16
+// columns, 512 contiguous bytes per warp per chunk, two chunks in flight) and
+// gathers z from the window — the layout schedules each quarter-warp step
+// onto 8 distinct bank groups, padding included (zero slots per bank group),
+// so every LDS.128 is 4 wavefronts — sums its inter columns (global z, the
+// first four issued before the intra loop), and runs the same epilogue as
+// above (same arithmetic, lane = row).  No row reductions, no per-row
+// pointers, no barrier between gathers and epilogue.  Accumulation order is
+// fixed by the layout: deterministic and independent of the CTA schedule.
+// ===========================================================================
+#ifndef CDK_ELL_THREADS
+#define CDK_ELL_THREADS 640
+#endif
+#ifndef CDK_ELL_WINDOW
+#define CDK_ELL_WINDOW 14336  // nodes: (14336 + 8) * 16 B = 224 KB of window + zero slots
+#endif
+#ifndef CDK_ELL_DEPTH
+#define CDK_ELL_DEPTH 4  // 16-byte chunks per lane in flight ahead of the gathers
+#endif
+#ifndef CDK_ELL_XUNIT
+#define CDK_ELL_XUNIT 0  // 1: chunk queue runs across a warp's consecutive work units (slower)
+#endif
+#ifndef CDK_ELL_RK4_RT
+#define CDK_ELL_RK4_RT 1  // persistent RK4: one stage body with a runtime mode (0: four inlined)
+#endif
+constexpr int ELL_THREADS = CDK_ELL_THREADS;
+constexpr int ELL_DEPTH = CDK_ELL_DEPTH;
+constexpr int ELL_WARPS = ELL_THREADS / 32;
+constexpr int ELL_GROUPS = ELL_THREADS / 8;
+
+__host__ __device__ inline size_t ell_smem_bytes(int smem_nodes) {
+  return ((size_t)smem_nodes + 8) * 16;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p, uint64_t bytes) {
+  // cp.async.bulk.prefetch.L2: 16-byte granules, issued in <= 64 KB pieces
+  uint64_t a = reinterpret_cast<uint64_t>(p) & ~(uint64_t)15;
+  const uint64_t end = reinterpret_cast<uint64_t>(p) + bytes;
+  while (a < end) {
+    const uint64_t left = (end - a + 15) & ~(uint64_t)15;
+    const uint32_t n = (uint32_t)(left < 65536 ? left : 65536);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    a += n;
+  }
+}
+
+// 8 entries of one chunk from the window: unconditional (pads hit zero slots)
+__device__ __forceinline__ void ell_gather8_smem(const uint4 w, uint32_t zs_addr, double &ar,
+                                                 double &ai, double &br, double &bi) {
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  double2 z[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+    z[k] = lds_d2(zs_addr + (u << 4));
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    ar += z[k].x;
+    ai += z[k].y;
+    br += z[k + 1].x;
+    bi += z[k + 1].y;
+  }
+}
+
+// unstaged rblocks (community wider than the window): global gathers, pads skipped
+__device__ __forceinline__ void ell_gather8_global(const uint4 w, const double2 *__restrict__ zb,
+                                                   double &ar, double &ai, double &br,
+                                                   double &bi) {
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+    if (u != CDK_INTRA_PAD) {
+      const double2 z = ldz(zb + u);
+      if (k & 1) {
+        br += z.x;
+        bi += z.y;
+      } else {
+        ar += z.x;
+        ai += z.y;
+      }
+    }
+  }
+}
+
+// per-stage values (the kernel parameter StageArgs stays untouched, so the
+// persistent kernel reads the graph from the parameter bank, not a local copy)
+struct StageVar {
+  const double2 *z_in;
+  double2 *z_out;
+  const double2 *part_in;
+  double2 *part_out;
+  double2 *const *peer_out;
+  double h;
+  int64_t step_rel;
+  __device__ static StageVar of(const StageArgs &a) {
+    return StageVar{a.z_in, a.z_out, a.part_in, a.part_out, a.peer_out, a.h, a.step_rel};
+  }
+};
+
+// chunk stream of work unit u (this lane's column): first chunk, chunk count
+struct UnitChunks {
+  const uint4 *cp;
+  int nch;
+};
+__device__ __forceinline__ UnitChunks unit_chunks(const cdk_graph &g, int u, int lane) {
+  const int rb = g.ell_units[2 * u], code = g.ell_units[2 * u + 1];
+  const int part = code & 0xFFFF, nparts = code >> 16;
+  const int nch_rb = (int)((g.ell_off[rb + 1] - g.ell_off[rb]) >> 5);
+  const int ch0 = nch_rb * part / nparts, ch1 = nch_rb * (part + 1) / nparts;
+  UnitChunks r;
+  r.cp = reinterpret_cast<const uint4 *>(g.ell_col) + g.ell_off[rb] + 32 * (int64_t)ch0 + lane;
+  r.nch = ch1 - ch0;
+  return r;
+}
+
+// One work unit (an rblock, or one part of a split rblock).  The warp's chunk
+// queue cq runs across units: while the last chunks of this unit are
+// gathered, the first chunks of the warp's next unit (nx_u, claimed at the
+// start of this one) are already loading, so no unit starts with an empty
+// pipeline.  On entry cq[d] holds chunk d of this unit for d >= need (the
+// prefix was not known when the previous unit refilled); on exit `need` is
+// the next unit's invalid prefix.
+template <bool STAGED>
+__device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, const StageVar &v,
+                                           int rb,
+                                           int part, int nparts,
+                                           uint32_t zs_addr, const double2 *zs, int64_t w0,
+                                           const double2 *__restrict__ zglob, double2 R,
+                                           uint4 (&cq)[ELL_DEPTH], int &need,
+                                           const UnitChunks &uc, const UnitChunks &nx_u) {
+  const cdk_graph &g = a.g;
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = g.rblk_row0[rb], r1 = g.rblk_row0[rb + 1];
+  const int64_t i = r0 + lane;
+  const bool valid = i < r1;
+  const int64_t x0 = g.xell_off[rb];
+  // this unit's chunks (part of a split rblock) and inter entries (part 0)
+  const int nch = uc.nch;
+  const int nx = (part == 0) ? (int)((g.xell_off[rb + 1] - x0) >> 5) : 0;
+  // epilogue inputs: in flight during the gathers
+  double om = 0.0, th0 = 0.0, ks0 = 0.0;
+  if (valid) {
+    om = a.omega[i];
+    if (MODE != 0) th0 = a.theta[i];
+    if (MODE >= 2 && MODE <= 4) ks0 = a.ksum[i];
+  }
+  // first four inter gathers (L2) issued before the intra loop
+  const int32_t *__restrict__ xc = g.xell_col + x0 + lane;
+  const double2 *__restrict__ z_in = v.z_in;
+  int jx[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) jx[q] = (q < nx) ? ldg(xc + 32 * q) : -1;
+  double2 xz[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) xz[q] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
+  // intra chunks: ELL_DEPTH in flight ahead of the one being gathered
+  const uint4 *__restrict__ cp = uc.cp;
+  const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+  for (int d = 0; d < ELL_DEPTH; ++d)
+    if (d < need && d < nch) cq[d] = ldg(cp + 32 * d);
+  need = ELL_DEPTH - nch > 0 ? ELL_DEPTH - nch : 0;
+  double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    const uint4 w = cq[0];
+#pragma unroll
+    for (int d = 0; d + 1 < ELL_DEPTH; ++d) cq[d] = cq[d + 1];
+    const int t = c + ELL_DEPTH;
+    cq[ELL_DEPTH - 1] = (t < nch) ? ldg(cp + 32 * t)
+                        : (t - nch < nx_u.nch) ? ldg(nx_u.cp + 32 * (t - nch)) : padv;
+    if (STAGED) {
+      ell_gather8_smem(w, zs_addr, ar, ai, br, bi);
+    } else {
+      ell_gather8_global(w, zglob, ar, ai, br, bi);
+    }
+  }
+  double sr = -(ar + br), si = -(ai + bi);  // intra-missing entries: sign -1
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    sr += xz[q].x;
+    si += xz[q].y;
+  }
+  for (int k = 4; k < nx; k += 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) jx[q] = (k + q < nx) ? ldg(xc + 32 * (k + q)) : -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      xz[q] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      sr += xz[q].x;
+      si += xz[q].y;
+    }
+  }
+  if (nparts > 1) {  // split rblock: publish the partial; the last part finishes
+    const int64_t base = (int64_t)g.ell_part_base[rb] * 32 + lane;
+    __stcg(a.ell_part + base + 32 * part, make_double2(sr, si));
+    __threadfence();
+    int old = 0;
+    if (lane == 0) old = atomicAdd(a.ell_cnt + rb, 1);
+    old = __shfl_sync(FULL, old, 0);
+    if (old != nparts - 1) return;
+    __threadfence();
+    const double2 own = make_double2(sr, si);
+    sr = 0.0;
+    si = 0.0;
+    for (int q = 0; q < nparts; ++q) {  // fixed part order
+      const double2 v = (q == part) ? own : ldcg2(a.ell_part + base + 32 * q);
+      sr += v.x;
+      si += v.y;
+    }
+    if (lane == 0) a.ell_cnt[rb] = 0;  // ready for the next stage
+  }
+  // epilogue (same arithmetic as stage_body's)
+  double zr = 0.0, zim = 0.0;
+  if (valid) {
+    const double2 zi = STAGED ? zs[i - w0] : ldz(z_in + i);
+    const double kn = a.k_over_n;
+    double k = om + kn * (R.y * zi.x - R.x * zi.y);
+    k = k + kn * (si * zi.x - sr * zi.y);
+    if (MODE == 0) {
+      a.out[i] = k;
+    } else {
+      double thn;
+      if (MODE == 1) {
+        a.ksum[i] = k;
+        thn = add_rn(th0, mul_rn(v.h, k));
+      } else if (MODE == 2 || MODE == 3) {
+        a.ksum[i] = add_rn(ks0, mul_rn(2.0, k));
+        thn = add_rn(th0, mul_rn(v.h, k));
+      } else {
+        const double ks = (MODE == 4) ? add_rn(ks0, k) : k;
+        thn = wrap_phase(add_rn(th0, mul_rn(v.h, ks)));
+        a.theta[i] = thn;
+        if (!isfinite(thn)) {
+          atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->nonfinite), 1ull);
+          atomicMin(reinterpret_cast<long long *>(&a.status->first_bad_step),
+                    (long long)(a.status->steps_done + v.step_rel + 1));
+        }
+      }
+      sincos(thn, &zim, &zr);
+      const double2 zn = make_double2(zr, zim);
+      v.z_out[i] = zn;
+      for (int q = 0; q < a.n_peers; ++q)  // NVLink P2P stores (fused all-gather)
+        if (q != a.rank) v.peer_out[q][i] = zn;
+    }
+  }
+  if (MODE != 0) {  // canonical rblock partial (same shape as stage_body's)
+    const double r8 = __shfl_down_sync(FULL, zr, 8), i8 = __shfl_down_sync(FULL, zim, 8);
+    const double r16 = __shfl_down_sync(FULL, zr, 16), i16 = __shfl_down_sync(FULL, zim, 16);
+    const double r24 = __shfl_down_sync(FULL, zr, 24), i24 = __shfl_down_sync(FULL, zim, 24);
+    double pr = ((zr + r8) + r16) + r24, pim = ((zim + i8) + i16) + i24;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      pr += __shfl_xor_sync(FULL, pr, o);
+      pim += __shfl_xor_sync(FULL, pim, o);
+    }
+    if (lane == 0) v.part_out[rb] = make_double2(pr, pim);
+  }
+}
+
+struct EllSmem {
+  double2 *zs;  // [smem_nodes + 8]: window, then one zero slot per bank group
+  uint64_t *bar;
+  double2 *sR;  // [SEG_MAX_COMM]
+  int *next;    // rblock claim counter
+};
+
+// MODE: 0 RHS, 1..4 RK4 stage, 5 Euler (a runtime value: constant-folded in
+// the per-stage kernels, one uniform branch per row in the persistent one)
+__device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, const StageVar &v,
+                                         const EllSmem &sm, uint32_t &phase) {
+  const cdk_graph &g = a.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t = lane & 7, grp = tid >> 3;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  const int segA = g.cta_seg[blockIdx.x], segB = g.cta_seg[blockIdx.x + 1];
+  const uint32_t zs_addr = smem_u32(sm.zs);
+  for (int s = segA; s < segB; ++s) {
+    const int rbA = g.seg_rblk[s], rbB = g.seg_rblk[s + 1];
+    const int64_t w0 = g.seg_win[2 * s], w1 = g.seg_win[2 * s + 1];
+    const bool staged = w1 > w0;
+    const int cA = g.rblk_comm[rbA];
+    if (tid == 0) {
+      fence_proxy_async_smem();  // earlier generic accesses before the async overwrite
+      if (staged) {
+        const uint32_t bw = (uint32_t)((w1 - w0) * 16);
+        mbar_expect_tx(sm.bar, bw);
+        bulk_g2s(sm.zs, v.z_in + w0, bw, sm.bar);
+      }
+      const int64_t eA = g.ell_off[rbA], eB = g.ell_off[rbB];
+      prefetch_l2(g.ell_col + 8 * eA, (uint64_t)(eB - eA) * 16);
+      const int64_t xA = g.xell_off[rbA], xB = g.xell_off[rbB];
+      prefetch_l2(g.xell_col + xA, (uint64_t)(xB - xA) * 4);
+      *sm.next = g.seg_unit[s] + ELL_WARPS;
+    }
+    if (cA >= 0) {  // community observables of the segment (canonical order)
+      const int cB = g.rblk_comm[rbB - 1];
+      const int cLast = cB >= 0 ? cB : (int)g.n_comm - 1;
+      for (int q = grp; q < cLast - cA + 1; q += ELL_GROUPS) {
+        const int c = cA + q;
+        const double2 Rc = reduce_comm8(v.part_in, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], t,
+                                        gmask);
+        if (t == 0) sm.sR[q] = Rc;
+      }
+    }
+    __syncthreads();
+    if (staged) {
+      mbar_wait(sm.bar, phase);
+      phase ^= 1u;
+    }
+    const double2 *zglob = v.z_in + g.seg_base[s];
+    const int uB = g.seg_unit[s + 1];
+    int u = g.seg_unit[s] + warp;
+    uint4 cq[ELL_DEPTH];
+    int need = ELL_DEPTH;
+    UnitChunks uc{nullptr, 0};
+    if (u < uB) uc = unit_chunks(g, u, lane);
+    while (u < uB) {
+      UnitChunks nu{nullptr, 0};
+#if CDK_ELL_XUNIT
+      int nxt = 0;  // claim the next unit first: its chunks stream in behind this one's
+      if (lane == 0) nxt = atomicAdd(sm.next, 1);
+      nxt = __shfl_sync(FULL, nxt, 0);
+      if (nxt < uB) nu = unit_chunks(g, nxt, lane);
+#endif
+      const int rb = g.ell_units[2 * u], code = g.ell_units[2 * u + 1];
+      const int c = g.rblk_comm[rb];
+      const double2 R = (c >= 0) ? sm.sR[c - cA] : make_double2(0.0, 0.0);
+      if (staged) {
+        ell_rblock<true>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob, R,
+                               cq, need, uc, nu);
+      } else {
+        ell_rblock<false>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob, R,
+                                cq, need, uc, nu);
+      }
+#if !CDK_ELL_XUNIT
+      int nxt = 0;
+      if (lane == 0) nxt = atomicAdd(sm.next, 1);
+      nxt = __shfl_sync(FULL, nxt, 0);
+      if (nxt < uB) nu = unit_chunks(g, nxt, lane);
+      need = ELL_DEPTH;
+#endif
+      u = nxt;
+      uc = nu;
+    }
+    __syncthreads();  // window and counters reused by the next segment
+  }
+  if (a.n_peers > 1) __threadfence_system();  // peer stores before the barrier signal
+}
+
+__device__ __forceinline__ EllSmem ell_init(unsigned char *smem_raw, uint64_t *bar, double2 *sR,
+                                            int *next, int smem_nodes) {
+  EllSmem sm;
+  sm.zs = reinterpret_cast<double2 *>(smem_raw);
+  sm.bar = bar;
+  sm.sR = sR;
+  sm.next = next;
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  if (threadIdx.x < 8) sm.zs[smem_nodes + threadIdx.x] = make_double2(0.0, 0.0);
+  __syncthreads();
+  return sm;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(ELL_THREADS, 1) ell_stage_kernel(const StageArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double2 sR[SEG_MAX_COMM];
+  __shared__ int next;
+  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, a.g.smem_nodes);
+  uint32_t phase = 0;
+#ifdef CDK_PROFILE
+  const unsigned long long t_begin = clock64();
+  unsigned long long g_begin;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_begin));
+#endif
+  ell_body(MODE, a, StageVar::of(a), sm, phase);
+#ifdef CDK_PROFILE
+  __syncthreads();
+  if (threadIdx.x == 0 && a.prof) {
+    unsigned long long *p = a.prof + 6 * blockIdx.x;
+    p[0] = clock64() - t_begin;
+    p[1] = p[2] = p[3] = 0;
+    unsigned long long g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    p[4] = g_begin;
+    p[5] = g_end;
+  }
+#endif
+}
+
+// Persistent RK4 over the ELL layout (cooperative launch, grid barrier
+// between stages; same sequencing as kuramoto_rk4_kernel).
+template <bool PEERS>
+__global__ void __launch_bounds__(ELL_THREADS, 1) ell_rk4_kernel(const __grid_constant__ StageArgs a,
+                                                                 StepPtrs ptr,
+                                                                 int64_t n_steps, double dt) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double2 sR[SEG_MAX_COMM];
+  __shared__ int next;
+  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, a.g.smem_nodes);
+  uint32_t phase = 0;
+  unsigned int sync_idx = 0;
+  const double h2 = dt / 2.0, h6 = dt / 6.0;
+  unsigned int peer_target = ptr.pb_base;
+#define CDK_STAGE_SYNC(last)                                                                 \
+  do {                                                                                       \
+    if (PEERS) {                                                                             \
+      grid_sync(ptr.bar, ++sync_idx * gridDim.x);                                            \
+      peer_target += (unsigned int)a.n_peers;                                                \
+      if (blockIdx.x == 0 && threadIdx.x == 0) peer_barrier(ptr.pb, peer_target, a.status);  \
+      if (!(last)) grid_sync(ptr.bar, ++sync_idx * gridDim.x);                               \
+    } else if (!(last)) {                                                                    \
+      grid_sync(ptr.bar, ++sync_idx * gridDim.x);                                            \
+    }                                                                                        \
+  } while (0)
+  StageVar v = StageVar::of(a);
+  for (int64_t step = 0; step < n_steps; ++step) {
+    v.step_rel = step;
+#if CDK_ELL_RK4_RT
+    for (int st = 1; st <= 4; ++st) {  // z / partial buffers ping-pong: odd stages read [0]
+      const int in = (st & 1) ? 0 : 1;
+      v.z_in = ptr.z[in]; v.z_out = ptr.z[in ^ 1];
+      v.part_in = ptr.part[in]; v.part_out = ptr.part[in ^ 1];
+      v.peer_out = ptr.peer_z[in ^ 1];
+      v.h = (st <= 2) ? h2 : (st == 3 ? dt : h6);
+      ell_body(st, a, v, sm, phase);
+      CDK_STAGE_SYNC(st == 4 && step + 1 == n_steps);
+    }
+#else
+#define CDK_ELL_STAGE(st, hh)                                                                \
+  do {                                                                                       \
+    const int in = ((st) & 1) ? 0 : 1;                                                       \
+    v.z_in = ptr.z[in]; v.z_out = ptr.z[in ^ 1];                                             \
+    v.part_in = ptr.part[in]; v.part_out = ptr.part[in ^ 1];                                 \
+    v.peer_out = ptr.peer_z[in ^ 1];                                                         \
+    v.h = (hh);                                                                              \
+    ell_body((st), a, v, sm, phase);                                                         \
+    CDK_STAGE_SYNC((st) == 4 && step + 1 == n_steps);                                        \
+  } while (0)
+    CDK_ELL_STAGE(1, h2);
+    CDK_ELL_STAGE(2, h2);
+    CDK_ELL_STAGE(3, dt);
+    CDK_ELL_STAGE(4, h6);
+#undef CDK_ELL_STAGE
+#endif
   }
 #undef CDK_STAGE_SYNC
 }
@@ -1052,7 +1529,14 @@ static int check_graph(const cdk_graph *g) {
     set_error("cdk_graph: invalid sizes");
     return CDK_INPUT;
   }
-  if (g->cta_threads != NTHREADS) {
+  if (g->ell_off) {
+    if (g->cta_threads != ELL_THREADS || !g->xell_off || !g->ell_units || !g->seg_unit ||
+        !g->ell_part_base || g->n_ell_parts < 0 || g->inter_blocks != 0 || g->intra_split) {
+      set_error("cdk_graph (ELL): cta_threads must equal cdk_kuramoto_ell_threads(), xell_off "
+                "set, no inter_blocks / intra_split");
+      return CDK_INPUT;
+    }
+  } else if (g->cta_threads != NTHREADS) {
     set_error("cdk_graph: cta_threads must equal cdk_kuramoto_stage_threads()");
     return CDK_INPUT;
   }
@@ -1069,11 +1553,42 @@ static int check_graph(const cdk_graph *g) {
 }
 
 static size_t stage_smem(const cdk_graph *g) {
+  if (g->ell_off) return ell_smem_bytes(g->smem_nodes);
   return stage_smem_bytes(g->seg_rows_cap, g->smem_nodes, g->xs_cap);
+}
+
+// opt a kernel into the largest dynamic shared memory its static use leaves
+template <typename K>
+static int smem_optin(K kernel, int &attr_bytes, const char *what) {
+  if (attr_bytes >= 0) return CDK_OK;
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  const int dyn_max = cdk_max_smem_optin() - (int)fa.sharedSizeBytes;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  attr_bytes = dyn_max;
+  return CDK_OK;
+}
+
+template <int MODE>
+static int launch_ell_stage(const StageArgs &a, cudaStream_t st) {
+  static int attr_bytes = -1;
+  const size_t smem = stage_smem(&a.g);
+  int rc = smem_optin(ell_stage_kernel<MODE>, attr_bytes, "cudaFuncSetAttribute(ell stage)");
+  if (rc) return rc;
+  if ((int)smem > attr_bytes) {
+    set_error("ELL window does not fit the shared-memory opt-in limit");
+    return CDK_INPUT;
+  }
+  ell_stage_kernel<MODE><<<a.g.n_cta, a.g.cta_threads, smem, st>>>(a);
+  CDK_CHECK_LAUNCH("ell_stage_kernel");
+  return CDK_OK;
 }
 
 template <int MODE>
 static int launch_stage(const StageArgs &a, cudaStream_t st) {
+  if (a.g.ell_off) return launch_ell_stage<MODE>(a, st);
   static int attr_bytes = -1;  // opt-in set once per instantiation (single-device process)
   const size_t smem = stage_smem(&a.g);
   if (attr_bytes < 0) {
@@ -1107,6 +1622,10 @@ static int prepare(const cdk_graph *g, const double *theta, const Workspace &w, 
   }
   reset_status_kernel<<<1, 1, 0, st>>>(w.status);
   CDK_CHECK_LAUNCH("reset_status_kernel");
+  if (w.ell_cnt) {  // split-rblock arrival counters start at zero (finishers reset them)
+    cudaError_t e = cudaMemsetAsync(w.ell_cnt, 0, ((size_t)g->n_rblk + 1) * sizeof(int), st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(ell counters)");
+  }
   return CDK_OK;
 }
 
@@ -1122,6 +1641,8 @@ static StageArgs base_args(const cdk_graph *g, const Workspace &w, double *theta
   a.omega = omega;
   a.ksum = w.ksum;
   a.xacc = w.xacc;
+  a.ell_part = w.ell_part;
+  a.ell_cnt = w.ell_cnt;
   a.peer_out = nullptr;
   a.n_peers = 1;
   a.rank = 0;
@@ -1170,9 +1691,18 @@ extern "C" int cdk_kuramoto_rhs(const cdk_graph *g, const double *theta, const d
 
 static int launch_rk4_persistent(const StageArgs &a, const Workspace &w, int64_t n_steps,
                                  double dt, cudaStream_t st, const cdk_peers *peers = nullptr) {
-  static int attr_bytes = -1;
+  static int attr_bytes = -1, ell_attr = -1, ell_attr_peers = -1;
   const size_t smem = stage_smem(&a.g);
-  if (attr_bytes < 0) {
+  const bool ell = a.g.ell_off != nullptr;
+  if (ell) {
+    int rc = smem_optin(ell_rk4_kernel<false>, ell_attr, "cudaFuncSetAttribute(ell rk4)");
+    if (!rc) rc = smem_optin(ell_rk4_kernel<true>, ell_attr_peers, "cudaFuncSetAttribute(ell rk4)");
+    if (rc) return rc;
+    if ((int)smem > ell_attr) {
+      set_error("ELL window does not fit the shared-memory opt-in limit");
+      return CDK_INPUT;
+    }
+  } else if (attr_bytes < 0) {
     cudaFuncAttributes fa{};
     cudaError_t e = cudaFuncGetAttributes(&fa, kuramoto_rk4_kernel<false>);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncGetAttributes(rk4)");
@@ -1185,7 +1715,7 @@ static int launch_rk4_persistent(const StageArgs &a, const Workspace &w, int64_t
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(rk4)");
     attr_bytes = dyn_max;
   }
-  if ((int)smem > attr_bytes) {
+  if (!ell && (int)smem > attr_bytes) {
     set_error("community state does not fit the shared-memory opt-in limit");
     return CDK_INPUT;
   }
@@ -1216,10 +1746,13 @@ static int launch_rk4_persistent(const StageArgs &a, const Workspace &w, int64_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (peers && peers->n_ranks > 1)
-    e = cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel<true>, a, ptr, n_steps, dt);
+  const bool pe = peers && peers->n_ranks > 1;
+  if (ell)
+    e = pe ? cudaLaunchKernelEx(&cfg, ell_rk4_kernel<true>, a, ptr, n_steps, dt)
+           : cudaLaunchKernelEx(&cfg, ell_rk4_kernel<false>, a, ptr, n_steps, dt);
   else
-    e = cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel<false>, a, ptr, n_steps, dt);
+    e = pe ? cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel<true>, a, ptr, n_steps, dt)
+           : cudaLaunchKernelEx(&cfg, kuramoto_rk4_kernel<false>, a, ptr, n_steps, dt);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(kuramoto_rk4_kernel)");
   return CDK_OK;
@@ -1335,7 +1868,7 @@ extern "C" int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const d
 }
 
 // CDK_PROFILE builds only: per-CTA phase cycles [total, staging, gather, epilogue]
-// of the most recent stage launch are written to prof (device, 4*n_cta u64).
+// of the most recent stage launch are written to prof (device, 6*n_cta u64).
 extern "C" CDK_API void cdk_debug_set_profile_buffer(void *prof) {
   g_prof = reinterpret_cast<unsigned long long *>(prof);
 }
@@ -1368,6 +1901,9 @@ extern "C" int cdk_kuramoto_advance(const cdk_graph *g, void *workspace, int64_t
 }
 
 extern "C" int cdk_kuramoto_stage_threads(void) { return cdk::NTHREADS; }
+extern "C" int cdk_kuramoto_stage_ctas_per_sm(void) { return CDK_STAGE_MINBLOCKS; }
+extern "C" int cdk_kuramoto_ell_threads(void) { return cdk::ELL_THREADS; }
+extern "C" int cdk_kuramoto_ell_window_nodes(void) { return CDK_ELL_WINDOW; }
 
 static int check_peers(const cdk_peers *p) {
   if (!p || p->n_ranks < 1 || p->rank < 0 || p->rank >= p->n_ranks ||

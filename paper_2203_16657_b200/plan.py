@@ -81,6 +81,7 @@ class Schedule:
     intra_col: np.ndarray  # uint16, rebased to each row's segment base, bank-ordered
     xs_cap: int = 0  # staged inter-column capacity (cdk_graph.xs_cap)
     seg_xr: np.ndarray | None = None  # int64[2*n_seg] inter_ptr at segment bounds
+    ell: "EllLayout | None" = None  # lane-per-row sliced layout (ELL kernels)
 
     @property
     def n_seg(self) -> int:
@@ -133,6 +134,37 @@ def stage_threads() -> int:
     from ._lib import load_library
 
     return int(load_library().cdk_kuramoto_stage_threads())
+
+
+def ell_threads() -> int:
+    """threads per CTA of the ELL stage kernels (cdk_kuramoto_ell_threads)"""
+    from ._lib import load_library
+
+    return int(load_library().cdk_kuramoto_ell_threads())
+
+
+def ell_window_nodes() -> int:
+    """window capacity of the ELL kernels (CDK_ELL_WINDOW may lower it)"""
+    from ._lib import load_library
+
+    cap = int(load_library().cdk_kuramoto_ell_window_nodes())
+    env = _os.environ.get("CDK_ELL_WINDOW")
+    return min(cap, int(env) // WIN_ALIGN * WIN_ALIGN) if env else cap
+
+
+def ell_enabled() -> bool:
+    """lane-per-row ELL kernels for graphs without the inter sweep (CDK_ELL=0: off)"""
+    return _os.environ.get("CDK_ELL", "1") != "0"
+
+
+def ctas_per_sm() -> int:
+    """resident stage CTAs per SM the library was built for
+    (cdk_kuramoto_stage_ctas_per_sm): the schedule has SMs x this many CTAs"""
+    from ._lib import load_library
+
+    return int(load_library().cdk_kuramoto_stage_ctas_per_sm())
+
+
 import os as _os
 
 ROWS_CAP = int(_os.environ.get("CDK_ROWS_CAP", 1536))  # rows per segment (multiple of 8)
@@ -286,18 +318,28 @@ def _rblk_rows(lay: HostLayout) -> np.ndarray:
 
 
 def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int = ROWS_CAP,
-                   smem_budget: int = SMEM_BUDGET) -> Schedule:
+                   smem_budget: int = SMEM_BUDGET, ell: bool = False) -> Schedule:
     """Cost-balanced contiguous CTA ranges of rblocks (one CTA per SM), split
     into segments of <= rows_cap rows whose intra neighbours fit one
     shared-memory window (or, for communities above the window capacity and
     the NONE pool, gather from global memory)."""
     rows_cap = int(rows_cap) // 8 * 8
     smem_nodes = window_nodes(rows_cap, smem_budget)
+    if ell:  # ELL kernels: no per-row shared buffers, the whole carve-out is window
+        rows_cap, smem_nodes = 1 << 24, ell_window_nodes()
+        if lay.intra_split is not None:
+            raise InputError("ELL schedules need a layout without window-pass sub-runs")
     n_cta = max(1, int(sm_count))
     nrb = lay.n_rblk
     rows = _rblk_rows(lay)
     cum = np.concatenate([[0.0], np.cumsum(lay.row_cost)])
     rb_cost = cum[rows[1:]] - cum[rows[:-1]]
+    seg_cost = SEG_COST
+    if ell:  # ELL kernels: cost of an rblock = its slots (padding included)
+        e_off, x_off = _ell_sizes(lay)
+        rb_cost = (np.diff(e_off) * 8 * ELL_SLOT_COST + np.diff(x_off) * ELL_XSLOT_COST
+                   + ELL_RBLK_COST).astype(np.float64)
+        seg_cost = ELL_SEG_COST
 
     off = lay.comm_off
     win_lo = off[:-1] // WIN_ALIGN * WIN_ALIGN
@@ -313,7 +355,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
     # window to the widest staged community and give the rest of the budget
     # to the segment's inter-column slice (row pipeline reads them from smem)
     xs_cap = 0
-    if (_os.environ.get("CDK_XS", "1") != "0" and not multi.any()
+    if (not ell and _os.environ.get("CDK_XS", "1") != "0" and not multi.any()
             and lay.nnz_inter > 0 and stageable.any()):
         need = int((win_hi - win_lo)[stageable].max())
         rem = smem_budget - stage_smem_bytes(need, rows_cap)
@@ -342,7 +384,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         segs = segments(bounds)
         nseg_b = np.diff(np.asarray(segs[3]))
         cum0 = np.concatenate([[0.0], np.cumsum(rb_cost)])
-        cta_cost = cum0[bounds[1:]] - cum0[bounds[:-1]] + SEG_COST * nseg_b
+        cta_cost = cum0[bounds[1:]] - cum0[bounds[:-1]] + seg_cost * nseg_b
         if best is None or cta_cost.max() < best[0]:
             best = (cta_cost.max(), segs)
         share = np.zeros(nrb)
@@ -350,15 +392,19 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
             lo, hi = int(bounds[b]), int(bounds[b + 1])
             if hi > lo:
                 w = rb_cost[lo:hi]
-                share[lo:hi] = SEG_COST * nseg_b[b] * w / max(w.sum(), 1e-9)
+                share[lo:hi] = seg_cost * nseg_b[b] * w / max(w.sum(), 1e-9)
         extra = 0.5 * extra + 0.5 * share
     seg_rblk, seg_win, seg_base, cta_seg, seg_lpr = best[1]
     seg_rblk = np.asarray(seg_rblk, dtype=np.int32)
     seg_lpr = np.asarray(seg_lpr, dtype=np.int32)
     seg_win = np.asarray(seg_win, dtype=np.int64).reshape(-1, 2)
     seg_base = np.asarray(seg_base, dtype=np.int64)
-    return _finish_schedule(lay, rows, n_cta, rows_cap, smem_nodes, xs_cap, seg_rblk, seg_win,
-                            seg_base, cta_seg, seg_lpr, off)
+    sch = _finish_schedule(lay, rows, n_cta, rows_cap, smem_nodes, xs_cap, seg_rblk, seg_win,
+                           seg_base, cta_seg, seg_lpr, off, bank_order=not ell)
+    if ell:
+        sch.cta_threads = ell_threads()
+        sch.ell = build_ell(lay, sch)
+    return sch
 
 
 def _build_segments(lay, rows, cta_bounds, n_cta, rows_cap, smem_nodes, win_lo, win_hi,
@@ -401,7 +447,7 @@ def _build_segments(lay, rows, cta_bounds, n_cta, rows_cap, smem_nodes, win_lo, 
 
 
 def _finish_schedule(lay, rows, n_cta, rows_cap, smem_nodes, xs_cap, seg_rblk, seg_win, seg_base,
-                     cta_seg, seg_lpr, off):
+                     cta_seg, seg_lpr, off, bank_order: bool = True):
     """rebasing, bank ordering, segment inter ranges -> Schedule"""
     nrb = lay.n_rblk
 
@@ -430,9 +476,147 @@ def _finish_schedule(lay, rows, n_cta, rows_cap, smem_nodes, xs_cap, seg_rblk, s
         if newc.size and (newc.min() < 0 or newc.max() >= INTRA_PAD):
             raise InputError("rebased intra column out of uint16 range")
         col[m] = newc.astype(np.uint16)
-    _bank_order(col, _sub_run_ptr(lay), smem_nodes)
+    if bank_order:
+        _bank_order(col, _sub_run_ptr(lay), smem_nodes)
     return Schedule(n_cta, stage_threads(), int(smem_nodes), int(rows_cap), seg_rblk, seg_win,
                     seg_base, np.asarray(cta_seg, dtype=np.int32), seg_lpr, col, xs_cap, seg_xr)
+
+
+@dataclass
+class EllLayout:
+    """Lane-per-row sliced layout of the ELL kernels (cdk_graph.ell_off ...):
+    per rblock, chunk c of lane l is ell_col[(ell_off[b] + 32 c + l) * 8 ..
+    +8) and inter column k of lane l is xell_col[xell_off[b] + 32 k + l]."""
+    ell_off: np.ndarray  # int64[n_rblk+1], uint4 units
+    ell_col: np.ndarray  # uint16[8 * ell_off[-1]]
+    xell_off: np.ndarray  # int64[n_rblk+1], int32 units
+    xell_col: np.ndarray  # int32[xell_off[-1]], -1 = none
+    ell_units: np.ndarray | None = None  # int32[2*n_units]: rblock, part | parts << 16
+    seg_unit: np.ndarray | None = None  # int32[n_seg+1]
+    ell_part_base: np.ndarray | None = None  # int32[n_rblk], -1 = not split
+    n_parts: int = 0  # partial-sum slots of split rblocks
+
+    def slots(self) -> int:
+        """intra gather slots (entries + padding) one RHS issues"""
+        return int(self.ell_col.shape[0])
+
+
+# ELL cost model (cycles-ish per CTA): intra slot (one LDS.128 lane, 1/8 of a
+# wavefront), inter slot (a global z gather), per-rblock fixed work
+# (pointers, epilogue, sincos, partial) and per-segment staging
+ELL_SLOT_COST = float(_os.environ.get("CDK_ELL_SLOT_COST", 0.17))
+ELL_XSLOT_COST = float(_os.environ.get("CDK_ELL_XSLOT_COST", 0.3))
+ELL_RBLK_COST = float(_os.environ.get("CDK_ELL_RBLK_COST", 430.0))
+ELL_SEG_COST = float(_os.environ.get("CDK_ELL_SEG_COST", 3500.0))
+
+
+def _ell_call(lay: HostLayout, col, staged, shift, zero_slot, ell_off, out):
+    import ctypes
+
+    from ._lib import load_library
+
+    vp = ctypes.c_void_p
+    rows_c = np.ascontiguousarray(lay.rblk_row0, dtype=np.int64)
+    ptr = np.ascontiguousarray(lay.intra_ptr, dtype=np.int64)
+    rc = load_library().cdk_host_ell_intra(
+        rows_c.ctypes.data_as(vp), lay.n_rblk, ptr.ctypes.data_as(vp), col.ctypes.data_as(vp),
+        staged.ctypes.data_as(vp), shift.ctypes.data_as(vp), int(zero_slot),
+        ell_off.ctypes.data_as(vp),
+        out.ctypes.data_as(vp) if out is not None else None)
+    if rc != 0:
+        raise InputError(f"cdk_host_ell_intra failed ({rc})")
+
+
+def _ell_sizes(lay: HostLayout):
+    """(ell_off, xell_off) of the ELL layout (sizes do not depend on the
+    segment windows: bank groups are column mod 8 before and after rebasing)"""
+    nrb = lay.n_rblk
+    col = np.ascontiguousarray(lay.intra_col if lay.intra_col is not None and lay.intra_col.size
+                               else np.full(8, INTRA_PAD, np.uint16))
+    ell_off = np.zeros(nrb + 1, dtype=np.int64)
+    # layout columns are community-local: bank group of the global column
+    shift = np.zeros(max(nrb, 1), np.uint8)
+    if nrb:
+        c = np.maximum(lay.rblk_comm, 0)
+        shift[:nrb] = np.where(lay.rblk_comm >= 0, lay.comm_off[c] & 7, 0).astype(np.uint8)
+    _ell_call(lay, col, np.zeros(max(nrb, 1), np.uint8), shift, 0, ell_off, None)
+    xcnt = np.diff(lay.inter_ptr)
+    nx = np.zeros(nrb, dtype=np.int64)
+    if nrb:
+        rows = lay.rblk_row0
+        rb_of_row = np.repeat(np.arange(nrb), np.diff(rows))
+        np.maximum.at(nx, rb_of_row, xcnt[int(rows[0]):int(rows[-1])])
+    xell_off = np.zeros(nrb + 1, dtype=np.int64)
+    np.cumsum(32 * nx, out=xell_off[1:])
+    return ell_off, xell_off
+
+
+def build_ell(lay: HostLayout, sch: Schedule) -> EllLayout:
+    """ELL arrays from the rebased intra columns (cdk_host_ell_intra: each
+    quarter-warp step on 8 distinct bank groups) and the inter runs."""
+    nrb = lay.n_rblk
+    rows = lay.rblk_row0
+    seg_of_rb = np.repeat(np.arange(sch.n_seg), np.diff(sch.seg_rblk))
+    staged = np.zeros(max(nrb, 1), dtype=np.uint8)
+    if nrb:
+        staged[:nrb] = (sch.seg_win[seg_of_rb, 1] > sch.seg_win[seg_of_rb, 0]).astype(np.uint8)
+    col = np.ascontiguousarray(sch.intra_col if sch.intra_col.size else
+                               np.full(8, INTRA_PAD, np.uint16))
+    shift = np.zeros(max(nrb, 1), np.uint8)  # rebased columns: base = seg_base
+    if nrb:
+        shift[:nrb] = (sch.seg_base[seg_of_rb] & 7).astype(np.uint8)
+    ell_off, xell_off = _ell_sizes(lay)
+    ell_col = np.full(8 * int(ell_off[-1]), INTRA_PAD, dtype=np.uint16)
+    if ell_col.size:
+        _ell_call(lay, col, staged, shift, sch.smem_nodes, ell_off, ell_col)
+    xcnt = np.diff(lay.inter_ptr)
+    xell_col = np.full(int(xell_off[-1]), -1, dtype=np.int32)
+    if nrb and lay.nnz_inter:
+        r = np.repeat(np.arange(lay.n_rows, dtype=np.int64), xcnt)
+        k = np.arange(r.shape[0], dtype=np.int64) - lay.inter_ptr[r]
+        b = np.searchsorted(rows, r, side="right") - 1
+        if np.any((r < rows[0]) | (r >= rows[-1])):
+            raise InputError("inter entries outside the rblocks")
+        xell_col[xell_off[b] + 32 * k + (r - rows[b])] = lay.inter_col
+    units, seg_unit, part_base, n_parts = _ell_units(ell_off, xell_off, sch)
+    return EllLayout(ell_off, ell_col, xell_off, xell_col, units, seg_unit, part_base, n_parts)
+
+
+# chunks per work unit of split rblocks; 0 = no splitting (the default: the
+# split parts meet through a device-scope fence that stalls on the warp's
+# in-flight chunk loads, measured slower on config 2)
+ELL_UNIT_CH = int(_os.environ.get("CDK_ELL_UNIT", 0))
+
+
+def _ell_units(ell_off, xell_off, sch: Schedule):
+    """Work units of the ELL kernels: rblocks of more than 2 ELL_UNIT_CH chunks
+    are split into P = nch // ELL_UNIT_CH parts (a function of the rblock
+    alone); each segment's units are listed longest first (the warps' claim
+    order), ties by (rblock, part)."""
+    nch = np.diff(ell_off) // 32
+    nparts = (np.maximum(1, nch // ELL_UNIT_CH) if ELL_UNIT_CH > 0
+              else np.ones_like(nch)).astype(np.int64)
+    split = nparts > 1
+    part_base = np.full(nch.shape[0], -1, dtype=np.int64)
+    cum = np.cumsum(np.where(split, nparts, 0))
+    part_base[split] = (cum - nparts)[split]
+    n_parts = int(cum[-1]) if cum.size else 0
+    nx = np.diff(xell_off) // 32
+    units, seg_unit = [], [0]
+    for si in range(sch.n_seg):
+        a, z = int(sch.seg_rblk[si]), int(sch.seg_rblk[si + 1])
+        rb = np.repeat(np.arange(a, z), nparts[a:z])
+        q = np.arange(rb.shape[0]) - np.repeat(np.cumsum(nparts[a:z]) - nparts[a:z], nparts[a:z])
+        P = nparts[rb]
+        work = (nch[rb] * (q + 1) // P - nch[rb] * q // P) * 8 + np.where(q == 0, nx[rb], 0)
+        order = np.lexsort((q, rb, -work))
+        u = np.empty((rb.shape[0], 2), dtype=np.int64)
+        u[:, 0], u[:, 1] = rb[order], q[order] | (P[order] << 16)
+        units.append(u)
+        seg_unit.append(seg_unit[-1] + rb.shape[0])
+    units = (np.concatenate(units) if units else np.zeros((0, 2), np.int64)).astype(np.int32)
+    return (units.reshape(-1), np.asarray(seg_unit, dtype=np.int32), part_base.astype(np.int32),
+            n_parts)
 
 
 SEG_INTER_PHASE = 256  # include/commdyn_cuda.h CDK_SEG_INTER_PHASE
@@ -543,11 +727,13 @@ class DeviceGraph:
         from ._lib import CdkGraph
 
         dev = torch.device(device if device is not None else "cuda")
+        ell = ell_enabled() and inter_blocking(int(dec.n_nodes))[0] == 0
         if sm_count is None:
             sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+            sm_count *= 1 if ell else ctas_per_sm()
         lay = build_layout(dec, row_range=row_range,
-                           pass_nodes=window_nodes(ROWS_CAP, smem_budget))
-        sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget)
+                           pass_nodes=(1 << 30) if ell else window_nodes(ROWS_CAP, smem_budget))
+        sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget, ell=ell)
         self.row_range = (0, lay.n_rows) if row_range is None else tuple(int(x) for x in row_range)
         self.layout = lay
         self.schedule = sch
@@ -584,6 +770,17 @@ class DeviceGraph:
             self._t["intra_col"] = torch.full((8,), -1, dtype=torch.int16, device=dev)
         if self._t["inter_col"].numel() == 0:
             self._t["inter_col"] = torch.zeros(4, dtype=torch.int32, device=dev)
+        if sch.ell is not None:
+            e = sch.ell
+            self._t["ell_off"] = up(e.ell_off)
+            self._t["ell_col"] = up(e.ell_col.view(np.int16) if e.ell_col.size
+                                    else np.full(8, -1, np.int16))
+            self._t["xell_off"] = up(e.xell_off)
+            self._t["xell_col"] = up(e.xell_col if e.xell_col.size else np.full(4, -1, np.int32))
+            self._t["ell_units"] = up(e.ell_units if e.ell_units.size else np.zeros(2, np.int32))
+            self._t["seg_unit"] = up(e.seg_unit)
+            self._t["ell_part_base"] = up(e.ell_part_base if e.ell_part_base.size
+                                          else np.full(1, -1, np.int32))
         _attach_inter_split(self, lay.n_rows)
         t = self._t
         self.struct = CdkGraph(
@@ -600,7 +797,15 @@ class DeviceGraph:
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
             inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
             inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
-            xs_cap=sch.xs_cap, reserved0=0, seg_xr=t["seg_xr"].data_ptr(),
+            xs_cap=sch.xs_cap, n_ell_parts=sch.ell.n_parts if sch.ell is not None else 0,
+            seg_xr=t["seg_xr"].data_ptr(),
+            ell_off=t["ell_off"].data_ptr() if "ell_off" in t else None,
+            ell_col=t["ell_col"].data_ptr() if "ell_off" in t else None,
+            xell_off=t["xell_off"].data_ptr() if "ell_off" in t else None,
+            xell_col=t["xell_col"].data_ptr() if "ell_off" in t else None,
+            ell_units=t["ell_units"].data_ptr() if "ell_off" in t else None,
+            seg_unit=t["seg_unit"].data_ptr() if "ell_off" in t else None,
+            ell_part_base=t["ell_part_base"].data_ptr() if "ell_off" in t else None,
         )
 
     def device_bytes(self) -> int:
@@ -621,7 +826,7 @@ class DeviceGraph:
         self = cls.__new__(cls)
         dev = torch.device(device)
         if sm_count is None:
-            sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+            sm_count = torch.cuda.get_device_properties(dev).multi_processor_count * ctas_per_sm()
         sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget)
         self.layout, self.schedule = lay, sch
         self.n_rows, self.n_comm, self.device = lay.n_rows, lay.n_comm, dev
@@ -675,6 +880,7 @@ class DeviceGraph:
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
             inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
             inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
-            xs_cap=sch.xs_cap, reserved0=0, seg_xr=t["seg_xr"].data_ptr(),
+            xs_cap=sch.xs_cap, n_ell_parts=sch.ell.n_parts if sch.ell is not None else 0,
+            seg_xr=t["seg_xr"].data_ptr(),
         )
         return self

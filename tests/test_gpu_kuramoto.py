@@ -33,6 +33,18 @@ def _oracle_rhs(dec, omega, coupling, norm):
     return rhs
 
 
+@pytest.fixture(params=["ell", "legacy"])
+def kernel_path(request, monkeypatch):
+    """Both stage-kernel families: the lane-per-row ELL kernels (default for
+    graphs without the inter sweep) and the row-group kernels (CDK_ELL=0)."""
+    monkeypatch.setenv("CDK_ELL", "1" if request.param == "ell" else "0")
+    return request.param
+
+
+def _assert_path(eng, path):
+    assert bool(eng.graph.struct.ell_off) == (path == "ell")
+
+
 @pytest.fixture(scope="module")
 def cfg1():
     c = configs.config1()
@@ -52,10 +64,11 @@ def test_cfg1_rhs_vs_golden(cfg1, golden_dir):
     assert np.abs(k - g["rhs0_naive"]).max() <= 1e-12
 
 
-def test_cfg1_trajectory_vs_golden(cfg1, golden_dir):
+def test_cfg1_trajectory_vs_golden(cfg1, golden_dir, kernel_path):
     c, dec, omega, theta0 = cfg1
     g = np.load(os.path.join(golden_dir, "cfg1.npz"))
     eng = _engine(dec, omega, c.coupling, c.n)
+    _assert_path(eng, kernel_path)
     eng.set_state(theta0)
     snaps = []
     for _ in range(c.steps // 100):
@@ -111,7 +124,7 @@ def _random_case(seed, sizes, p_in, p_out, pool=0):
     dict(seed=4, sizes=[300], p_in=1.0, p_out=0.0, pool=0),            # empty S
     dict(seed=5, sizes=[33, 31, 32, 64, 65], p_in=0.2, p_out=0.3, pool=7),  # ragged rblocks
 ])
-def test_rhs_edge_cases_vs_oracle_and_naive(case):
+def test_rhs_edge_cases_vs_oracle_and_naive(case, kernel_path):
     import torch
 
     g, dec, omega_o, theta_o = _random_case(**case)
@@ -127,7 +140,7 @@ def test_rhs_edge_cases_vs_oracle_and_naive(case):
     assert np.abs(k - kn[perm]).max() <= 1e-12
 
 
-def test_unstaged_large_community():
+def test_unstaged_large_community(kernel_path):
     """A community above the shared-memory cap gathers from global memory."""
     import torch
 
@@ -143,12 +156,13 @@ def test_unstaged_large_community():
     omega = rng.standard_normal(n)
     theta = rng.uniform(-math.pi, math.pi, n)
     eng = _engine(dec, omega, 5.0, n)
+    _assert_path(eng, kernel_path)
     k = eng.rhs(torch.from_numpy(theta).cuda()).cpu().numpy()
     k_or = _oracle_rhs(dec, omega, 5.0, n)(theta)
     assert np.abs(k - k_or).max() <= RHS_TOL
 
 
-def test_schedule_independent_bitwise(cfg1):
+def test_schedule_independent_bitwise(cfg1, kernel_path):
     """Row-owned fixed-order accumulation: results are bitwise identical for
     any CTA schedule (the property the multi-GPU partition relies on)."""
     import torch
@@ -166,7 +180,7 @@ def test_schedule_independent_bitwise(cfg1):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
-def test_euler_and_blowup(cfg1):
+def test_euler_and_blowup(cfg1, kernel_path):
     c, dec, omega, theta0 = cfg1
     eng = _engine(dec, omega, c.coupling, c.n)
     eng.set_state(theta0)
@@ -189,7 +203,7 @@ def test_euler_and_blowup(cfg1):
     assert ei.value.step == 1
 
 
-def test_cfg2_rhs_and_steps_vs_golden(golden_dir):
+def test_cfg2_rhs_and_steps_vs_golden(golden_dir, kernel_path):
     import torch
 
     g = np.load(os.path.join(golden_dir, "cfg2_sample.npz"))
@@ -197,6 +211,7 @@ def test_cfg2_rhs_and_steps_vs_golden(golden_dir):
     dec = c.decomposition()
     omega, theta0 = c.state()
     eng = _engine(dec, omega, c.coupling, c.n)
+    _assert_path(eng, kernel_path)
     k = eng.rhs(torch.from_numpy(theta0).cuda()).cpu().numpy()
     idx = g["idx"]
     assert np.abs(k[idx] - g["rhs0"]).max() <= RHS_TOL

@@ -1,0 +1,6 @@
+#!/bin/bash
+# config-2 step time for ELL library variants (threads x chunk prefetch depth)
+B=paper_2203_16657_b200/_build
+for lib in "$@"; do
+  CDK_LIB=$B/libcommdyn_cuda_$lib.so timeout 300 python bench.py --steps 400 --warmup 10 --no-cpu-baseline 2>/tmp/err_$$ | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$lib', round(d['ms_per_step']*1e3,1), 'us/step', round(d['roofline']['stage_ms_mean']*1e3,1), 'us/stage e2e', round(d['e2e']['value']/1e9,3))" || tail -3 /tmp/err_$$
+done

@@ -16,13 +16,18 @@ else:
     c = configs.config2(); dec = c.decomposition(); omega, theta0 = c.state()
     eng = KuramotoEngine(dec, omega, coupling=c.coupling, norm=c.n)
 sch = eng.graph.schedule; lay = eng.graph.layout
-prof = torch.zeros(4 * sch.n_cta, dtype=torch.int64, device="cuda")
+prof = torch.zeros(6 * sch.n_cta, dtype=torch.int64, device="cuda")
 eng.lib.cdk_debug_set_profile_buffer(prof.data_ptr())
 eng.set_state(theta0)
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for it in range(3):
-    eng.rk4_stage(c.dt, 1)
+    ev[0].record(); eng.rk4_stage(c.dt, 1); ev[1].record()
 torch.cuda.synchronize()
-P = prof.view(-1, 4).cpu().numpy().astype(np.float64)
+P6 = prof.view(-1, 6).cpu().numpy()
+P = P6[:, :4].astype(np.float64)
+g0, g1 = P6[:, 4] - P6[:, 4].min(), P6[:, 5] - P6[:, 4].min()
+print(f"event-timed stage {ev[0].elapsed_time(ev[1])*1e3:.1f} us; CTA start skew max {g0.max()/1e3:.1f} us "
+      f"(p50 {np.median(g0)/1e3:.1f}); CTA end min {g1.min()/1e3:.1f} p50 {np.median(g1)/1e3:.1f} max {g1.max()/1e3:.1f} us")
 rows = lay.rblk_row0
 seg_rows = rows[sch.seg_rblk]
 feat = []
