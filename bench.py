@@ -52,13 +52,13 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic_bytes():
+def ncu_traffic_bytes(kernel: str = "stage_kernel"):
     """dram__bytes_read.sum + dram__bytes_write.sum of the stage kernel from the
-    committed `ncu --set full` capture (profiles/*_stage_kernel_ncu_raw.csv)."""
+    committed `ncu --set full` capture (profiles/rNN_<kernel>_ncu_raw.csv)."""
     import csv
     import glob
 
-    files = sorted(glob.glob(os.path.join(REPO, "profiles", "*_stage_kernel_ncu_raw.csv")))
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_{kernel}_ncu_raw.csv")))
     if not files:
         return None, None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -338,7 +338,9 @@ def run_ours(args):
     stage1_ms = float(stage_ms[:, 0].mean())
     peak, peak_kind = _peaks()
     achieved = b_rhs / (stage_mean_ms / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic_bytes()
+    kernel = "ell_stage_kernel" if dg.struct.ell_off else "kuramoto_stage_kernel"
+    traffic, traffic_src = ncu_traffic_bytes("ell_stage_kernel" if dg.struct.ell_off
+                                             else "stage_kernel")
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
@@ -355,7 +357,7 @@ def run_ours(args):
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "peak_kind": peak_kind,
-            "kernel": "kuramoto_stage_kernel", "algorithmic_bytes_per_launch": b_rhs,
+            "kernel": kernel, "algorithmic_bytes_per_launch": b_rhs,
             "stage_ms_mean": stage_mean_ms, "stage1_ms_mean": stage1_ms,
             "stage_ms_by_stage": [float(x) for x in stage_ms.mean(axis=0)],
         },

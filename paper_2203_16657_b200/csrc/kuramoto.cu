@@ -1038,13 +1038,14 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 // fixed by the layout: deterministic and independent of the CTA schedule.
 // ===========================================================================
 #ifndef CDK_ELL_THREADS
-#define CDK_ELL_THREADS 640
+#define CDK_ELL_THREADS 512  // measured (config 2, 8192-node window): 512 > 640 > 448 > 384 > 768
 #endif
 #ifndef CDK_ELL_WINDOW
-#define CDK_ELL_WINDOW 14336  // nodes: (14336 + 8) * 16 B = 224 KB of window + zero slots
+#define CDK_ELL_WINDOW 8192  // nodes: (8192 + 8) * 16 B = 128 KB; the rest of the SM stays L1
+                             // (measured: 14336 nodes, 224 KB, is 3% slower on config 2)
 #endif
 #ifndef CDK_ELL_DEPTH
-#define CDK_ELL_DEPTH 4  // 16-byte chunks per lane in flight ahead of the gathers
+#define CDK_ELL_DEPTH 8  // 16-byte chunks per lane in flight ahead of the gathers (6-8 best)
 #endif
 #ifndef CDK_ELL_XUNIT
 #define CDK_ELL_XUNIT 0  // 1: chunk queue runs across a warp's consecutive work units (slower)

@@ -727,7 +727,10 @@ class DeviceGraph:
         from ._lib import CdkGraph
 
         dev = torch.device(device if device is not None else "cuda")
-        ell = ell_enabled() and inter_blocking(int(dec.n_nodes))[0] == 0
+        # ELL kernels unless the graph needs the inter sweep or the caller
+        # asked for the row-group kernels' shared-memory budget
+        ell = (ell_enabled() and inter_blocking(int(dec.n_nodes))[0] == 0
+               and smem_budget == SMEM_BUDGET)
         if sm_count is None:
             sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
             sm_count *= 1 if ell else ctas_per_sm()
