@@ -1054,6 +1054,7 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 #define CDK_ELL_RK4_RT 1  // persistent RK4: one stage body with a runtime mode (0: four inlined)
 #endif
 constexpr int ELL_THREADS = CDK_ELL_THREADS;
+constexpr int ELL_PART_CAP = 512;  // rblock partials of a segment staged in shared memory
 constexpr int ELL_DEPTH = CDK_ELL_DEPTH;
 constexpr int ELL_WARPS = ELL_THREADS / 32;
 constexpr int ELL_GROUPS = ELL_THREADS / 8;
@@ -1296,6 +1297,7 @@ struct EllSmem {
   uint64_t *bar;
   double2 *sR;  // [SEG_MAX_COMM]
   int *next;    // rblock claim counter
+  double2 *sP;  // [ELL_PART_CAP] the segment's rblock partials (community sums)
 };
 
 // MODE: 0 RHS, 1..4 RK4 stage, 5 Euler (a runtime value: constant-folded in
@@ -1329,10 +1331,31 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
     if (cA >= 0) {  // community observables of the segment (canonical order)
       const int cB = g.rblk_comm[rbB - 1];
       const int cLast = cB >= 0 ? cB : (int)g.n_comm - 1;
+      const int pb0 = g.comm_rblk_off[cA], np = g.comm_rblk_off[cLast + 1] - pb0;
+      if (np <= ELL_PART_CAP) {  // all partials in one round trip, then the 8-lane sums
+        for (int q = tid; q < np; q += ELL_THREADS) sm.sP[q] = ldcg2(v.part_in + pb0 + q);
+        __syncthreads();
+      }
       for (int q = grp; q < cLast - cA + 1; q += ELL_GROUPS) {
         const int c = cA + q;
-        const double2 Rc = reduce_comm8(v.part_in, g.comm_rblk_off[c], g.comm_rblk_off[c + 1], t,
-                                        gmask);
+        const int b0 = g.comm_rblk_off[c], b1 = g.comm_rblk_off[c + 1];
+        double2 Rc;
+        if (np <= ELL_PART_CAP) {  // same order as reduce_comm8
+          double sr = 0.0, si = 0.0;
+          for (int b = b0 + t; b < b1; b += 8) {
+            const double2 pv = sm.sP[b - pb0];
+            sr += pv.x;
+            si += pv.y;
+          }
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(gmask, sr, o);
+            si += __shfl_xor_sync(gmask, si, o);
+          }
+          Rc = make_double2(sr, si);
+        } else {
+          Rc = reduce_comm8(v.part_in, b0, b1, t, gmask);
+        }
         if (t == 0) sm.sR[q] = Rc;
       }
     }
@@ -1382,8 +1405,9 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
 }
 
 __device__ __forceinline__ EllSmem ell_init(unsigned char *smem_raw, uint64_t *bar, double2 *sR,
-                                            int *next, int smem_nodes) {
+                                            int *next, double2 *sP, int smem_nodes) {
   EllSmem sm;
+  sm.sP = sP;
   sm.zs = reinterpret_cast<double2 *>(smem_raw);
   sm.bar = bar;
   sm.sR = sR;
@@ -1400,7 +1424,8 @@ __global__ void __launch_bounds__(ELL_THREADS, 1) ell_stage_kernel(const StageAr
   __shared__ __align__(8) uint64_t bar;
   __shared__ double2 sR[SEG_MAX_COMM];
   __shared__ int next;
-  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, a.g.smem_nodes);
+  __shared__ double2 sP[ELL_PART_CAP];
+  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, a.g.smem_nodes);
   uint32_t phase = 0;
 #ifdef CDK_PROFILE
   const unsigned long long t_begin = clock64();
@@ -1432,7 +1457,8 @@ __global__ void __launch_bounds__(ELL_THREADS, 1) ell_rk4_kernel(const __grid_co
   __shared__ __align__(8) uint64_t bar;
   __shared__ double2 sR[SEG_MAX_COMM];
   __shared__ int next;
-  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, a.g.smem_nodes);
+  __shared__ double2 sP[ELL_PART_CAP];
+  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, a.g.smem_nodes);
   uint32_t phase = 0;
   unsigned int sync_idx = 0;
   const double h2 = dt / 2.0, h6 = dt / 6.0;

@@ -501,13 +501,14 @@ class EllLayout:
         return int(self.ell_col.shape[0])
 
 
-# ELL cost model (cycles-ish per CTA): intra slot (one LDS.128 lane, 1/8 of a
+# ELL cost model (cycles per CTA, least-squares fit of per-CTA cycles on
+# config 2, tools/prof_ell.py): intra slot (one LDS.128 lane, 1/8 of a
 # wavefront), inter slot (a global z gather), per-rblock fixed work
 # (pointers, epilogue, sincos, partial) and per-segment staging
-ELL_SLOT_COST = float(_os.environ.get("CDK_ELL_SLOT_COST", 0.17))
-ELL_XSLOT_COST = float(_os.environ.get("CDK_ELL_XSLOT_COST", 0.3))
-ELL_RBLK_COST = float(_os.environ.get("CDK_ELL_RBLK_COST", 430.0))
-ELL_SEG_COST = float(_os.environ.get("CDK_ELL_SEG_COST", 3500.0))
+ELL_SLOT_COST = float(_os.environ.get("CDK_ELL_SLOT_COST", 0.144))
+ELL_XSLOT_COST = float(_os.environ.get("CDK_ELL_XSLOT_COST", 0.39))
+ELL_RBLK_COST = float(_os.environ.get("CDK_ELL_RBLK_COST", 100.0))
+ELL_SEG_COST = float(_os.environ.get("CDK_ELL_SEG_COST", 6500.0))
 
 
 def _ell_call(lay: HostLayout, col, staged, shift, zero_slot, ell_off, out):
