@@ -220,6 +220,8 @@ CDK_API int cdk_kuramoto_stage_threads(void);
 CDK_API int cdk_kuramoto_stage_ctas_per_sm(void);
 /* threads per CTA of the ELL stage kernels (graphs with ell_off set) */
 CDK_API int cdk_kuramoto_ell_threads(void);
+/* resident ELL CTAs per SM the library was built for */
+CDK_API int cdk_kuramoto_ell_ctas_per_sm(void);
 /* node capacity of the ELL kernels' shared-memory window (zero slots follow) */
 CDK_API int cdk_kuramoto_ell_window_nodes(void);
 

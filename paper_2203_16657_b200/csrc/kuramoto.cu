@@ -1054,7 +1054,10 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 #define CDK_ELL_RK4_RT 1  // persistent RK4: one stage body with a runtime mode (0: four inlined)
 #endif
 constexpr int ELL_THREADS = CDK_ELL_THREADS;
-constexpr int ELL_PART_CAP = 512;  // rblock partials of a segment staged in shared memory
+#ifndef CDK_ELL_MINBLOCKS
+#define CDK_ELL_MINBLOCKS 1  // resident ELL CTAs per SM (the planner launches SMs x this many)
+#endif
+constexpr int ELL_PART_CAP = 512 / CDK_ELL_MINBLOCKS;  // a segment's rblock partials in smem
 constexpr int ELL_DEPTH = CDK_ELL_DEPTH;
 constexpr int ELL_WARPS = ELL_THREADS / 32;
 constexpr int ELL_GROUPS = ELL_THREADS / 8;
@@ -1419,7 +1422,7 @@ __device__ __forceinline__ EllSmem ell_init(unsigned char *smem_raw, uint64_t *b
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(ELL_THREADS, 1) ell_stage_kernel(const StageArgs a) {
+__global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_stage_kernel(const StageArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ double2 sR[SEG_MAX_COMM];
@@ -1450,7 +1453,7 @@ __global__ void __launch_bounds__(ELL_THREADS, 1) ell_stage_kernel(const StageAr
 // Persistent RK4 over the ELL layout (cooperative launch, grid barrier
 // between stages; same sequencing as kuramoto_rk4_kernel).
 template <bool PEERS>
-__global__ void __launch_bounds__(ELL_THREADS, 1) ell_rk4_kernel(const __grid_constant__ StageArgs a,
+__global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_rk4_kernel(const __grid_constant__ StageArgs a,
                                                                  StepPtrs ptr,
                                                                  int64_t n_steps, double dt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1484,7 +1487,20 @@ __global__ void __launch_bounds__(ELL_THREADS, 1) ell_rk4_kernel(const __grid_co
       v.part_in = ptr.part[in]; v.part_out = ptr.part[in ^ 1];
       v.peer_out = ptr.peer_z[in ^ 1];
       v.h = (st <= 2) ? h2 : (st == 3 ? dt : h6);
+#ifdef CDK_PROFILE
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
       ell_body(st, a, v, sm, phase);
+#ifdef CDK_PROFILE
+      __syncthreads();
+      if (a.prof && step == 1 && threadIdx.x == 0) {  // second step: stage timeline per CTA
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        a.prof[6 * gridDim.x + 8 * blockIdx.x + 2 * (st - 1)] = t0;
+        a.prof[6 * gridDim.x + 8 * blockIdx.x + 2 * (st - 1) + 1] = t1;
+      }
+#endif
       CDK_STAGE_SYNC(st == 4 && step + 1 == n_steps);
     }
 #else
@@ -1930,6 +1946,7 @@ extern "C" int cdk_kuramoto_advance(const cdk_graph *g, void *workspace, int64_t
 extern "C" int cdk_kuramoto_stage_threads(void) { return cdk::NTHREADS; }
 extern "C" int cdk_kuramoto_stage_ctas_per_sm(void) { return CDK_STAGE_MINBLOCKS; }
 extern "C" int cdk_kuramoto_ell_threads(void) { return cdk::ELL_THREADS; }
+extern "C" int cdk_kuramoto_ell_ctas_per_sm(void) { return CDK_ELL_MINBLOCKS; }
 extern "C" int cdk_kuramoto_ell_window_nodes(void) { return CDK_ELL_WINDOW; }
 
 static int check_peers(const cdk_peers *p) {

@@ -143,6 +143,13 @@ def ell_threads() -> int:
     return int(load_library().cdk_kuramoto_ell_threads())
 
 
+def ell_ctas_per_sm() -> int:
+    """resident ELL CTAs per SM the library was built for"""
+    from ._lib import load_library
+
+    return int(load_library().cdk_kuramoto_ell_ctas_per_sm())
+
+
 def ell_window_nodes() -> int:
     """window capacity of the ELL kernels (CDK_ELL_WINDOW may lower it)"""
     from ._lib import load_library
@@ -734,7 +741,7 @@ class DeviceGraph:
                and smem_budget == SMEM_BUDGET)
         if sm_count is None:
             sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-            sm_count *= 1 if ell else ctas_per_sm()
+            sm_count *= ell_ctas_per_sm() if ell else ctas_per_sm()
         lay = build_layout(dec, row_range=row_range,
                            pass_nodes=(1 << 30) if ell else window_nodes(ROWS_CAP, smem_budget))
         sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget, ell=ell)
