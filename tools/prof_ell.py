@@ -29,13 +29,14 @@ F = []
 for b in range(sch.n_cta):
     s0, s1 = sch.cta_seg[b], sch.cta_seg[b + 1]
     a, z = seg_rb[s0], seg_rb[s1]
-    F.append((8 * (e.ell_off[z] - e.ell_off[a]), e.xell_off[z] - e.xell_off[a], z - a, s1 - s0))
+    win = sum(int(sch.seg_win[q, 1] - sch.seg_win[q, 0]) for q in range(s0, s1))
+    F.append((8 * (e.ell_off[z] - e.ell_off[a]), e.xell_off[z] - e.xell_off[a], z - a, s1 - s0, win))
 F = np.array(F, dtype=np.float64)
 print("cycles mean/max/min", cyc.mean(), cyc.max(), cyc.min())
-print("slots/xslots/rblocks/segs mean", F.mean(0), "max", F.max(0))
+print("slots/xslots/rblocks/segs/window mean", F.mean(0), "max", F.max(0))
 X = np.column_stack([F, np.ones(len(F))])
 coef, *_ = np.linalg.lstsq(X, cyc, rcond=None)
 pred = X @ coef
-print("fit slots/xslots/rblocks/segs/const", np.round(coef, 4), "R2", round(1 - ((cyc - pred) ** 2).sum() / ((cyc - cyc.mean()) ** 2).sum(), 3))
+print("fit slots/xslots/rblocks/segs/window/const", np.round(coef, 4), "R2", round(1 - ((cyc - pred) ** 2).sum() / ((cyc - cyc.mean()) ** 2).sum(), 3))
 for b in np.argsort(-cyc)[:6]: print("slow", b, int(cyc[b]), F[b].astype(int))
 for b in np.argsort(cyc)[:4]: print("fast", b, int(cyc[b]), F[b].astype(int))
