@@ -1045,7 +1045,13 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
                              // (measured: 14336 nodes, 224 KB, is 3% slower on config 2)
 #endif
 #ifndef CDK_ELL_DEPTH
-#define CDK_ELL_DEPTH 8  // 16-byte chunks per lane in flight ahead of the gathers (6-8 best)
+#define CDK_ELL_DEPTH 6  // 16-byte chunks per lane in flight ahead of the gathers (6-8 best)
+#endif
+#ifndef CDK_ELL_XCOLS
+#define CDK_ELL_XCOLS 12  // inter columns per lane loaded before the intra loop (multiple of 4)
+#endif
+#ifndef CDK_ELL_PF
+#define CDK_ELL_PF 0  // chunks prefetched into L1 beyond the register queue (0: off)
 #endif
 #ifndef CDK_ELL_XUNIT
 #define CDK_ELL_XUNIT 0  // 1: chunk queue runs across a warp's consecutive work units (slower)
@@ -1054,6 +1060,7 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 #define CDK_ELL_RK4_RT 1  // persistent RK4: one stage body with a runtime mode (0: four inlined)
 #endif
 constexpr int ELL_THREADS = CDK_ELL_THREADS;
+constexpr int ELL_XCOLS = CDK_ELL_XCOLS;
 #ifndef CDK_ELL_MINBLOCKS
 #define CDK_ELL_MINBLOCKS 1  // resident ELL CTAs per SM (the planner launches SMs x this many)
 #endif
@@ -1180,12 +1187,15 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     if (MODE != 0) th0 = a.theta[i];
     if (MODE >= 2 && MODE <= 4) ks0 = a.ksum[i];
   }
-  // first four inter gathers (L2) issued before the intra loop
+  // inter entries: the first ELL_XCOLS columns load before the intra loop and
+  // the z of the first four go out with them; after the loop the z of the
+  // remaining columns go out together (one exposed L2 round trip, not one
+  // column + one z round trip per batch of four)
   const int32_t *__restrict__ xc = g.xell_col + x0 + lane;
   const double2 *__restrict__ z_in = v.z_in;
-  int jx[4];
+  int jx[ELL_XCOLS];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) jx[q] = (q < nx) ? ldg(xc + 32 * q) : -1;
+  for (int q = 0; q < ELL_XCOLS; ++q) jx[q] = (q < nx) ? ldg(xc + 32 * q) : -1;
   double2 xz[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) xz[q] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
@@ -1202,6 +1212,10 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
 #pragma unroll
     for (int d = 0; d + 1 < ELL_DEPTH; ++d) cq[d] = cq[d + 1];
     const int t = c + ELL_DEPTH;
+#if CDK_ELL_PF > 0  // L1 prefetch CDK_ELL_PF chunks beyond the register queue
+    if (t + CDK_ELL_PF < nch)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(cp + 32 * (t + CDK_ELL_PF)));
+#endif
     cq[ELL_DEPTH - 1] = (t < nch) ? ldg(cp + 32 * t)
                         : (t - nch < nx_u.nch) ? ldg(nx_u.cp + 32 * (t - nch)) : padv;
     if (STAGED) {
@@ -1216,7 +1230,18 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     sr += xz[q].x;
     si += xz[q].y;
   }
-  for (int k = 4; k < nx; k += 4) {
+  if (ELL_XCOLS > 4 && nx > 4) {
+    double2 xw[ELL_XCOLS > 4 ? ELL_XCOLS - 4 : 1];
+#pragma unroll
+    for (int q = 4; q < ELL_XCOLS; ++q)
+      xw[q - 4] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 4; q < ELL_XCOLS; ++q) {
+      sr += xw[q - 4].x;
+      si += xw[q - 4].y;
+    }
+  }
+  for (int k = ELL_XCOLS; k < nx; k += 4) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) jx[q] = (k + q < nx) ? ldg(xc + 32 * (k + q)) : -1;
 #pragma unroll
