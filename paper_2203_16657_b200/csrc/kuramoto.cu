@@ -1050,6 +1050,9 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 #ifndef CDK_ELL_XCOLS
 #define CDK_ELL_XCOLS 12  // inter columns per lane loaded before the intra loop (multiple of 4)
 #endif
+#ifndef CDK_ELL_XLEAD
+#define CDK_ELL_XLEAD 0  // chunks before a unit's end at which its remaining inter gathers go out
+#endif
 #ifndef CDK_ELL_PF
 #define CDK_ELL_PF 0  // chunks prefetched into L1 beyond the register queue (0: off)
 #endif
@@ -1061,6 +1064,7 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 #endif
 constexpr int ELL_THREADS = CDK_ELL_THREADS;
 constexpr int ELL_XCOLS = CDK_ELL_XCOLS;
+constexpr int ELL_XLEAD = CDK_ELL_XLEAD;
 #ifndef CDK_ELL_MINBLOCKS
 #define CDK_ELL_MINBLOCKS 1  // resident ELL CTAs per SM (the planner launches SMs x this many)
 #endif
@@ -1207,7 +1211,16 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     if (d < need && d < nch) cq[d] = ldg(cp + 32 * d);
   need = ELL_DEPTH - nch > 0 ? ELL_DEPTH - nch : 0;
   double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+  double2 xw[ELL_XCOLS > 4 ? ELL_XCOLS - 4 : 1];
+  const int xtrig = (ELL_XLEAD > 0 && ELL_XCOLS > 4 && nx > 4)
+                        ? (nch > ELL_XLEAD ? nch - ELL_XLEAD : 0) : -1;
+  auto issue_xw = [&]() {
+#pragma unroll
+    for (int q = 4; q < ELL_XCOLS; ++q)
+      xw[q - 4] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
+  };
   for (int c = 0; c < nch; ++c) {
+    if (c == xtrig) issue_xw();  // the rest of the inter gathers, a few chunks before the end
     const uint4 w = cq[0];
 #pragma unroll
     for (int d = 0; d + 1 < ELL_DEPTH; ++d) cq[d] = cq[d + 1];
@@ -1231,10 +1244,7 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     si += xz[q].y;
   }
   if (ELL_XCOLS > 4 && nx > 4) {
-    double2 xw[ELL_XCOLS > 4 ? ELL_XCOLS - 4 : 1];
-#pragma unroll
-    for (int q = 4; q < ELL_XCOLS; ++q)
-      xw[q - 4] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
+    if (xtrig < 0 || nch == 0) issue_xw();
 #pragma unroll
     for (int q = 4; q < ELL_XCOLS; ++q) {
       sr += xw[q - 4].x;
