@@ -99,6 +99,9 @@ __device__ __forceinline__ void group_reduce(double2 &v, unsigned gmask) {
   }
 }
 
+#ifndef CDK_HO_LANE_ROW
+#define CDK_HO_LANE_ROW 1  // gathers: lane = row (1) or 8 lanes per row, 4 rows at a time (0)
+#endif
 // pass 1: Y, V (missing), X (inter), P = z Y, rblock partials of P
 __global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
   const int lane = threadIdx.x & 31, t = lane & 7, grp = lane >> 3;
@@ -108,6 +111,29 @@ __global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
     const int64_t row0 = a.rblk_row0[rb];
     const int nr = (int)(a.rblk_row0[rb + 1] - row0);
     double2 myP = make_double2(0.0, 0.0);
+#if CDK_HO_LANE_ROW
+    if (lane < nr) {  // lane = row (see pass 2)
+      const int64_t i = row0 + lane;
+      double2 y = make_double2(0.0, 0.0), v = y, x = y;
+      const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
+#pragma unroll 4
+      for (int64_t p = m0; p < m1; ++p) {
+        const double2 z = __ldg(a.z_in + a.miss_col[p]);
+        y = cadd(y, z);
+        v = cadd(v, cmul(z, z));
+      }
+      const int64_t x0 = a.inter_ptr[i], x1 = a.inter_ptr[i + 1];
+#pragma unroll 4
+      for (int64_t p = x0; p < x1; ++p) x = cadd(x, __ldg(a.z_in + a.inter_col[p]));
+      a.Y[i] = y;
+      a.V[i] = v;
+      a.X[i] = x;
+      myP = cmul(__ldg(a.z_in + i), y);
+      a.P[i] = myP;
+    }
+    (void)t;
+    (void)grp;
+#else
     for (int q = 0; q < 8; ++q) {
       const int r = 4 * q + grp;
       double2 y = make_double2(0.0, 0.0), v = y, x = y;
@@ -138,6 +164,7 @@ __global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
       const double py = __shfl_sync(FULL, pr.y, (lane & 3) * 8);
       if ((lane >> 2) == q) myP = make_double2(px, py);
     }
+#endif
     (void)gmask;
     const double2 part = rblock_partial(myP);
     if (lane == 0) a.pP[rb] = part;
@@ -161,6 +188,28 @@ __global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
       Wc = comm_sum(a.pP, b0, b1, lane);
     }
     double2 myU = make_double2(0.0, 0.0), myT = myU;
+#if CDK_HO_LANE_ROW
+    // lane = row: 32 independent gather streams per warp (the warp count is
+    // one per rblock, so memory-level parallelism has to come from the lanes)
+    if (lane < nr) {
+      const int64_t i = row0 + lane;
+      const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
+#pragma unroll 4
+      for (int64_t p = m0; p < m1; ++p) myU = cadd(myU, __ldcg(a.P + a.miss_col[p]));
+      const int64_t q0 = a.tri_ptr[i], q1 = a.tri_ptr[i + 1];
+#pragma unroll 4
+      for (int64_t p = q0; p < q1; ++p) {
+        const int2 jk = a.tri_jk[p];
+        const bool inter = jk.x < 0;
+        const int j = inter ? -jk.x - 1 : jk.x;
+        const double2 w = cmul(__ldg(a.z_in + j), __ldg(a.z_in + jk.y));
+        const double s = inter ? 2.0 : -2.0;  // missing -2 z_j z_k, spanning +2 z_j z_k
+        myT = cadd(myT, make_double2(s * w.x, s * w.y));
+      }
+    }
+    (void)t;
+    (void)grp;
+#else
     for (int q = 0; q < 8; ++q) {
       const int r = 4 * q + grp;
       double2 u = make_double2(0.0, 0.0), tri = u;
@@ -189,6 +238,7 @@ __global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
         myT = make_double2(tx, ty);
       }
     }
+#endif
     // epilogue: lane = row
     double2 zn = make_double2(0.0, 0.0), zn2 = zn;
     if (lane < nr) {
