@@ -253,9 +253,11 @@ def run_ours(args):
         eng.rk4(dt, 1, stream=stream)  # warm + attribute setup outside capture
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
+    lc0 = int(lib.cdk_launch_count())
     with torch.cuda.graph(graph, stream=stream):
         eng.rk4(dt, 1, stream=stream)
     torch.cuda.synchronize()
+    per_step_launches = int(lib.cdk_launch_count()) - lc0  # kernels one captured step holds
 
     W, K = max(3, args.warmup), args.steps
     sampler = ClockSampler(local)
@@ -280,8 +282,9 @@ def run_ours(args):
         _barrier(world)
         step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         # graph replays do not go through the library's launch counter: count
-        # the kernels each captured step holds (4 stage + 1 bookkeeping)
-        launches = int(lib.cdk_launch_count()) - l0 + 5 * K
+        # the kernels each captured step holds (persistent RK4 kernel +
+        # bookkeeping, counted at capture)
+        launches = int(lib.cdk_launch_count()) - l0 + per_step_launches * K
         eng.check()
         total_ms = _max_over_ranks(float(np.sum(step_ms)), world)
 
