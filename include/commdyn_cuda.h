@@ -225,6 +225,13 @@ CDK_API int cdk_kuramoto_ell_ctas_per_sm(void);
 /* node capacity of the ELL kernels' shared-memory window (zero slots follow) */
 CDK_API int cdk_kuramoto_ell_window_nodes(void);
 
+/* planner calibration (ELL graphs): one RK4 stage-1 launch writing each CTA's
+ * cycle count to cycles[n_cta] (device); only the workspace's stage buffers
+ * change (run cdk_kuramoto_prepare before a trajectory) */
+CDK_API int cdk_kuramoto_stage_cycles(const cdk_graph *g, double *theta, const double *omega,
+                                      double k_over_n, double dt, void *workspace,
+                                      unsigned long long *cycles, void *stream);
+
 /* bytes of device workspace the fused Kuramoto path needs for graph g */
 CDK_API size_t cdk_kuramoto_workspace_bytes(const cdk_graph *g);
 

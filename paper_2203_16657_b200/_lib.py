@@ -153,6 +153,7 @@ _SIGS = {
     "cdk_host_bank_order": [P, P, I64, I32, I32],
     "cdk_host_ell_intra": [P, I32, P, P, P, P, I32, P, P],
     "cdk_kuramoto_ell_threads": [],
+    "cdk_kuramoto_stage_cycles": [P, P, P, D, D, P, P, P],
     "cdk_kuramoto_ell_ctas_per_sm": [],
     "cdk_kuramoto_ell_window_nodes": [],
     "cdk_debug_set_profile_buffer": [P],

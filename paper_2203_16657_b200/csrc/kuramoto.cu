@@ -103,6 +103,7 @@ struct StageArgs {
   double h;     // stage increment (dt/2, dt/2, dt) or dt/6 at stage 4
   int64_t step_rel;
   unsigned long long *prof;  // CDK_PROFILE builds: per-CTA phase cycles
+  unsigned long long *cta_cycles;  // ELL stage kernels: per-CTA cycles (planner calibration)
   double2 *ell_part;  // Workspace::ell_part / ell_cnt
   int *ell_cnt;
 };
@@ -1465,12 +1466,17 @@ __global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_stage_kern
   __shared__ double2 sP[ELL_PART_CAP];
   const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, a.g.smem_nodes);
   uint32_t phase = 0;
+  const unsigned long long t_cal = a.cta_cycles ? clock64() : 0ull;
 #ifdef CDK_PROFILE
   const unsigned long long t_begin = clock64();
   unsigned long long g_begin;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_begin));
 #endif
   ell_body(MODE, a, StageVar::of(a), sm, phase);
+  if (a.cta_cycles) {  // calibration launches only
+    __syncthreads();
+    if (threadIdx.x == 0) a.cta_cycles[blockIdx.x] = clock64() - t_cal;
+  }
 #ifdef CDK_PROFILE
   __syncthreads();
   if (threadIdx.x == 0 && a.prof) {
@@ -1943,6 +1949,29 @@ extern "C" int cdk_kuramoto_rk4_stage(const cdk_graph *g, double *theta, const d
     case 3: a.h = dt; return launch_stage<3>(a, st);
     default: a.h = dt / 6.0; return launch_stage<4>(a, st);
   }
+}
+
+// Planner calibration: one RK4 stage-1 launch of the ELL stage kernel with
+// per-CTA cycle counts written to cycles[n_cta] (device).  Touches only the
+// workspace's stage buffers (ksum, z[1], partials[1]); theta is unchanged.
+extern "C" int cdk_kuramoto_stage_cycles(const cdk_graph *g, double *theta, const double *omega,
+                                         double k_over_n, double dt, void *workspace,
+                                         unsigned long long *cycles, void *stream) {
+  int rc = check_graph(g);
+  if (rc) return rc;
+  if (!g->ell_off || !cycles) {
+    set_error("cdk_kuramoto_stage_cycles: ELL graphs only, cycles required");
+    return CDK_INPUT;
+  }
+  cudaStream_t st = as_stream(stream);
+  Workspace w = carve(g, workspace, nullptr);
+  StageArgs a = base_args(g, w, theta, omega, k_over_n);
+  a.z_in = w.z[0]; a.z_out = w.z[1];
+  a.part_in = w.part[0]; a.part_out = w.part[1];
+  a.step_rel = 0;
+  a.h = dt / 2.0;
+  a.cta_cycles = cycles;
+  return launch_stage<1>(a, st);
 }
 
 // CDK_PROFILE builds only: per-CTA phase cycles [total, staging, gather, epilogue]

@@ -82,6 +82,7 @@ class Schedule:
     xs_cap: int = 0  # staged inter-column capacity (cdk_graph.xs_cap)
     seg_xr: np.ndarray | None = None  # int64[2*n_seg] inter_ptr at segment bounds
     ell: "EllLayout | None" = None  # lane-per-row sliced layout (ELL kernels)
+    rb_cost: np.ndarray | None = None  # the cost model the CTA cuts balanced
 
     @property
     def n_seg(self) -> int:
@@ -162,6 +163,12 @@ def ell_window_nodes() -> int:
 def ell_enabled() -> bool:
     """lane-per-row ELL kernels for graphs without the inter sweep (CDK_ELL=0: off)"""
     return _os.environ.get("CDK_ELL", "1") != "0"
+
+
+def ell_calibrate_iters() -> int:
+    """measured re-cuts of the ELL CTA ranges at DeviceGraph construction
+    (CDK_ELL_CALIBRATE, 0 = off)"""
+    return int(_os.environ.get("CDK_ELL_CALIBRATE", 4))
 
 
 def ctas_per_sm() -> int:
@@ -325,7 +332,8 @@ def _rblk_rows(lay: HostLayout) -> np.ndarray:
 
 
 def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int = ROWS_CAP,
-                   smem_budget: int = SMEM_BUDGET, ell: bool = False) -> Schedule:
+                   smem_budget: int = SMEM_BUDGET, ell: bool = False,
+                   rb_scale: np.ndarray | None = None) -> Schedule:
     """Cost-balanced contiguous CTA ranges of rblocks (one CTA per SM), split
     into segments of <= rows_cap rows whose intra neighbours fit one
     shared-memory window (or, for communities above the window capacity and
@@ -346,6 +354,8 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
         e_off, x_off = _ell_sizes(lay)
         rb_cost = (np.diff(e_off) * 8 * ELL_SLOT_COST + np.diff(x_off) * ELL_XSLOT_COST
                    + ELL_RBLK_COST).astype(np.float64)
+        if rb_scale is not None:  # measured calibration (DeviceGraph._calibrate)
+            rb_cost = rb_cost * rb_scale
         seg_cost = ELL_SEG_COST
 
     off = lay.comm_off
@@ -408,6 +418,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
     seg_base = np.asarray(seg_base, dtype=np.int64)
     sch = _finish_schedule(lay, rows, n_cta, rows_cap, smem_nodes, xs_cap, seg_rblk, seg_win,
                            seg_base, cta_seg, seg_lpr, off, bank_order=not ell)
+    sch.rb_cost = rb_cost
     if ell:
         sch.cta_threads = ell_threads()
         sch.ell = build_ell(lay, sch)
@@ -747,10 +758,78 @@ class DeviceGraph:
         sch = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget, ell=ell)
         self.row_range = (0, lay.n_rows) if row_range is None else tuple(int(x) for x in row_range)
         self.layout = lay
-        self.schedule = sch
         self.n_rows = lay.n_rows
         self.n_comm = lay.n_comm
         self.device = dev
+        self._upload(lay, sch)
+        if ell and ell_calibrate_iters() > 0 and lay.n_rblk > sch.n_cta:
+            self._calibrate(lay, sm_count, smem_budget)
+
+    def _calibrate(self, lay, sm_count, smem_budget):
+        """Re-cut the CTA ranges from measured per-CTA cycles: the cost model
+        balances the planner's features, but what is left of the CTA spread
+        is stable across launches (tools/prof_stab.py), so each rblock's cost
+        is rescaled by its CTA's measured/modelled ratio and the cuts are
+        redone (ELL_CAL_ITERS times, keeping the fastest schedule)."""
+        import ctypes
+
+        import torch
+
+        from ._lib import check, load_library
+
+        lib = load_library()
+        n = lay.n_rows
+        scale = np.ones(lay.n_rblk)
+        dev = self.device
+        theta = torch.zeros(n + 4, dtype=torch.float64, device=dev)
+        omega = torch.zeros(n + 4, dtype=torch.float64, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+
+        def measure():
+            nb = int(lib.cdk_kuramoto_workspace_bytes(ctypes.byref(self.struct)))
+            ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
+            cyc = torch.zeros(self.schedule.n_cta, dtype=torch.int64, device=dev)
+            gp = ctypes.byref(self.struct)
+            check(lib.cdk_kuramoto_prepare(gp, theta.data_ptr(), ws.data_ptr(), stream), "prepare")
+            best = None
+            for _ in range(3):  # min over launches: drops one-off noise
+                check(lib.cdk_kuramoto_stage_cycles(gp, theta.data_ptr(), omega.data_ptr(), 0.0,
+                                                    0.01, ws.data_ptr(), cyc.data_ptr(), stream),
+                      "stage_cycles")
+                c = cyc.cpu().numpy().astype(np.float64)
+                best = c if best is None else np.minimum(best, c)
+            return best
+
+        cur = measure()
+        best_max, best = cur.max(), (self.schedule, self._t, self.struct)
+        for _ in range(ell_calibrate_iters()):
+            sch = self.schedule
+            rows_rb = sch.seg_rblk[sch.cta_seg]  # first rblock of each CTA (+ end)
+            cta_of_rb = np.repeat(np.arange(sch.n_cta), np.diff(rows_rb))
+            model = np.asarray(sch.rb_cost, dtype=np.float64)
+            cta_model = np.bincount(cta_of_rb, weights=model[rows_rb[0]:rows_rb[-1]],
+                                    minlength=sch.n_cta)
+            ratio = np.where(cta_model > 0, cur / np.maximum(cta_model, 1e-9), 0.0)
+            ratio = ratio / max(np.mean(ratio[ratio > 0]), 1e-12) if np.any(ratio > 0) else ratio
+            r_rb = np.ones(lay.n_rblk)
+            r_rb[rows_rb[0]:rows_rb[-1]] = np.where(ratio[cta_of_rb] > 0, ratio[cta_of_rb], 1.0)
+            scale = scale * np.sqrt(r_rb)  # damped
+            sch2 = build_schedule(lay, sm_count=sm_count, smem_budget=smem_budget, ell=True,
+                                  rb_scale=scale)
+            self._upload(lay, sch2)
+            cur = measure()
+            if cur.max() < best_max:
+                best_max, best = cur.max(), (self.schedule, self._t, self.struct)
+        self.schedule, self._t, self.struct = best
+        self.calibration = {"cta_max_cycles": float(best_max)}
+
+    def _upload(self, lay, sch):
+        import torch
+
+        from ._lib import CdkGraph
+
+        dev = self.device
+        self.schedule = sch
 
         def up(a):
             return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
