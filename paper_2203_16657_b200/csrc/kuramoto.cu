@@ -1403,6 +1403,9 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
       mbar_wait(sm.bar, phase);
       phase ^= 1u;
     }
+#ifdef CDK_PROFILE
+    if (tid == 0 && a.prof && s == segA) a.prof[6 * blockIdx.x + 1] = clock64();  // ready (raw)
+#endif
     const double2 *zglob = v.z_in + g.seg_base[s];
     const int uB = g.seg_unit[s + 1];
     int u = g.seg_unit[s] + warp;
@@ -1482,7 +1485,8 @@ __global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_stage_kern
   if (threadIdx.x == 0 && a.prof) {
     unsigned long long *p = a.prof + 6 * blockIdx.x;
     p[0] = clock64() - t_begin;
-    p[1] = p[2] = p[3] = 0;
+    p[1] = p[1] - t_begin;  // first segment ready (window + community sums)
+    p[2] = p[3] = 0;
     unsigned long long g_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
     p[4] = g_begin;

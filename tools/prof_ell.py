@@ -33,6 +33,8 @@ for b in range(sch.n_cta):
     F.append((8 * (e.ell_off[z] - e.ell_off[a]), e.xell_off[z] - e.xell_off[a], z - a, s1 - s0, win))
 F = np.array(F, dtype=np.float64)
 print("cycles mean/max/min", cyc.mean(), cyc.max(), cyc.min())
+rdy = P6[:, 1].astype(np.float64)
+print("first segment ready after (cycles) mean/max/min", rdy.mean(), rdy.max(), rdy.min())
 print("slots/xslots/rblocks/segs/window mean", F.mean(0), "max", F.max(0))
 X = np.column_stack([F, np.ones(len(F))])
 coef, *_ = np.linalg.lstsq(X, cyc, rcond=None)
