@@ -119,3 +119,17 @@ def test_ell_layout_edge_cases(monkeypatch):
     lay, sch = _ell_schedule(dec, sm_count=3)
     _check(lay, sch)
     assert sch.ell.slots() == 0
+
+
+def test_rb_scale_recuts_keep_layout():
+    """build_schedule(rb_scale=...) (the calibration's re-cut) changes only the
+    CTA ranges: every layout invariant still holds and the per-rblock
+    schedules (chunk columns) are unchanged for unchanged segment windows."""
+    c = configs.config1()
+    lay = PL.build_layout(c.decomposition(), pass_nodes=1 << 30)
+    sch0 = PL.build_schedule(lay, sm_count=7, ell=True)
+    scale = np.linspace(0.5, 2.0, lay.n_rblk)
+    sch1 = PL.build_schedule(lay, sm_count=7, ell=True, rb_scale=scale)
+    _check(lay, sch1)
+    assert not np.array_equal(sch0.cta_seg, sch1.cta_seg) or not np.array_equal(
+        sch0.seg_rblk, sch1.seg_rblk)

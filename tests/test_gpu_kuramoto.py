@@ -228,3 +228,22 @@ def test_cfg2_rhs_and_steps_vs_golden(golden_dir, kernel_path):
     eng.set_state(theta0)
     eng.rk4(c.dt, int(g["steps"]))
     assert np.array_equal(fin, eng.theta.cpu().numpy())
+
+
+def test_calibrated_cuts_bitwise(monkeypatch):
+    """The measured re-cut of the ELL CTA ranges moves rblocks between CTAs
+    only: trajectories are bitwise equal with and without it."""
+    c = configs.scaled_config2(20000, 24, seed=5)
+    dec = c.decomposition()
+    omega, theta0 = c.state()
+    outs = []
+    for cal in ("0", "3"):
+        monkeypatch.setenv("CDK_ELL_CALIBRATE", cal)
+        eng = _engine(dec, omega, c.coupling, c.n)
+        assert bool(eng.graph.struct.ell_off)
+        assert hasattr(eng.graph, "calibration") == (cal != "0")
+        eng.set_state(theta0)
+        eng.rk4(c.dt, 10)
+        eng.check()
+        outs.append(eng.theta.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
