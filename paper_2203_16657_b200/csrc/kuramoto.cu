@@ -1265,14 +1265,16 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     }
   }
   if (nparts > 1) {  // split rblock: publish the partial; the last part finishes
+    // every part of an rblock is a unit of the same segment, hence of this
+    // CTA: CTA-scope fence and atomic (no device-scope drain)
     const int64_t base = (int64_t)g.ell_part_base[rb] * 32 + lane;
     __stcg(a.ell_part + base + 32 * part, make_double2(sr, si));
-    __threadfence();
+    __threadfence_block();
     int old = 0;
-    if (lane == 0) old = atomicAdd(a.ell_cnt + rb, 1);
+    if (lane == 0) old = atomicAdd_block(a.ell_cnt + rb, 1);
     old = __shfl_sync(FULL, old, 0);
     if (old != nparts - 1) return;
-    __threadfence();
+    __threadfence_block();
     const double2 own = make_double2(sr, si);
     sr = 0.0;
     si = 0.0;
