@@ -1065,6 +1065,14 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 #endif
 constexpr int ELL_THREADS = CDK_ELL_THREADS;
 constexpr int ELL_XCOLS = CDK_ELL_XCOLS;
+#ifndef CDK_ELL_XEARLY
+#define CDK_ELL_XEARLY 4  // inter z gathers issued before the intra loop (4 <= . <= XCOLS)
+#endif
+#ifndef CDK_ELL_LDSB
+#define CDK_ELL_LDSB 8  // shared-memory gathers in flight per lane (8 or 4)
+#endif
+constexpr int ELL_XEARLY = CDK_ELL_XEARLY;
+constexpr int ELL_LDSB = CDK_ELL_LDSB;
 constexpr int ELL_XLEAD = CDK_ELL_XLEAD;
 #ifndef CDK_ELL_MINBLOCKS
 #define CDK_ELL_MINBLOCKS 1  // resident ELL CTAs per SM (the planner launches SMs x this many)
@@ -1094,18 +1102,21 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint64_t bytes) {
 __device__ __forceinline__ void ell_gather8_smem(const uint4 w, uint32_t zs_addr, double &ar,
                                                  double &ai, double &br, double &bi) {
   const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-  double2 z[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
-    z[k] = lds_d2(zs_addr + (u << 4));
-  }
+  for (int k0 = 0; k0 < 8; k0 += ELL_LDSB) {  // ELL_LDSB loads in flight, then their adds
+    double2 z[ELL_LDSB];
 #pragma unroll
-  for (int k = 0; k < 8; k += 2) {
-    ar += z[k].x;
-    ai += z[k].y;
-    br += z[k + 1].x;
-    bi += z[k + 1].y;
+    for (int k = 0; k < ELL_LDSB; ++k) {
+      const uint32_t u = (wv[(k0 + k) >> 1] >> (((k0 + k) & 1) * 16)) & 0xFFFFu;
+      z[k] = lds_d2(zs_addr + (u << 4));
+    }
+#pragma unroll
+    for (int k = 0; k < ELL_LDSB; k += 2) {
+      ar += z[k].x;
+      ai += z[k].y;
+      br += z[k + 1].x;
+      bi += z[k + 1].y;
+    }
   }
 }
 
@@ -1201,9 +1212,10 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
   int jx[ELL_XCOLS];
 #pragma unroll
   for (int q = 0; q < ELL_XCOLS; ++q) jx[q] = (q < nx) ? ldg(xc + 32 * q) : -1;
-  double2 xz[4];
+  double2 xz[ELL_XEARLY];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) xz[q] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
+  for (int q = 0; q < ELL_XEARLY; ++q)
+    xz[q] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
   // intra chunks: ELL_DEPTH in flight ahead of the one being gathered
   const uint4 *__restrict__ cp = uc.cp;
   const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -1240,16 +1252,28 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
   }
   double sr = -(ar + br), si = -(ai + bi);  // intra-missing entries: sign -1
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < ELL_XEARLY; ++q) {
     sr += xz[q].x;
     si += xz[q].y;
   }
-  if (ELL_XCOLS > 4 && nx > 4) {
-    if (xtrig < 0 || nch == 0) issue_xw();
+  if (ELL_XCOLS > ELL_XEARLY && nx > ELL_XEARLY) {
+    if (ELL_XEARLY == 4) {
+      if (xtrig < 0 || nch == 0) issue_xw();
 #pragma unroll
-    for (int q = 4; q < ELL_XCOLS; ++q) {
-      sr += xw[q - 4].x;
-      si += xw[q - 4].y;
+      for (int q = 4; q < ELL_XCOLS; ++q) {
+        sr += xw[q - 4].x;
+        si += xw[q - 4].y;
+      }
+    } else {
+      double2 xl[ELL_XCOLS > ELL_XEARLY ? ELL_XCOLS - ELL_XEARLY : 1];
+#pragma unroll
+      for (int q = ELL_XEARLY; q < ELL_XCOLS; ++q)
+        xl[q - ELL_XEARLY] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = ELL_XEARLY; q < ELL_XCOLS; ++q) {
+        sr += xl[q - ELL_XEARLY].x;
+        si += xl[q - ELL_XEARLY].y;
+      }
     }
   }
   for (int k = ELL_XCOLS; k < nx; k += 4) {
