@@ -99,6 +99,10 @@ __device__ __forceinline__ void group_reduce(double2 &v, unsigned gmask) {
   }
 }
 
+#ifndef CDK_HO_UNROLL
+#define CDK_HO_UNROLL 16  // lane = row gather loops: entries in flight per lane (4: 0.68, 8: 0.42, 16: 0.375, 32: 0.39 ms per cfg3 step)
+#endif
+constexpr int HO_UNROLL = CDK_HO_UNROLL;
 #ifndef CDK_HO_LANE_ROW
 #define CDK_HO_LANE_ROW 1  // gathers: lane = row (1) or 8 lanes per row, 4 rows at a time (0)
 #endif
@@ -116,14 +120,14 @@ __global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
       const int64_t i = row0 + lane;
       double2 y = make_double2(0.0, 0.0), v = y, x = y;
       const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
-#pragma unroll 4
+#pragma unroll HO_UNROLL
       for (int64_t p = m0; p < m1; ++p) {
         const double2 z = __ldg(a.z_in + a.miss_col[p]);
         y = cadd(y, z);
         v = cadd(v, cmul(z, z));
       }
       const int64_t x0 = a.inter_ptr[i], x1 = a.inter_ptr[i + 1];
-#pragma unroll 4
+#pragma unroll HO_UNROLL
       for (int64_t p = x0; p < x1; ++p) x = cadd(x, __ldg(a.z_in + a.inter_col[p]));
       a.Y[i] = y;
       a.V[i] = v;
@@ -194,10 +198,10 @@ __global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
     if (lane < nr) {
       const int64_t i = row0 + lane;
       const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
-#pragma unroll 4
+#pragma unroll HO_UNROLL
       for (int64_t p = m0; p < m1; ++p) myU = cadd(myU, __ldcg(a.P + a.miss_col[p]));
       const int64_t q0 = a.tri_ptr[i], q1 = a.tri_ptr[i + 1];
-#pragma unroll 4
+#pragma unroll HO_UNROLL
       for (int64_t p = q0; p < q1; ++p) {
         const int2 jk = a.tri_jk[p];
         const bool inter = jk.x < 0;
