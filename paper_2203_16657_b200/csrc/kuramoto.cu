@@ -905,6 +905,9 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_stage_
 #endif
 }
 
+#ifndef CDK_GRID_SLEEP_NS
+#define CDK_GRID_SLEEP_NS 0  // grid-barrier poll back-off (64 ns: release ~0.2 us later)
+#endif
 // grid-wide barrier for the cooperative (co-resident) persistent kernel:
 // monotone arrival counter, target = (sync index + 1) * gridDim.x
 __device__ __forceinline__ void grid_sync(unsigned int *counter, unsigned int target) {
@@ -915,7 +918,7 @@ __device__ __forceinline__ void grid_sync(unsigned int *counter, unsigned int ta
     unsigned int v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-      if (v < target) __nanosleep(64);
+      if (v < target) __nanosleep(CDK_GRID_SLEEP_NS);
     } while (v < target);
     __threadfence();
   }
