@@ -792,7 +792,7 @@ class DeviceGraph:
             gp = ctypes.byref(self.struct)
             check(lib.cdk_kuramoto_prepare(gp, theta.data_ptr(), ws.data_ptr(), stream), "prepare")
             best = None
-            for _ in range(3):  # min over launches: drops one-off noise
+            for _ in range(5):  # min over launches: drops one-off noise
                 check(lib.cdk_kuramoto_stage_cycles(gp, theta.data_ptr(), omega.data_ptr(), 0.0,
                                                     0.01, ws.data_ptr(), cyc.data_ptr(), stream),
                       "stage_cycles")
