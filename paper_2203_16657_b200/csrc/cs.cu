@@ -114,18 +114,23 @@ __global__ void __launch_bounds__(512) cs_contract_kernel(const CsArgs a) {
 }
 
 #ifndef CDK_CS_UNROLL
-#define CDK_CS_UNROLL 1  // sparse-correction loops: entries in flight per lane (4, 8: 10% slower)
+#define CDK_CS_UNROLL 2  // sparse-correction loops: entries in flight per lane
 #endif
 constexpr int CS_UNROLL = CDK_CS_UNROLL;
+#ifndef CDK_CS_LPR
+#define CDK_CS_LPR 4  // lanes per row of cs_rows (1, 2, 4, 8); measured 4 (+ unroll 2) best
+#endif
+constexpr int CS_LPR = CDK_CS_LPR;
 
 // MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.
 template <int MODE>
 __global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
-  const int lane = threadIdx.x & 31, t = lane & 7;
-  const unsigned gmask = 0xFFu << (lane & 24);
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  const int lane = threadIdx.x & 31, t = lane & (CS_LPR - 1);
+  const unsigned gmask = CS_LPR == 32 ? 0xFFFFFFFFu
+                                      : (((1u << CS_LPR) - 1u) << (lane & ~(CS_LPR - 1)));
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / CS_LPR;
   // rows of communities first, then NONE pool rows (no dense part)
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; i < a.n_rows;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / CS_LPR; i < a.n_rows;
        i += ngroups) {
     // community of row i (binary search over comm_off)
     int c = -1;
@@ -148,9 +153,9 @@ __global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
       const double *Hc = a.H + (int64_t)c * CS_NOUT;
       double xp = 1.0;
       for (int k = 0; k < t; ++k) xp *= x;
-      double x8 = 1.0;
-      for (int k = 0; k < 8; ++k) x8 *= x;
-      for (int p = t; p <= CS_D2; p += 8) {
+      double x8 = 1.0;  // x^CS_LPR
+      for (int k = 0; k < CS_LPR; ++k) x8 *= x;
+      for (int p = t; p <= CS_D2; p += CS_LPR) {
         const int r0 = c_mono_row[p];
         double yq = 1.0;
         for (int q = 0; q <= CS_D2 - p; ++q) {
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
     // exact sparse correction
     double ax = 0.0, ay = 0.0;
 #pragma unroll CS_UNROLL
-    for (int64_t p = a.miss_ptr[i] + t; p < a.miss_ptr[i + 1]; p += 8) {
+    for (int64_t p = a.miss_ptr[i] + t; p < a.miss_ptr[i + 1]; p += CS_LPR) {
       const int j = a.miss_col[p];
       const double2 sj = a.s_in[j], vj = a.v_in[j];
       const double dx = sj.x - sm.x, dy = sj.y - sm.y;
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
       ay -= w * (vj.y - vm.y);
     }
 #pragma unroll CS_UNROLL
-    for (int64_t p = a.inter_ptr[i] + t; p < a.inter_ptr[i + 1]; p += 8) {
+    for (int64_t p = a.inter_ptr[i] + t; p < a.inter_ptr[i + 1]; p += CS_LPR) {
       const int j = a.inter_col[p];
       const double2 sj = a.s_in[j], vj = a.v_in[j];
       const double dx = sj.x - sm.x, dy = sj.y - sm.y;
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
       ay += w * (vj.y - vm.y);
     }
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
+    for (int o = CS_LPR / 2; o > 0; o >>= 1) {
       g0 += __shfl_xor_sync(gmask, g0, o);
       gx += __shfl_xor_sync(gmask, gx, o);
       gy += __shfl_xor_sync(gmask, gy, o);
@@ -318,7 +323,7 @@ static CsArgs cs_args(const cdk_cs_graph *g, const CsWs &w, double K, double sig
 }
 
 static unsigned cs_row_grid(int64_t n) {
-  const int64_t groups_per_block = 256 / 8;
+  const int64_t groups_per_block = 256 / CS_LPR;
   int64_t g = (n + groups_per_block - 1) / groups_per_block;
   if (g > 148 * 16) g = 148 * 16;
   return (unsigned)(g > 0 ? g : 1);
