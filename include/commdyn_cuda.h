@@ -173,6 +173,11 @@ typedef struct cdk_graph {
   const int32_t *ell_units;     /* [2 * n_units] */
   const int32_t *seg_unit;      /* [n_seg+1] */
   const int32_t *ell_part_base; /* [n_rblk], -1 = not split */
+  /* packed ELL unit metadata (or NULL): unit u = int32[8] at ell_meta + 8u:
+   * {first chunk (uint4 units), xell start, first row, rblock; chunks, inter
+   * entries per lane (0 for parts > 0), rows, ci | part << 8 | nparts << 16}
+   * with ci the rblock's community minus the segment's first (255: pool) */
+  const int32_t *ell_meta;
 } cdk_graph;
 
 /* device-side run status (lives inside the workspace) */

@@ -59,6 +59,7 @@ class CdkGraph(ctypes.Structure):
         ("ell_units", P),
         ("seg_unit", P),
         ("ell_part_base", P),
+        ("ell_meta", P),
     ]
 
 

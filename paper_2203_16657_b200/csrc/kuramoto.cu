@@ -1165,6 +1165,14 @@ struct UnitChunks {
   int nch;
 };
 __device__ __forceinline__ UnitChunks unit_chunks(const cdk_graph &g, int u, int lane) {
+  if (g.ell_meta) {  // packed unit metadata: one round trip
+    const int4 m0 = ldg(reinterpret_cast<const int4 *>(g.ell_meta) + 2 * u);
+    const int4 m1 = ldg(reinterpret_cast<const int4 *>(g.ell_meta) + 2 * u + 1);
+    UnitChunks r;
+    r.cp = reinterpret_cast<const uint4 *>(g.ell_col) + (uint32_t)m0.x + lane;
+    r.nch = m1.x;
+    return r;
+  }
   const int rb = g.ell_units[2 * u], code = g.ell_units[2 * u + 1];
   const int part = code & 0xFFFF, nparts = code >> 16;
   const int nch_rb = (int)((g.ell_off[rb + 1] - g.ell_off[rb]) >> 5);
@@ -1189,16 +1197,27 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
                                            uint32_t zs_addr, const double2 *zs, int64_t w0,
                                            const double2 *__restrict__ zglob, double2 R,
                                            uint4 (&cq)[ELL_DEPTH], int &need,
-                                           const UnitChunks &uc, const UnitChunks &nx_u) {
+                                           const UnitChunks &uc, const UnitChunks &nx_u,
+                                           const int4 *mt = nullptr) {
   const cdk_graph &g = a.g;
   const int lane = threadIdx.x & 31;
-  const int64_t r0 = g.rblk_row0[rb], r1 = g.rblk_row0[rb + 1];
+  int64_t r0, r1, x0;
+  int nx;
+  if (mt) {  // packed unit metadata (cdk_graph.ell_meta)
+    r0 = (uint32_t)mt->z;
+    r1 = r0 + (mt[1].z & 0xFF);
+    x0 = (uint32_t)mt->y;
+    nx = mt[1].y;
+  } else {
+    r0 = g.rblk_row0[rb];
+    r1 = g.rblk_row0[rb + 1];
+    x0 = g.xell_off[rb];
+    nx = (part == 0) ? (int)((g.xell_off[rb + 1] - x0) >> 5) : 0;
+  }
   const int64_t i = r0 + lane;
   const bool valid = i < r1;
-  const int64_t x0 = g.xell_off[rb];
   // this unit's chunks (part of a split rblock) and inter entries (part 0)
   const int nch = uc.nch;
-  const int nx = (part == 0) ? (int)((g.xell_off[rb + 1] - x0) >> 5) : 0;
   // epilogue inputs: in flight during the gathers
   double om = 0.0, th0 = 0.0, ks0 = 0.0;
   if (valid) {
@@ -1450,15 +1469,32 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
       nxt = __shfl_sync(FULL, nxt, 0);
       if (nxt < uB) nu = unit_chunks(g, nxt, lane);
 #endif
-      const int rb = g.ell_units[2 * u], code = g.ell_units[2 * u + 1];
-      const int c = g.rblk_comm[rb];
-      const double2 R = (c >= 0) ? sm.sR[c - cA] : make_double2(0.0, 0.0);
-      if (staged) {
-        ell_rblock<true>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob, R,
-                               cq, need, uc, nu);
+      int rb, part, nparts;
+      double2 R;
+      int4 mt[2];
+      if (g.ell_meta) {  // rblock, rows, inter range and community in one round trip
+        mt[0] = ldg(reinterpret_cast<const int4 *>(g.ell_meta) + 2 * u);
+        mt[1] = ldg(reinterpret_cast<const int4 *>(g.ell_meta) + 2 * u + 1);
+        rb = mt[0].w;
+        part = (mt[1].w >> 8) & 0xFF;
+        nparts = (mt[1].w >> 16) & 0xFF;
+        const int ci = mt[1].w & 0xFF;  // community relative to the segment's first (255: pool)
+        R = (ci != 0xFF) ? sm.sR[ci] : make_double2(0.0, 0.0);
       } else {
-        ell_rblock<false>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob, R,
-                                cq, need, uc, nu);
+        rb = g.ell_units[2 * u];
+        const int code = g.ell_units[2 * u + 1];
+        part = code & 0xFFFF;
+        nparts = code >> 16;
+        const int c = g.rblk_comm[rb];
+        R = (c >= 0) ? sm.sR[c - cA] : make_double2(0.0, 0.0);
+      }
+      const int4 *mp = g.ell_meta ? mt : nullptr;
+      if (staged) {
+        ell_rblock<true>(MODE, a, v, rb, part, nparts, zs_addr, sm.zs, w0, zglob, R, cq, need,
+                         uc, nu, mp);
+      } else {
+        ell_rblock<false>(MODE, a, v, rb, part, nparts, zs_addr, sm.zs, w0, zglob, R, cq, need,
+                          uc, nu, mp);
       }
 #if !CDK_ELL_XUNIT
       int nxt = 0;

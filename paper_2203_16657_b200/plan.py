@@ -513,6 +513,7 @@ class EllLayout:
     seg_unit: np.ndarray | None = None  # int32[n_seg+1]
     ell_part_base: np.ndarray | None = None  # int32[n_rblk], -1 = not split
     n_parts: int = 0  # partial-sum slots of split rblocks
+    ell_meta: np.ndarray | None = None  # int32[8*n_units] packed unit metadata (or None)
 
     def slots(self) -> int:
         """intra gather slots (entries + padding) one RHS issues"""
@@ -598,7 +599,42 @@ def build_ell(lay: HostLayout, sch: Schedule) -> EllLayout:
             raise InputError("inter entries outside the rblocks")
         xell_col[xell_off[b] + 32 * k + (r - rows[b])] = lay.inter_col
     units, seg_unit, part_base, n_parts = _ell_units(ell_off, xell_off, sch)
-    return EllLayout(ell_off, ell_col, xell_off, xell_col, units, seg_unit, part_base, n_parts)
+    meta = _ell_meta(lay, sch, ell_off, xell_off, units, seg_unit)
+    return EllLayout(ell_off, ell_col, xell_off, xell_col, units, seg_unit, part_base, n_parts,
+                     meta)
+
+
+def _ell_meta(lay: HostLayout, sch: Schedule, ell_off, xell_off, units, seg_unit):
+    """packed per-unit metadata (cdk_graph.ell_meta): the kernel reads one
+    unit's rblock, rows, chunk and inter ranges and community slot in one
+    round trip instead of three dependent lookups; None if offsets overflow
+    int32"""
+    if ell_off[-1] >= 2**31 or xell_off[-1] >= 2**31 or lay.n_rows >= 2**31:
+        return None
+    u = units.reshape(-1, 2).astype(np.int64)
+    nu = u.shape[0]
+    meta = np.zeros((nu, 8), dtype=np.int64)
+    if nu == 0:
+        return meta.astype(np.int32).reshape(-1)
+    rb, q, P = u[:, 0], u[:, 1] & 0xFFFF, u[:, 1] >> 16
+    rows = lay.rblk_row0
+    nch_rb = (ell_off[rb + 1] - ell_off[rb]) // 32
+    ch0, ch1 = nch_rb * q // P, nch_rb * (q + 1) // P
+    seg = np.repeat(np.arange(sch.n_seg), np.diff(seg_unit))
+    c = lay.rblk_comm[rb].astype(np.int64)
+    cA = lay.rblk_comm[sch.seg_rblk[seg]].astype(np.int64)
+    ci = np.where(c >= 0, c - cA, 255)
+    if np.any((ci < 0) | ((ci > SEG_MAX_COMM) & (ci != 255))) or np.any(P > 255):
+        return None
+    meta[:, 0] = ell_off[rb] + 32 * ch0
+    meta[:, 1] = xell_off[rb]
+    meta[:, 2] = rows[rb]
+    meta[:, 3] = rb
+    meta[:, 4] = ch1 - ch0
+    meta[:, 5] = np.where(q == 0, (xell_off[rb + 1] - xell_off[rb]) // 32, 0)
+    meta[:, 6] = rows[rb + 1] - rows[rb]
+    meta[:, 7] = ci | (q << 8) | (P << 16)
+    return meta.astype(np.int32).reshape(-1)
 
 
 # chunks per work unit of split rblocks; 0 = no splitting (the default: the
@@ -871,6 +907,8 @@ class DeviceGraph:
             self._t["seg_unit"] = up(e.seg_unit)
             self._t["ell_part_base"] = up(e.ell_part_base if e.ell_part_base.size
                                           else np.full(1, -1, np.int32))
+            if e.ell_meta is not None and _os.environ.get("CDK_ELL_META", "1") != "0":
+                self._t["ell_meta"] = up(e.ell_meta if e.ell_meta.size else np.zeros(8, np.int32))
         _attach_inter_split(self, lay.n_rows)
         t = self._t
         self.struct = CdkGraph(
@@ -896,6 +934,7 @@ class DeviceGraph:
             ell_units=t["ell_units"].data_ptr() if "ell_off" in t else None,
             seg_unit=t["seg_unit"].data_ptr() if "ell_off" in t else None,
             ell_part_base=t["ell_part_base"].data_ptr() if "ell_off" in t else None,
+            ell_meta=t["ell_meta"].data_ptr() if "ell_meta" in t else None,
         )
 
     def device_bytes(self) -> int:

@@ -80,6 +80,18 @@ def _check(lay, sch):
         want = [(b, q) for b in range(a, z) for q in range(_parts(nch[b]))]
         assert got == want
         assert np.all(P == np.array([_parts(x) for x in nch[u[:, 0]]], dtype=P.dtype))
+    if e.ell_meta is not None:  # packed unit metadata agrees with the arrays
+        m = e.ell_meta.reshape(-1, 8)
+        assert m.shape[0] == units.shape[0]
+        for k in range(m.shape[0]):
+            b, code = int(units[k, 0]), int(units[k, 1])
+            q, P = code & 0xFFFF, code >> 16
+            nb = int(nch[b])
+            assert m[k, 3] == b and m[k, 2] == rows[b] and m[k, 6] == rows[b + 1] - rows[b]
+            assert m[k, 0] == e.ell_off[b] + 32 * (nb * q // P)
+            assert m[k, 4] == nb * (q + 1) // P - nb * q // P
+            assert m[k, 5] == ((e.xell_off[b + 1] - e.xell_off[b]) // 32 if q == 0 else 0)
+            assert (m[k, 7] >> 8) & 0xFF == q and (m[k, 7] >> 16) & 0xFF == P
     split = np.nonzero(e.ell_part_base >= 0)[0]
     P = np.array([_parts(x) for x in nch], dtype=np.int64)
     assert np.all(P[e.ell_part_base < 0] == 1)
