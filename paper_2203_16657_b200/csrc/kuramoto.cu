@@ -1060,6 +1060,9 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
 #ifndef CDK_ELL_PF
 #define CDK_ELL_PF 0  // chunks prefetched into L1 beyond the register queue (0: off)
 #endif
+#ifndef CDK_ELL_MPF
+#define CDK_ELL_MPF 0  // claim the next unit and load its metadata at the start of the current one
+#endif
 #ifndef CDK_ELL_XUNIT
 #define CDK_ELL_XUNIT 0  // 1: chunk queue runs across a warp's consecutive work units (slower)
 #endif
@@ -1459,6 +1462,53 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
     int u = g.seg_unit[s] + warp;
     uint4 cq[ELL_DEPTH];
     int need = ELL_DEPTH;
+    if (g.ell_meta) {  // packed metadata: the unit's description travels in registers
+      const int4 *meta = reinterpret_cast<const int4 *>(g.ell_meta);
+      int4 ma = make_int4(0, 0, 0, 0), mb = ma;
+      if (u < uB) {
+        ma = ldg(meta + 2 * u);
+        mb = ldg(meta + 2 * u + 1);
+      }
+      while (u < uB) {
+        int nxt = 0;
+        int4 na = make_int4(0, 0, 0, 0), nb = na;
+#if CDK_ELL_MPF  // claim the next unit and fetch its description up front
+        if (lane == 0) nxt = atomicAdd(sm.next, 1);
+        nxt = __shfl_sync(FULL, nxt, 0);
+        if (nxt < uB) {
+          na = ldg(meta + 2 * nxt);
+          nb = ldg(meta + 2 * nxt + 1);
+        }
+#endif
+        const int ci = mb.w & 0xFF;  // community relative to the segment's first (255: pool)
+        const double2 R = (ci != 0xFF) ? sm.sR[ci] : make_double2(0.0, 0.0);
+        const UnitChunks uc{reinterpret_cast<const uint4 *>(g.ell_col) + (uint32_t)ma.x + lane,
+                            mb.x};
+        const UnitChunks nu{nullptr, 0};
+        const int4 mt[2] = {ma, mb};
+        need = ELL_DEPTH;
+        if (staged) {
+          ell_rblock<true>(MODE, a, v, ma.w, (mb.w >> 8) & 0xFF, (mb.w >> 16) & 0xFF, zs_addr,
+                           sm.zs, w0, zglob, R, cq, need, uc, nu, mt);
+        } else {
+          ell_rblock<false>(MODE, a, v, ma.w, (mb.w >> 8) & 0xFF, (mb.w >> 16) & 0xFF, zs_addr,
+                            sm.zs, w0, zglob, R, cq, need, uc, nu, mt);
+        }
+#if !CDK_ELL_MPF
+        if (lane == 0) nxt = atomicAdd(sm.next, 1);
+        nxt = __shfl_sync(FULL, nxt, 0);
+        if (nxt < uB) {
+          na = ldg(meta + 2 * nxt);
+          nb = ldg(meta + 2 * nxt + 1);
+        }
+#endif
+        u = nxt;
+        ma = na;
+        mb = nb;
+      }
+      __syncthreads();  // window and counters reused by the next segment
+      continue;
+    }
     UnitChunks uc{nullptr, 0};
     if (u < uB) uc = unit_chunks(g, u, lane);
     while (u < uB) {
