@@ -1084,6 +1084,10 @@ constexpr int ELL_XLEAD = CDK_ELL_XLEAD;
 #define CDK_ELL_MINBLOCKS 1  // resident ELL CTAs per SM (the planner launches SMs x this many)
 #endif
 constexpr int ELL_PART_CAP = 512 / CDK_ELL_MINBLOCKS;  // a segment's rblock partials in smem
+#ifndef CDK_ELL_META_CAP
+#define CDK_ELL_META_CAP 256  // unit records of a staged segment held in shared memory
+#endif
+constexpr int ELL_META_CAP = CDK_ELL_META_CAP;
 constexpr int ELL_DEPTH = CDK_ELL_DEPTH;
 constexpr int ELL_WARPS = ELL_THREADS / 32;
 constexpr int ELL_GROUPS = ELL_THREADS / 8;
@@ -1388,6 +1392,7 @@ struct EllSmem {
   double2 *sR;  // [SEG_MAX_COMM]
   int *next;    // rblock claim counter
   double2 *sP;  // [ELL_PART_CAP] the segment's rblock partials (community sums)
+  int4 *meta;   // [2 * ELL_META_CAP] the segment's unit records (cdk_graph.ell_meta)
 };
 
 // MODE: 0 RHS, 1..4 RK4 stage, 5 Euler (a runtime value: constant-folded in
@@ -1409,8 +1414,13 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
       fence_proxy_async_smem();  // earlier generic accesses before the async overwrite
       if (staged) {
         const uint32_t bw = (uint32_t)((w1 - w0) * 16);
-        mbar_expect_tx(sm.bar, bw);
+        // the segment's unit records ride along with the window (read from
+        // shared memory at each claim instead of L2)
+        const int nu = g.seg_unit[s + 1] - g.seg_unit[s];
+        const uint32_t bm = (g.ell_meta && nu <= ELL_META_CAP) ? (uint32_t)nu * 32u : 0u;
+        mbar_expect_tx(sm.bar, bw + bm);
         bulk_g2s(sm.zs, v.z_in + w0, bw, sm.bar);
+        if (bm) bulk_g2s(sm.meta, g.ell_meta + 8 * (int64_t)g.seg_unit[s], bm, sm.bar);
       }
       const int64_t eA = g.ell_off[rbA], eB = g.ell_off[rbB];
       prefetch_l2(g.ell_col + 8 * eA, (uint64_t)(eB - eA) * 16);
@@ -1463,11 +1473,13 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
     uint4 cq[ELL_DEPTH];
     int need = ELL_DEPTH;
     if (g.ell_meta) {  // packed metadata: the unit's description travels in registers
-      const int4 *meta = reinterpret_cast<const int4 *>(g.ell_meta);
+      const bool mloc = staged && uB - g.seg_unit[s] <= ELL_META_CAP;  // records in smem
+      const int4 *meta = mloc ? sm.meta - 2 * g.seg_unit[s]
+                              : reinterpret_cast<const int4 *>(g.ell_meta);
       int4 ma = make_int4(0, 0, 0, 0), mb = ma;
       if (u < uB) {
-        ma = ldg(meta + 2 * u);
-        mb = ldg(meta + 2 * u + 1);
+        ma = meta[2 * u];
+        mb = meta[2 * u + 1];
       }
       while (u < uB) {
         int nxt = 0;
@@ -1476,8 +1488,8 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
         if (lane == 0) nxt = atomicAdd(sm.next, 1);
         nxt = __shfl_sync(FULL, nxt, 0);
         if (nxt < uB) {
-          na = ldg(meta + 2 * nxt);
-          nb = ldg(meta + 2 * nxt + 1);
+          na = meta[2 * nxt];
+          nb = meta[2 * nxt + 1];
         }
 #endif
         const int ci = mb.w & 0xFF;  // community relative to the segment's first (255: pool)
@@ -1498,8 +1510,8 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
         if (lane == 0) nxt = atomicAdd(sm.next, 1);
         nxt = __shfl_sync(FULL, nxt, 0);
         if (nxt < uB) {
-          na = ldg(meta + 2 * nxt);
-          nb = ldg(meta + 2 * nxt + 1);
+          na = meta[2 * nxt];
+          nb = meta[2 * nxt + 1];
         }
 #endif
         u = nxt;
@@ -1562,9 +1574,11 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
 }
 
 __device__ __forceinline__ EllSmem ell_init(unsigned char *smem_raw, uint64_t *bar, double2 *sR,
-                                            int *next, double2 *sP, int smem_nodes) {
+                                            int *next, double2 *sP, int4 *meta,
+                                            int smem_nodes) {
   EllSmem sm;
   sm.sP = sP;
+  sm.meta = meta;
   sm.zs = reinterpret_cast<double2 *>(smem_raw);
   sm.bar = bar;
   sm.sR = sR;
@@ -1582,7 +1596,8 @@ __global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_stage_kern
   __shared__ double2 sR[SEG_MAX_COMM];
   __shared__ int next;
   __shared__ double2 sP[ELL_PART_CAP];
-  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, a.g.smem_nodes);
+  __shared__ __align__(16) int4 smeta[2 * ELL_META_CAP];
+  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, smeta, a.g.smem_nodes);
   uint32_t phase = 0;
   const unsigned long long t_cal = a.cta_cycles ? clock64() : 0ull;
 #ifdef CDK_PROFILE
@@ -1621,7 +1636,8 @@ __global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_rk4_kernel
   __shared__ double2 sR[SEG_MAX_COMM];
   __shared__ int next;
   __shared__ double2 sP[ELL_PART_CAP];
-  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, a.g.smem_nodes);
+  __shared__ __align__(16) int4 smeta[2 * ELL_META_CAP];
+  const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, smeta, a.g.smem_nodes);
   uint32_t phase = 0;
   unsigned int sync_idx = 0;
   const double h2 = dt / 2.0, h6 = dt / 6.0;
