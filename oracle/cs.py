@@ -48,3 +48,30 @@ def cs_rhs_cia(kern, pos, vel, dec, plan, K, sigma2, beta, norm):
     s = dec.correction
     kern.pairs_cs(s.iu, s.iv, pos, vel, 1.0 / norm, K, sigma2, beta, s.sgn, out)
     return out
+
+
+def full_edge_list(dec):
+    """(eu, ev) int64: every edge {u < v} of the graph D + S (permuted order):
+    the present intra-community pairs plus the inter edges — the direct sum's
+    input (SPEC.md:368-374)."""
+    s = dec.correction
+    off = dec.offsets
+    od = s.iu != s.iv
+    miss = od & (s.sgn < 0)
+    n = dec.n_nodes
+    mkey = np.sort(s.iu[miss] * n + s.iv[miss])
+    eus, evs = [], []
+    for c in range(dec.partition.n_comm):
+        idx = np.arange(off[c], off[c + 1], dtype=np.int64)
+        u, v = np.triu_indices(idx.shape[0], 1)
+        u, v = idx[u], idx[v]
+        key = u * n + v
+        pos = np.searchsorted(mkey, key)
+        pos = np.minimum(pos, max(mkey.shape[0] - 1, 0))
+        keep = mkey[pos] != key if mkey.shape[0] else np.ones(key.shape[0], bool)
+        eus.append(u[keep])
+        evs.append(v[keep])
+    inter = od & (s.sgn > 0)
+    eus.append(s.iu[inter])
+    evs.append(s.iv[inter])
+    return np.concatenate(eus), np.concatenate(evs)

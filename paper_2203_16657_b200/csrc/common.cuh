@@ -94,6 +94,12 @@ __device__ __forceinline__ void stcg_stream(double2 *a, double2 v, uint64_t pol)
                :: "l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
 }
 
+// status.reserved bit 0 (Kuramoto paths): a peer barrier timed out; the run
+// is aborted (kuramoto.cu peer_barrier)
+__device__ __forceinline__ bool run_aborted(const cdk_run_status *st) {
+  return (*reinterpret_cast<const volatile long long *>(&st->reserved) & 1ll) != 0;
+}
+
 // --- warp reductions (xor butterfly: every lane ends with the same bits) ----
 __device__ __forceinline__ double warp_sum(double v, int width = 32) {
   for (int o = width >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);

@@ -879,6 +879,7 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_stage_
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar_seg, bar_epi;
   __shared__ double2 sR[SEG_MAX_COMM];
+  if (a.n_peers > 1 && run_aborted(a.status)) return;  // a peer barrier timed out earlier
   const SegSmem sm = carve_smem(smem_raw, a.g.seg_rows_cap, a.g.smem_nodes);
   init_cta(a.g, sm, bar_seg, bar_epi);
   uint32_t parity = 0;
@@ -909,17 +910,20 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_stage_
 #define CDK_GRID_SLEEP_NS 0  // grid-barrier poll back-off (64 ns: release ~0.2 us later)
 #endif
 // grid-wide barrier for the cooperative (co-resident) persistent kernel:
-// monotone arrival counter, target = (sync index + 1) * gridDim.x
+// monotone arrival counter, target = (sync index + 1) * gridDim.x.  The test
+// is wrap-safe (serial-number arithmetic), so a launch may run more than
+// 2^32 / gridDim.x barriers.
 __device__ __forceinline__ void grid_sync(unsigned int *counter, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(counter, 1u);
     unsigned int v;
-    do {
+    for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-      if (v < target) __nanosleep(CDK_GRID_SLEEP_NS);
-    } while (v < target);
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(CDK_GRID_SLEEP_NS);
+    }
     __threadfence();
   }
   __syncthreads();
@@ -927,8 +931,10 @@ __device__ __forceinline__ void grid_sync(unsigned int *counter, unsigned int ta
 
 // System-scope counter barrier of the fused exchange: signal every rank
 // (its counter gets +1 from each rank per stage), then wait until this
-// rank's counter reaches `target`.  A 20 s watchdog turns a lost peer into a
-// status error instead of a hang.
+// rank's counter reaches `target`.  A 20 s watchdog turns a lost peer into
+// an ABORT: status.reserved bit 0 is set, the persistent kernels return at
+// their next grid barrier, later stage launches return at entry and later
+// peer barriers do not wait — one timeout ends the run (the host raises).
 struct PeerBar {
   unsigned int *const *bar;
   unsigned int *mine;
@@ -937,6 +943,7 @@ struct PeerBar {
 
 __device__ __forceinline__ void peer_barrier(const PeerBar &pb, unsigned int target,
                                              cdk_run_status *st) {
+  if (run_aborted(st)) return;
   __threadfence_system();
   for (int q = 0; q < pb.n; ++q) atomicAdd_system(pb.bar[q], 1u);
   if (!pb.wait) return;
@@ -995,6 +1002,7 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
       peer_target += (unsigned int)a.n_peers;                                          \
       if (blockIdx.x == 0 && threadIdx.x == 0) peer_barrier(ptr.pb, peer_target, a.status); \
       if (!(last)) grid_sync(ptr.bar, ++sync_idx * gridDim.x);                         \
+      if (run_aborted(a.status)) return;                                               \
     } else if (!(last)) {                                                              \
       grid_sync(ptr.bar, ++sync_idx * gridDim.x);                                      \
     }                                                                                  \
@@ -1597,6 +1605,7 @@ __global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_stage_kern
   __shared__ int next;
   __shared__ double2 sP[ELL_PART_CAP];
   __shared__ __align__(16) int4 smeta[2 * ELL_META_CAP];
+  if (a.n_peers > 1 && run_aborted(a.status)) return;  // a peer barrier timed out earlier
   const EllSmem sm = ell_init(smem_raw, &bar, sR, &next, sP, smeta, a.g.smem_nodes);
   uint32_t phase = 0;
   const unsigned long long t_cal = a.cta_cycles ? clock64() : 0ull;
@@ -1649,6 +1658,7 @@ __global__ void __launch_bounds__(ELL_THREADS, CDK_ELL_MINBLOCKS) ell_rk4_kernel
       peer_target += (unsigned int)a.n_peers;                                                \
       if (blockIdx.x == 0 && threadIdx.x == 0) peer_barrier(ptr.pb, peer_target, a.status);  \
       if (!(last)) grid_sync(ptr.bar, ++sync_idx * gridDim.x);                               \
+      if (run_aborted(a.status)) return;                                                     \
     } else if (!(last)) {                                                                    \
       grid_sync(ptr.bar, ++sync_idx * gridDim.x);                                            \
     }                                                                                        \

@@ -9,8 +9,9 @@
   rows (other rows empty), columns stay global, so inter-community neighbours
   are gathered from the rank's full copy of the stage state z.
 * After every stage kernel each rank has written z for its own rows; the ranks
-  exchange those slices with one group of NCCL broadcasts (an uneven
-  all-gather, `exchange_slices`).  That is the only collective: 16 B per node
+  exchange those slices with one NCCL all-gather of padded equal blocks
+  (`exchange_slices`), or — the default when every peer is reachable — the
+  stage epilogues store them straight into the peers' buffers over NVLink.  That is the only collective: 16 B per node
   per stage.
 * Row-owned, fixed-order accumulation + canonical community reductions make
   the trajectory bitwise identical for any rank count (tested with the
@@ -69,15 +70,35 @@ def partition_by_cost(off, n: int, cost, world: int) -> list[tuple[int, int]]:
 
 def exchange_slices(buf, ranges, rank: int, group=None) -> None:
     """Uneven all-gather along dim 0 of ``buf``: rank r owns buf[lo_r:hi_r];
-    afterwards every rank holds every slice.  One group of broadcasts."""
+    afterwards every rank holds every slice.  ONE all-gather of equal,
+    padded blocks (max slice length), then one index copy back into place."""
+    import torch
     import torch.distributed as dist
 
-    work = []
-    for src, (lo, hi) in enumerate(ranges):
-        if hi > lo:
-            work.append(dist.broadcast(buf[lo:hi], src=src, group=group, async_op=True))
-    for w in work:
-        w.wait()
+    world = len(ranges)
+    if world == 1:
+        return
+    lens = [hi - lo for lo, hi in ranges]
+    L = max(max(lens), 1)
+    tail = tuple(buf.shape[1:])
+    key = (buf.device, buf.dtype, L, tail, tuple(ranges))
+    cache = _EXCHANGE_CACHE.get(key)
+    if cache is None:
+        send = torch.zeros((L,) + tail, dtype=buf.dtype, device=buf.device)
+        recv = torch.empty((world * L,) + tail, dtype=buf.dtype, device=buf.device)
+        src = torch.cat([torch.arange(r * L, r * L + n) for r, n in enumerate(lens)])
+        dst = torch.cat([torch.arange(lo, hi) for lo, hi in ranges])
+        cache = (send, recv, src.to(buf.device), dst.to(buf.device))
+        _EXCHANGE_CACHE.clear()
+        _EXCHANGE_CACHE[key] = cache
+    send, recv, src, dst = cache
+    lo, hi = ranges[rank]
+    send[: hi - lo].copy_(buf[lo:hi])
+    dist.all_gather_into_tensor(recv, send, group=group)
+    buf.index_copy_(0, dst, recv.index_select(0, src))
+
+
+_EXCHANGE_CACHE: dict = {}
 
 
 def workspace_offsets(engine: KuramotoEngine) -> list[int]:
@@ -226,9 +247,11 @@ class ShardedKuramotoEngine:
             for s in range(1, 5):
                 self.eng.rk4_stage(dt, s, stream=stream)
                 self._exchange(s & 1, stream)
-        _lib.check(self.eng.lib.cdk_kuramoto_advance(ctypes.byref(self.graph.struct),
-                                                     self.eng.workspace.data_ptr(), int(n_steps),
-                                                     _lib.stream_ptr(stream)), "advance")
+            # per step, so a blow-up is reported at its own step (stage
+            # kernels count from status.steps_done)
+            _lib.check(self.eng.lib.cdk_kuramoto_advance(ctypes.byref(self.graph.struct),
+                                                         self.eng.workspace.data_ptr(), 1,
+                                                         _lib.stream_ptr(stream)), "advance")
 
     def gather_theta(self):
         """Full theta on every rank (own slices exchanged)."""
@@ -305,6 +328,9 @@ class VirtualCluster:
                     for e, _ in self.ranks:
                         e.rk4_stage(dt, s)
                     self._exchange(s & 1)
+            for e, _ in self.ranks:
+                _lib.check(e.lib.cdk_kuramoto_advance(ctypes.byref(e.graph.struct),
+                                                      e.workspace.data_ptr(), 1, None), "advance")
 
     def theta(self):
         import torch

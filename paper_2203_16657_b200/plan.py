@@ -624,7 +624,7 @@ def _ell_meta(lay: HostLayout, sch: Schedule, ell_off, xell_off, units, seg_unit
     c = lay.rblk_comm[rb].astype(np.int64)
     cA = lay.rblk_comm[sch.seg_rblk[seg]].astype(np.int64)
     ci = np.where(c >= 0, c - cA, 255)
-    if np.any((ci < 0) | ((ci > SEG_MAX_COMM) & (ci != 255))) or np.any(P > 255):
+    if np.any((ci < 0) | ((ci >= SEG_MAX_COMM) & (ci != 255))) or np.any(P > 255):
         return None
     meta[:, 0] = ell_off[rb] + 32 * ch0
     meta[:, 1] = xell_off[rb]

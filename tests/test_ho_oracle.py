@@ -85,3 +85,26 @@ def test_config3_scaled_oracles_agree():
     kd = oh.ho_rhs_direct(theta0, omega, A, c.k1, c.k2)
     kc = oh.ho_rhs_cia(theta0, omega, dec, c.k1, c.k2, inter_triangles=ho.spanning_triangles(dec))
     assert np.abs(kd - kc).max() <= 1e-12
+
+
+@pytest.mark.parametrize("seed,pool", [(0, 0), (5, 9)])
+def test_precomputed_cia_oracle_equals_restatement(seed, pool):
+    """oracle.ho.HoCia (enumerated missing and spanning triangles, used for
+    the long-horizon config-3 fixture) equals ho_rhs_cia and the literal sum."""
+    rng = np.random.default_rng(seed)
+    g, part = G.planted_partition_graph([45, 30, 50, 4, 1], 0.7, 0.1, seed)
+    if pool:
+        part = _with_pool(g, part, rng, pool)
+    dec = G.decompose(g, part)
+    orc = oh.HoCia(dec)
+    span = ho.spanning_triangles(dec)
+    assert {tuple(t) for t in orc.span.tolist()} == {tuple(t) for t in span.tolist()}
+    mt = ho.missing_triangles(dec)
+    assert {tuple(t) for t in orc.tri.tolist()} == {tuple(t) for t in mt.tolist()}
+    A = g.dense()[np.ix_(part.perm, part.perm)]
+    th = rng.uniform(-math.pi, math.pi, g.n_nodes)
+    om = rng.standard_normal(g.n_nodes)
+    kd = oh.ho_rhs_direct(th, om, A, 1.0, 0.5)
+    kc = orc.rhs(th, om, 1.0, 0.5)
+    assert np.abs(kd - kc).max() <= 1e-12
+    assert np.abs(kc - oh.ho_rhs_cia(th, om, dec, 1.0, 0.5, inter_triangles=span)).max() <= 1e-13
