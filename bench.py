@@ -9,18 +9,26 @@ node-update = one node advanced by one full RK4 step (4 CIA RHS evaluations).
 Timing protocol (ours):
 * inputs (graph CSR, theta, omega) resident in HBM before the timed region;
 * every timed step is one replay of a captured CUDA graph holding one RK4 step
-  (4 fused stage kernels + 1 bookkeeping kernel); L2 (126 MB) is FLUSHED
-  before every step by writing a 512 MB buffer outside the events, so each
-  step streams its CSR from HBM in stage 1 (config 2's inputs, ~60 MB
-  compressed, are smaller than L2);
+  (the persistent RK4 kernel: 4 fused stages with grid barriers, + 1
+  bookkeeping kernel); L2 (126 MB) is FLUSHED before every step by writing a
+  512 MB buffer outside the events, so each step streams its CSR from HBM in
+  stage 1 (config 2's inputs, ~60 MB compressed, are smaller than L2);
 * CUDA events on the launching stream, barrier + synchronize on both sides,
   max over ranks; value = N x K / sum(step times).
-Extra keys: roofline of the dominant (stage) kernel, the CPU baseline (oracle
-C port, 1 thread, bounded sample), e2e through the public integrate() API
-with host arrays, clocks sampled during the run, gpu_launches.
+Extra keys: roofline of the timed kernel (4 x canonical RHS bytes per launch
+/ measured step time), the CPU baseline (the REAL reference, baseline/_ref
+commdyn with its numba kernels as shipped, pinned to one core, bounded
+sample), e2e through the public integrate() API with host arrays, clocks
+sampled during the run, gpu_launches.
 
---impl reference times the reference algorithm's CPU implementation (the
-oracle C port of commdyn/_kernels.py, all host threads) on the same config.
+--impl reference runs the unmodified reference (baseline/_ref/commdyn, numba
+backend as shipped: single-threaded kernels) through its own public kernel
+dispatchers, composed by the SPEC orchestration (oracle/cia.py), on the same
+config; if baseline/_ref is absent it falls back to the oracle C port with
+all host threads and says so.
+
+--gpus N without WORLD_SIZE in the environment launches N ranks itself
+(torch.distributed.run on 127.0.0.1), as the driver does for its scaling run.
 """
 
 from __future__ import annotations
@@ -52,9 +60,10 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic_bytes(kernel: str = "stage_kernel"):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the stage kernel from the
-    committed `ncu --set full` capture (profiles/rNN_<kernel>_ncu_raw.csv)."""
+def ncu_traffic_bytes(kernel: str = "ell_rk4_kernel"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of ``kernel``
+    from the committed `ncu --set full` capture of the same build
+    (profiles/rNN_<kernel>_ncu_raw.csv, the newest round)."""
     import csv
     import glob
 
@@ -155,58 +164,138 @@ def _max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_baseline_sample(case, dec, omega, theta0, steps: int = 3, threads: int = 1):
-    """Oracle C port (restatement of commdyn/_kernels.py, numba's single-thread
-    order) over `steps` full RK4 steps of the whole graph."""
-    from oracle import cia
-    from oracle import kernels as K
+def load_reference():
+    """The unmodified reference package installed under baseline/_ref (pip
+    --target).  Returns (commdyn._kernels, backend name) or
+    (None, why).  numba's JIT cache goes to a writable temp dir
+    (commdyn/_backend.py:61-63 compiles with cache=True)."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref_dir, "commdyn", "_kernels.py")):
+        return None, "baseline/_ref/commdyn not installed"
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/commdyn_numba_cache")
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    saved = os.environ.pop("COMMDYN_BACKEND", None)  # reference default: numba if importable
+    try:
+        from commdyn import _backend as rb, _kernels as rk
+    except Exception as e:  # noqa: BLE001
+        return None, f"import failed: {e}"
+    finally:
+        if saved is not None:
+            os.environ["COMMDYN_BACKEND"] = saved
+    return rk, rb.backend()
 
-    K.set_threads(threads)
+
+def _cpu_rk4_rate(kern, case, dec, omega, theta0, steps: int):
+    """``steps`` full RK4 steps of the whole graph through ``kern``'s
+    dispatchers (order_params_blocks + dense_complex + pairs_trig), SPEC
+    orchestration of oracle/cia.py.  Returns (node-updates/s, seconds)."""
+    from oracle import cia
+
     s = dec.correction
 
     def rhs(x):
-        return cia.kuramoto_rhs_cia(K, x, omega, dec.offsets, s.iu, s.iv, s.sgn, case.coupling,
-                                    case.n)
+        return cia.kuramoto_rhs_cia(kern, x, omega, dec.offsets, s.iu, s.iv, s.sgn,
+                                    case.coupling, case.n)
 
-    rhs(theta0[: case.n])  # warm (page-in)
     t = time.perf_counter()
     cia.rk4_integrate(rhs, theta0, case.dt, steps)
     el = time.perf_counter() - t
-    K.set_threads(1)
     return case.n * steps / el, el
+
+
+def _warm_reference(kern):
+    """Compile the reference's numba kernels on a tiny input (outside timing)."""
+    from oracle import cia
+
+    x = np.linspace(-3, 3, 8)
+    off = np.array([0, 4, 8], dtype=np.int64)
+    iu = np.array([0, 1], dtype=np.int64)
+    iv = np.array([1, 5], dtype=np.int64)
+    cia.kuramoto_rhs_cia(kern, x, np.zeros(8), off, iu, iv, np.array([-1.0, 1.0]), 1.0, 8)
+
+
+def cpu_baseline_sample(case, dec, omega, theta0, steps: int = 3):
+    """The real reference (baseline/_ref commdyn, numba as shipped) pinned to
+    ONE host core (taskset -c 0 equivalent via
+    sched_setaffinity), JIT warmed first; falls back to the oracle C port
+    (1 thread) when baseline/_ref is absent.  Returns the cpu_baseline dict."""
+    kern, backend = load_reference()
+    kind = "reference"
+    if kern is None:
+        from oracle import kernels as kern  # noqa: N813
+
+        kern.set_threads(1)
+        kind, backend = "port", f"oracle C port ({backend})"
+    else:
+        _warm_reference(kern)
+    aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    try:
+        if aff:
+            os.sched_setaffinity(0, {min(aff)})
+        rate, el = _cpu_rk4_rate(kern, case, dec, omega, theta0, steps)
+    finally:
+        if aff:
+            os.sched_setaffinity(0, aff)
+    src = ("baseline/_ref commdyn._kernels (unmodified reference, numba backend, "
+           "single-threaded as shipped)" if kind == "reference" else backend)
+    return {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{steps} full RK4 steps of config 2 ({el:.1f} s) through {src}, "
+                      f"SPEC orchestration (oracle/cia.py), pinned to 1 of {os.cpu_count()} "
+                      "host cores"}
+
+
+def cfg2_config(case, dec):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": "cfg2 Kuramoto CIA RK4, SBM N=200000, 200 power-law communities, "
+                        "p_in .95, inter degree 5, K=5 (global 1/N), dt .01",
+            "n_nodes": case.n, "n_comm": int(len(case.sizes)), "nnz_dir": int(dec.nnz_dir),
+            "dt": case.dt, "l2": "GPU arm: L2 flushed (512 MB write) before every timed step"}
 
 
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
         return 0
-    from oracle import kernels as K
     from paper_2203_16657_b200 import configs
 
     case = configs.config2()
     dec = case.decomposition()
     omega, theta0 = case.state()
-    threads = max(1, os.cpu_count() or 1)
-    # per-step cost probe, then bound the run to a few minutes
-    rate1, el1 = cpu_baseline_sample(case, dec, omega, theta0, steps=1, threads=threads)
-    budget_s = 150.0
-    steps = int(max(1, min(args.steps, budget_s // max(el1, 1e-3))))
-    warm = min(args.warmup, 1)
-    if warm:
-        cpu_baseline_sample(case, dec, omega, theta0, steps=warm, threads=threads)
-    rate, el = cpu_baseline_sample(case, dec, omega, theta0, steps=steps, threads=threads)
-    sample = (f"{steps} full RK4 step(s) of config 2 (N={case.n}, nnz_dir={dec.nnz_dir}) "
-              f"of the requested {args.steps}; oracle C port of commdyn/_kernels.py "
-              f"(pairs_trig OpenMP per-thread buffers), {threads} threads")
+    kern, backend = load_reference()
+    if kern is not None:
+        _warm_reference(kern)
+        kind, cores = "reference", 1
+        src = (f"baseline/_ref commdyn._kernels (unmodified reference, {backend} backend; its "
+               "kernels are single-threaded as shipped, _kernels.py:4-6)")
+    else:
+        from oracle import kernels as kern  # noqa: N813
+
+        cores = max(1, os.cpu_count() or 1)
+        kern.set_threads(cores)
+        kind = "port"
+        src = (f"oracle C port of commdyn/_kernels.py, {cores} OpenMP threads "
+               f"(reference unavailable: {backend})")
+    W, K = args.warmup, args.steps
+    t_w = 0.0
+    if W:
+        _, t_w = _cpu_rk4_rate(kern, case, dec, omega, theta0, W)
+    per_step = t_w / W if W else None
+    budget_s = 900.0
+    if per_step is None:
+        _, per_step = _cpu_rk4_rate(kern, case, dec, omega, theta0, 1)
+    steps = int(max(1, min(K, budget_s // max(per_step, 1e-3))))
+    rate, el = _cpu_rk4_rate(kern, case, dec, omega, theta0, steps)
+    sample = (f"{steps} full RK4 steps of config 2 (N={case.n}, nnz_dir={dec.nnz_dir}) after "
+              f"{W} warm-up steps, from theta0; {src}; SPEC orchestration (oracle/cia.py)"
+              + ("" if steps == K else f"; bounded to {budget_s:.0f} s of the requested {K}"))
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-        "warmup": warm, "ms_per_step": 1e3 * el / steps, "higher_is_better": True,
+        "warmup": W, "ms_per_step": 1e3 * el / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "cfg2 Kuramoto CIA RK4, SBM N=200000, 200 power-law communities, "
-                   "p_in .95, inter degree 5, dt .01", "n_nodes": case.n,
-                   "nnz_dir": dec.nnz_dir, "parallelism": "host threads"},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+        "config": cfg2_config(case, dec),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -288,33 +377,10 @@ def run_ours(args):
         eng.check()
         total_ms = _max_over_ranks(float(np.sum(step_ms)), world)
 
-        # --- roofline pass: the stage kernel alone.  Each stage is its own
-        #     captured graph; the L2 flush before every step keeps the GPU
-        #     busy while the host enqueues, so the events bracket kernel time.
-        eng.set_state(theta0)
-        stage_graphs = []
-        torch.cuda.synchronize()
-        for st_i in range(1, 5):
-            sg = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(sg, stream=stream):
-                eng.rk4_stage(dt, st_i, stream=stream)
-            stage_graphs.append(sg)
-        eng.set_state(theta0)
-        torch.cuda.synchronize()
-        Kr = min(K, 200)
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(Kr)]
-        for i in range(Kr):
-            flush_l2()
-            ev[i][0].record(cur)
-            for st_i in range(4):
-                stage_graphs[st_i].replay()
-                ev[i][st_i + 1].record(cur)
-        torch.cuda.synchronize()
-        stage_ms = np.array([[ev[i][s_ - 1].elapsed_time(ev[i][s_]) for s_ in range(1, 5)]
-                             for i in range(Kr)])
-
-        # --- e2e: public API with host arrays (fresh model: omega + theta0 uploaded,
-        #     final state read back), inside the timed region
+        # --- e2e: the public API with host arrays (a fresh model object: omega
+        #     and theta0 uploaded from the host, the final state read back),
+        #     inside the timed region; the decomposition's device graph is
+        #     already resident (it is part of the problem setup, like the CSR)
         from paper_2203_16657_b200 import IntegrationPlan, integrate, kuramoto_model
 
         dec._cache["device_graph"] = dg
@@ -331,54 +397,46 @@ def run_ours(args):
         e2e_s = min(e2e_times)
     clocks = sampler.summary()
 
-    # parity spot check of the timed trajectory vs the e2e run (same K steps)
     if not np.all(np.isfinite(final)):
         raise RuntimeError("non-finite final state")
 
     value = n * K / (total_ms / 1e3)
     b_rhs = algorithmic_bytes_per_rhs(n, nnz)
-    stage_mean_ms = float(stage_ms.mean())
-    stage1_ms = float(stage_ms[:, 0].mean())
+    ell = bool(dg.struct.ell_off)
+    kernel = "ell_rk4_kernel" if ell else "kuramoto_rk4_kernel"
+    # one launch of the timed kernel = one RK4 step = 4 RHS stages; its
+    # duration is the timed step (the bookkeeping kernel adds ~2 us)
+    launch_ms = float(np.mean(step_ms))
     peak, peak_kind = _peaks()
-    achieved = b_rhs / (stage_mean_ms / 1e3) / 1e9
-    kernel = "ell_stage_kernel" if dg.struct.ell_off else "kuramoto_stage_kernel"
-    traffic, traffic_src = ncu_traffic_bytes("ell_stage_kernel" if dg.struct.ell_off
-                                             else "stage_kernel")
+    achieved = 4 * b_rhs / (launch_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic_bytes(kernel)
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": "cfg2 Kuramoto CIA RK4, SBM N=200000, 200 power-law communities, "
-                        "p_in .95, inter degree 5, dt .01",
-            "n_nodes": n, "n_comm": len(case.sizes), "nnz_dir": nnz,
-            "csr_device_bytes": dg.device_bytes(), "l2": "flushed (512 MB write) before every "
-            "timed step", "parallelism": f"dp{world} (replicas)" if world > 1 else "1 GPU",
-            "graph_gen_s": round(t_gen, 2), "plan_build_s": round(t_plan, 2),
-        },
+        "config": cfg2_config(case, dec),
+        "setup": {"csr_device_bytes": dg.device_bytes(), "graph_gen_s": round(t_gen, 2),
+                  "plan_build_s": round(t_plan, 2), "parallelism": "1 GPU"},
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-            "peak_kind": peak_kind,
-            "kernel": kernel, "algorithmic_bytes_per_launch": b_rhs,
-            "stage_ms_mean": stage_mean_ms, "stage1_ms_mean": stage1_ms,
-            "stage_ms_by_stage": [float(x) for x in stage_ms.mean(axis=0)],
+            "peak_kind": peak_kind, "kernel": kernel,
+            "algorithmic_bytes_per_launch": 4 * b_rhs,
+            "algorithmic_bytes_per_rhs": b_rhs,
+            "launch_ms_mean": launch_ms,
+            "note": "one launch = one RK4 step (4 fused stages); achieved = 4 B_rhs / mean "
+                    "timed step (CUDA events, L2 flushed before each step)",
         },
         "e2e": {"value": n * K / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(2 * 8 * n / K),
                 "d2h_bytes_per_step": int(2 * 8 * n / K),
                 "note": "integrate() via the public API: omega + theta0 from host, "
-                        "initial + final states back to host; CSR already on device"},
+                        "initial + final states back to host; device graph already resident"},
         "gpu_launches": launches,
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, el = cpu_baseline_sample(case, dec, omega, theta0, steps=args.cpu_steps, threads=1)
-        res["cpu_baseline"] = {
-            "value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{args.cpu_steps} full RK4 steps of config 2 ({el:.1f} s), oracle C port "
-                      "of commdyn/_kernels.py, single thread as the reference's numba kernels",
-        }
+        res["cpu_baseline"] = cpu_baseline_sample(case, dec, omega, theta0, steps=args.cpu_steps)
     if rank == 0:
         print(json.dumps(res), flush=True)
     return 0
@@ -536,6 +594,21 @@ def run_cfg5(args):
     return 0
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` run directly: launch N ranks on this node exactly as
+    the driver does (torch.distributed.run, 127.0.0.1, a free port); rank 0
+    prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -548,6 +621,8 @@ def main():
                     help="cfg2 = the metric's config (default); cfg5 = the LFR-style N=8e6 "
                          "config (steps default 200)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.config == "cfg5":
         if args.impl != "reference" and (int(os.environ.get("WORLD_SIZE", "1")) > 1
                                          or os.environ.get("CDK_BENCH_SHARDED") == "1"):

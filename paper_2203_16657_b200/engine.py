@@ -51,6 +51,20 @@ class KuramotoEngine:
         self._gp = ctypes.byref(self.graph.struct)
         self._rhs_ws = None
 
+    def set_params(self, omega, coupling: float, norm: float) -> None:
+        """New model parameters on the same graph and workspace (the public API
+        reuses one engine per decomposition across model objects)."""
+        import torch
+
+        omega = torch.as_tensor(np.asarray(omega, dtype=np.float64) if not torch.is_tensor(omega)
+                                else omega, dtype=torch.float64)
+        if omega.shape != (self.n,):
+            raise InputError(f"omega must have shape ({self.n},)")
+        self.omega.copy_(omega, non_blocking=True)
+        self.coupling = float(coupling)
+        self.norm = float(norm)
+        self.k_over_n = self.coupling / self.norm
+
     # -- state --------------------------------------------------------------
     def set_state(self, theta, stream=None) -> None:
         import torch

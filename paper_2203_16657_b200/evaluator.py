@@ -27,16 +27,25 @@ NAIVE_N_CAP = 2**15
 
 
 def _engine(model: Kuramoto, dec: Decomposition) -> KuramotoEngine:
+    """One engine (device graph + workspace) per decomposition; a different
+    model object only re-uploads omega and the coupling constants."""
     cached = dec._cache.get("engine")  # (model, engine) of the most recent model
-    eng = cached[1] if cached is not None and cached[0] is model else None
-    if eng is None:
-        perm = dec.partition.perm
+    if cached is not None and cached[0] is model:
+        return cached[1]
+    perm = dec.partition.perm
+    omega = np.asarray(model.omega, dtype=np.float64)
+    if omega.shape != (dec.n_nodes,):
+        raise InputError("omega shape does not match the decomposition")
+    if cached is not None:
+        eng = cached[1]
+        eng.set_params(omega[perm], model.coupling, model.norm_value())
+    else:
         dg = dec._cache.get("device_graph")
         if dg is None:
             dg = dec._cache["device_graph"] = DeviceGraph(dec)
-        eng = KuramotoEngine(dec, np.asarray(model.omega)[perm], coupling=model.coupling,
+        eng = KuramotoEngine(dec, omega[perm], coupling=model.coupling,
                              norm=model.norm_value(), graph=dg)
-        dec._cache["engine"] = (model, eng)
+    dec._cache["engine"] = (model, eng)
     return eng
 
 
@@ -68,9 +77,16 @@ def engine_for(model, dec: Decomposition):
 
 
 def _cs_engine(model, dec: Decomposition, pos_perm, vel_perm, t_end: float):
+    """The P2 fit (centres, scales, polynomial) depends on the initial state and
+    the horizon, so the cache key carries a fingerprint of both: a cached
+    engine is reused only for the same model, horizon and initial state."""
+    import hashlib
+
     from .cs import CSEngine
 
-    key = ("cs_engine", id(model), float(t_end))
+    h = hashlib.sha1(np.ascontiguousarray(pos_perm, np.float64).tobytes())
+    h.update(np.ascontiguousarray(vel_perm, np.float64).tobytes())
+    key = ("cs_engine", id(model), float(t_end), h.hexdigest())
     cached = dec._cache.get("cs_engine")
     if cached is not None and cached[0] == key and cached[1] is model:
         eng = cached[2]
