@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 12
+#define CDK_ABI_VERSION 13
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -81,6 +81,26 @@ CDK_API int cdk_moments_blocks(const double *x, const int64_t *offsets, int64_t 
 /* replaces dense_poly, _kernels.py:231-235 (:207-217). */
 CDK_API int cdk_dense_poly(const double *x, const int64_t *offsets, int64_t m_comm, const double *tbl,
                    int p, double scale, double shift, double *out, void *stream);
+
+/* replaces pairs_poly, _kernels.py:365-369 (:264-271, :286-294).  coef f64[p+1]. */
+CDK_API int cdk_pairs_poly(const int64_t *iu, const int64_t *iv, int64_t n_pairs, const double *x,
+                   double inv_n, const double *coef, int p, double x0, const double *sgn,
+                   double *out, void *stream);
+
+/* replaces ho_naive_block, _kernels.py:424-428 (:398-410).  theta, out f64[lam],
+ * lam <= 4096 (the literal O(lam^4) oracle; one thread per m). */
+CDK_API int cdk_ho_naive_block(const double *theta, int64_t lam, double l1, double l2, double l3,
+                       double l4, double *out, void *stream);
+
+/* replaces nn_recurrence, _kernels.py:472-477 (:436-456).  ph, f c128[n]; one
+ * thread per anchored segment, same additions in the same order. */
+CDK_API int cdk_nn_recurrence(const double *ph, int64_t n, int64_t k, double inv_n,
+                      int64_t anchor_every, double *f, void *stream);
+
+/* replaces spin_field_sums, _kernels.py:505-509 (:485-502).  spins, f int64[n];
+ * scratch: 8 device bytes. */
+CDK_API int cdk_spin_field_sums(const int64_t *spins, int64_t n, int64_t *f, void *scratch,
+                        void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* Fused CIA path: Kuramoto RHS (E1 + E2) inside RK4 stages.                */

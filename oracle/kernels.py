@@ -57,6 +57,9 @@ def _load():
         lib.or_moments_blocks.argtypes = [P, P, I64, I, D, D, P]
         lib.or_dense_poly.argtypes = [P, P, I64, P, I, D, D, P]
         lib.or_ho_naive_block.argtypes = [P, I64, D, D, D, D, P]
+        lib.or_pairs_poly.argtypes = [P, P, I64, P, D, P, I, D, P, P]
+        lib.or_nn_recurrence.argtypes = [P, I64, I64, D, I64, P]
+        lib.or_spin_field_sums.argtypes = [P, I64, P]
         lib.or_num_threads.restype = I
         _lib = lib
     return _lib
@@ -177,3 +180,34 @@ def ho_naive_block(theta, lambdas):
     out = np.empty(th.shape[0], dtype=np.float64)
     lib.or_ho_naive_block(thp, th.shape[0], l1, l2, l3, l4, out.ctypes.data)
     return out
+
+
+def pairs_poly(iu, iv, x, inv_n, coef, x0, sgn, out):
+    """_kernels.py:365-369 -> :286-294 (+ :264-271)."""
+    lib = _load()
+    iu, iup = _i64(iu)
+    iv, ivp = _i64(iv)
+    x, xp = _f64(x)
+    c, cp = _f64(coef)
+    sg, sgp = _f64(sgn)
+    lib.or_pairs_poly(iup, ivp, iu.shape[0], xp, float(inv_n), cp, c.shape[0] - 1, float(x0),
+                      sgp, _check_out(out))
+
+
+def nn_recurrence(ph, k, inv_n, anchor_every=1024):
+    """_kernels.py:472-477 -> :436-456."""
+    lib = _load()
+    ph = np.ascontiguousarray(ph, dtype=np.complex128)
+    f = np.empty_like(ph)
+    lib.or_nn_recurrence(ph.ctypes.data, ph.shape[0], int(k), float(inv_n), int(anchor_every),
+                         f.ctypes.data)
+    return f
+
+
+def spin_field_sums(spins):
+    """_kernels.py:505-509 -> :485-495."""
+    lib = _load()
+    s, sp = _i64(spins)
+    f = np.empty(s.shape[0], dtype=np.int64)
+    lib.or_spin_field_sums(sp, s.shape[0], f.ctypes.data)
+    return f

@@ -171,3 +171,58 @@ def dense_poly(x, offsets, tbl, scale, shift, out):
                                 tt.shape[1] - 1, float(scale), float(shift), o.t.data_ptr(),
                                 _lib.stream_ptr()), "dense_poly")
     o.finish()
+
+
+def pairs_poly(iu, iv, x, inv_n, coef, x0, sgn, out):
+    """replaces _kernels.py:365-369 (Desai-Zwanzig polynomial coupling)."""
+    import torch
+
+    L = _lib.lib()
+    it, vt = _dev(iu, torch.int64), _dev(iv, torch.int64)
+    xt = _dev(x, torch.float64)
+    ct = _dev(coef, torch.float64)
+    st = _dev(sgn, torch.float64)
+    o = _Out(out)
+    _lib.check(L.cdk_pairs_poly(it.data_ptr(), vt.data_ptr(), it.shape[0], xt.data_ptr(),
+                                float(inv_n), ct.data_ptr(), ct.shape[0] - 1, float(x0),
+                                st.data_ptr(), o.t.data_ptr(), _lib.stream_ptr()), "pairs_poly")
+    o.finish()
+
+
+def ho_naive_block(theta, lambdas):
+    """replaces _kernels.py:424-428 (literal quadruple loop; lam <= 4096)."""
+    import torch
+
+    L = _lib.lib()
+    l1, l2, l3, l4 = (float(v) for v in lambdas)
+    tt = _dev(theta, torch.float64)
+    out = torch.empty_like(tt)
+    _lib.check(L.cdk_ho_naive_block(tt.data_ptr(), tt.shape[0], l1, l2, l3, l4, out.data_ptr(),
+                                    _lib.stream_ptr()), "ho_naive_block")
+    return out if torch.is_tensor(theta) else out.cpu().numpy()
+
+
+def nn_recurrence(ph, k, inv_n, anchor_every=1024):
+    """replaces _kernels.py:472-477 (window sums, re-anchored recurrence)."""
+    import torch
+
+    L = _lib.lib()
+    pt = _dev(ph, torch.complex128)
+    f = torch.empty_like(pt)
+    _lib.check(L.cdk_nn_recurrence(pt.data_ptr(), pt.shape[0], int(k), float(inv_n),
+                                   int(anchor_every), f.data_ptr(), _lib.stream_ptr()),
+               "nn_recurrence")
+    return f if torch.is_tensor(ph) else f.cpu().numpy()
+
+
+def spin_field_sums(spins):
+    """replaces _kernels.py:505-509 (per-node sum over all spins, int64)."""
+    import torch
+
+    L = _lib.lib()
+    st = _dev(spins, torch.int64)
+    f = torch.empty_like(st)
+    scratch = torch.empty(1, dtype=torch.int64, device=st.device)
+    _lib.check(L.cdk_spin_field_sums(st.data_ptr(), st.shape[0], f.data_ptr(),
+                                     scratch.data_ptr(), _lib.stream_ptr()), "spin_field_sums")
+    return f if torch.is_tensor(spins) else f.cpu().numpy()

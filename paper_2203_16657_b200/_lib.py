@@ -142,6 +142,10 @@ _SIGS = {
     "cdk_pairs_cs": [P, P, I64, P, P, I, D, D, D, D, P, P, P],
     "cdk_moments_blocks": [P, P, I64, I, D, D, P, P],
     "cdk_dense_poly": [P, P, I64, P, I, D, D, P, P],
+    "cdk_pairs_poly": [P, P, I64, P, D, P, I, D, P, P, P],
+    "cdk_ho_naive_block": [P, I64, D, D, D, D, P, P],
+    "cdk_nn_recurrence": [P, I64, I64, D, I64, P, P],
+    "cdk_spin_field_sums": [P, I64, P, P, P],
     "cdk_kuramoto_workspace_bytes": [ctypes.POINTER(CdkGraph)],
     "cdk_kuramoto_prepare": [ctypes.POINTER(CdkGraph), P, P, P],
     "cdk_kuramoto_rhs": [ctypes.POINTER(CdkGraph), P, P, D, P, P, P],
@@ -202,7 +206,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 12
+ABI_VERSION = 13
 
 _lock = threading.Lock()
 _lib = None

@@ -3,6 +3,8 @@
 // trajectory hot path does NOT use these (it runs the fused kernels in
 // kuramoto.cu); they exist so every reference dispatcher on the path has a
 // device counterpart.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cdk {
@@ -217,6 +219,95 @@ __global__ void dense_poly_kernel(const double *x, const int64_t *offsets, int64
   out[m] += val;
 }
 
+// _kernels.py:264-271,286-294 (poly coupling over pairs; Horner as
+// _poly_eval_nb; scatter to both ends with fp64 atomics like pairs_trig)
+__global__ void pairs_poly_kernel(const int64_t *iu, const int64_t *iv, int64_t n_pairs,
+                                  const double *x, double inv_n, const double *coef, int p,
+                                  double x0, const double *sgn, double *out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_pairs) return;
+  const int64_t u = iu[e], v = iv[e];
+  const double s = sgn[e] * inv_n;
+  const double d = x[v] - x[u];
+  // no FMA contraction (the reference's numba body rounds every * and +)
+  double t = d - x0, val = coef[p];
+  for (int a = p - 1; a >= 0; --a) val = __dadd_rn(__dmul_rn(val, t), coef[a]);
+  atomicAdd(out + u, s * val);
+  if (u != v) {
+    t = -d - x0;
+    val = coef[p];
+    for (int a = p - 1; a >= 0; --a) val = __dadd_rn(__dmul_rn(val, t), coef[a]);
+    atomicAdd(out + v, s * val);
+  }
+}
+
+// _kernels.py:398-410: out[m] = (1/lam^3) sum_{i1,i2,i3} sin(l1 th1 + l2 th2 +
+// l3 th3 + l4 th_m).  One thread per m walks (i1, i2, i3) in the reference's
+// order, so every out[m] sums its terms in the same sequence; theta staged in
+// shared memory (lam <= 4096).
+constexpr int HO_NAIVE_MAX = 4096;
+__global__ void ho_naive_block_kernel(const double *theta, int lam, double l1, double l2,
+                                      double l3, double l4, double *out) {
+  __shared__ double th[HO_NAIVE_MAX];
+  for (int i = threadIdx.x; i < lam; i += blockDim.x) th[i] = theta[i];
+  __syncthreads();
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= lam) return;
+  const double am = l4 * th[m];
+  double acc = 0.0;
+  for (int i1 = 0; i1 < lam; ++i1) {
+    const double a1 = l1 * th[i1];
+    for (int i2 = 0; i2 < lam; ++i2) {
+      const double a12 = __dadd_rn(a1, __dmul_rn(l2, th[i2]));
+      for (int i3 = 0; i3 < lam; ++i3) acc += sin(__dadd_rn(a12, __dmul_rn(l3, th[i3])) + am);
+    }
+  }
+  const double l3d = (double)lam * (double)lam * (double)lam;
+  out[m] = acc / l3d;
+}
+
+// _kernels.py:436-456: window sums F_m = inv_n sum_{l=m-k..m+k} ph[l mod n]
+// with the O(1) update, re-anchored by a direct sum every anchor_every steps.
+// Anchored segments are independent, so one thread per segment reproduces the
+// reference's arithmetic exactly (same additions in the same order).
+__global__ void nn_recurrence_kernel(const double2 *ph, int64_t n, int64_t k, double inv_n,
+                                     int64_t anchor_every, double2 *f) {
+  const int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t start = seg * anchor_every;
+  if (start >= n) return;
+  const int64_t stop = min(start + anchor_every, n);
+  auto at = [&](int64_t l) { int64_t r = l % n; return ph[r < 0 ? r + n : r]; };
+  double wr = 0.0, wi = 0.0;
+  for (int64_t l = start - k; l <= start + k; ++l) {
+    const double2 q = at(l);
+    wr += q.x;
+    wi += q.y;
+  }
+  f[start] = make_double2(wr * inv_n, wi * inv_n);
+  for (int64_t m = start + 1; m < stop; ++m) {
+    const double2 a = at(m - 1 - k), b = at(m + k);
+    wr = (wr - a.x) + b.x;
+    wi = (wi - a.y) + b.y;
+    f[m] = make_double2(wr * inv_n, wi * inv_n);
+  }
+}
+
+// _kernels.py:485-509: f[m] = sum_l spins[l] for every m (int64, exact).
+__global__ void spin_sum_kernel(const int64_t *spins, int64_t n, unsigned long long *total) {
+  long long acc = 0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x)
+    acc += spins[l];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(total, (unsigned long long)acc);  // two's complement
+}
+
+__global__ void spin_fill_kernel(const unsigned long long *total, int64_t n, int64_t *f) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m < n) f[m] = (int64_t)*total;
+}
+
 static inline unsigned grid_for(int64_t n) {
   return (unsigned)((n + TW_THREADS - 1) / TW_THREADS);
 }
@@ -329,5 +420,62 @@ extern "C" int cdk_dense_poly(const double *x, const int64_t *offsets, int64_t m
   dense_poly_kernel<<<grid_for(n_in), TW_THREADS, 0, st>>>(x, offsets, m_comm, tbl, p, scale,
                                                             shift, out);
   CDK_CHECK_LAUNCH("dense_poly_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_pairs_poly(const int64_t *iu, const int64_t *iv, int64_t n_pairs,
+                              const double *x, double inv_n, const double *coef, int p,
+                              double x0, const double *sgn, double *out, void *stream) {
+  if (p < 0 || n_pairs < 0) return set_error("pairs_poly: bad sizes"), CDK_INPUT;
+  if (n_pairs == 0) return CDK_OK;
+  pairs_poly_kernel<<<grid_for(n_pairs), TW_THREADS, 0, as_stream(stream)>>>(
+      iu, iv, n_pairs, x, inv_n, coef, p, x0, sgn, out);
+  CDK_CHECK_LAUNCH("pairs_poly_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_ho_naive_block(const double *theta, int64_t lam, double l1, double l2,
+                                  double l3, double l4, double *out, void *stream) {
+  if (lam < 0 || lam > HO_NAIVE_MAX) {
+    set_error("ho_naive_block: need 0 <= lam <= 4096");
+    return CDK_INPUT;
+  }
+  if (lam == 0) return CDK_OK;
+  constexpr int T = 128;
+  ho_naive_block_kernel<<<(unsigned)((lam + T - 1) / T), T, 0, as_stream(stream)>>>(
+      theta, (int)lam, l1, l2, l3, l4, out);
+  CDK_CHECK_LAUNCH("ho_naive_block_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_nn_recurrence(const double *ph, int64_t n, int64_t k, double inv_n,
+                                 int64_t anchor_every, double *f, void *stream) {
+  if (n < 0 || k < 0 || anchor_every < 1) {
+    set_error("nn_recurrence: need n >= 0, k >= 0, anchor_every >= 1");
+    return CDK_INPUT;
+  }
+  if (n == 0) return CDK_OK;
+  const int64_t segs = (n + anchor_every - 1) / anchor_every;
+  constexpr int T = 64;
+  nn_recurrence_kernel<<<(unsigned)((segs + T - 1) / T), T, 0, as_stream(stream)>>>(
+      reinterpret_cast<const double2 *>(ph), n, k, inv_n, anchor_every,
+      reinterpret_cast<double2 *>(f));
+  CDK_CHECK_LAUNCH("nn_recurrence_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_spin_field_sums(const int64_t *spins, int64_t n, int64_t *f,
+                                   void *scratch, void *stream) {
+  if (n < 0) return set_error("spin_field_sums: bad n"), CDK_INPUT;
+  if (n == 0) return CDK_OK;
+  cudaStream_t st = as_stream(stream);
+  auto *total = reinterpret_cast<unsigned long long *>(scratch);
+  cudaError_t e = cudaMemsetAsync(total, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return cuda_status(e, "spin_field_sums memset");
+  const unsigned g = (unsigned)std::min<int64_t>(grid_for(n), 148 * 8);
+  spin_sum_kernel<<<g, TW_THREADS, 0, st>>>(spins, n, total);
+  CDK_CHECK_LAUNCH("spin_sum_kernel");
+  spin_fill_kernel<<<grid_for(n), TW_THREADS, 0, st>>>(total, n, f);
+  CDK_CHECK_LAUNCH("spin_fill_kernel");
   return CDK_OK;
 }

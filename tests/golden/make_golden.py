@@ -188,7 +188,46 @@ def cfg2_fixture(n_sample=4096, steps=2):
     print("cfg2_sample.npz written")
 
 
+def f4_fixtures():
+    """SURVEY §8(f) rank 4 kernels: pairs_poly (Desai-Zwanzig coupling),
+    nn_recurrence (Appendix B window sums), spin_field_sums (Bornholdt-Rohlf
+    oracle) and ho_naive_block at a larger block, all by the real reference."""
+    rng = np.random.Generator(np.random.PCG64(424242))
+    out = {}
+    n = 257
+    x = rng.uniform(-2.0, 2.0, n)
+    P = 800
+    iu = rng.integers(0, n, P)
+    iv = rng.integers(0, n, P)
+    iv[:40] = iu[:40]  # diagonal entries: counted once
+    sgn = np.where(rng.random(P) < 0.5, -1.0, 1.0)
+    coef = rng.standard_normal(4)
+    o = rng.standard_normal(n)
+    out.update(pp_x=x, pp_iu=iu, pp_iv=iv, pp_sgn=sgn, pp_coef=coef, pp_out0=o.copy())
+    ref.pairs_poly(iu, iv, x, 1.0 / n, coef, 0.2, sgn, o)
+    out["pp_out"] = o
+    # window sums: phases on the unit circle; windows narrower than, equal to
+    # and wider than the ring; anchor strides that do / do not divide n
+    for tag, nn, k, anchor in (("a", 5000, 1, 1024), ("b", 5000, 37, 100), ("c", 5000, 1250, 1024),
+                               ("d", 7, 10, 1024), ("e", 3001, 500, 1)):
+        ph = np.exp(1j * rng.uniform(-math.pi, math.pi, nn))
+        out[f"nn_{tag}_ph"] = ph
+        out[f"nn_{tag}_k"] = np.array(k)
+        out[f"nn_{tag}_anchor"] = np.array(anchor)
+        out[f"nn_{tag}_f"] = ref.nn_recurrence(ph, k, 1.0 / nn, anchor)
+    spins = np.where(rng.random(1000) < 0.37, -1, 1).astype(np.int64)
+    out["spin"] = spins
+    out["spin_f"] = ref.spin_field_sums(spins)
+    th = rng.uniform(-math.pi, math.pi, 40)
+    out["ho40_theta"] = th
+    out["ho40_1102"] = ref.ho_naive_block(th, (1, 1, 0, -2))
+    out["ho40_2m11m2"] = ref.ho_naive_block(th, (2, -1, 1, -2))
+    np.savez_compressed(os.path.join(HERE, "kernels_f4.npz"), **out)
+    print("kernels_f4.npz written")
+
+
 if __name__ == "__main__":
-    kernel_fixtures()
-    cfg1_fixture()
-    cfg2_fixture()
+    which = sys.argv[1:] or ["kernels", "cfg1", "cfg2", "f4"]
+    for w in which:
+        {"kernels": kernel_fixtures, "cfg1": cfg1_fixture, "cfg2": cfg2_fixture,
+         "f4": f4_fixtures}[w]()
