@@ -102,6 +102,12 @@ CDK_API int cdk_nn_recurrence(const double *ph, int64_t n, int64_t k, double inv
 CDK_API int cdk_spin_field_sums(const int64_t *spins, int64_t n, int64_t *f, void *scratch,
                         void *stream);
 
+/* Direct-sum (naive-mode) triadic term of the higher-order Kuramoto model,
+ * SPEC.md:463-470 eval_rhs_naive: tri int64[n_tri][3] (the graph's 3-cliques),
+ * out[a] += coef sin(theta_b + theta_c - 2 theta_a) and rotations. */
+CDK_API int cdk_triangles_sin(const int64_t *tri, int64_t n_tri, const double *theta, double coef,
+                      double *out, void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* Fused CIA path: Kuramoto RHS (E1 + E2) inside RK4 stages.                */
 /* ------------------------------------------------------------------------ */

@@ -146,6 +146,7 @@ _SIGS = {
     "cdk_ho_naive_block": [P, I64, D, D, D, D, P, P],
     "cdk_nn_recurrence": [P, I64, I64, D, I64, P, P],
     "cdk_spin_field_sums": [P, I64, P, P, P],
+    "cdk_triangles_sin": [P, I64, P, D, P, P],
     "cdk_kuramoto_workspace_bytes": [ctypes.POINTER(CdkGraph)],
     "cdk_kuramoto_prepare": [ctypes.POINTER(CdkGraph), P, P, P],
     "cdk_kuramoto_rhs": [ctypes.POINTER(CdkGraph), P, P, D, P, P, P],

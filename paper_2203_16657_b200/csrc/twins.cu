@@ -308,6 +308,21 @@ __global__ void spin_fill_kernel(const unsigned long long *total, int64_t n, int
   if (m < n) f[m] = (int64_t)*total;
 }
 
+// Direct-sum triadic term of the higher-order Kuramoto model (SPEC.md:463-470
+// naive mode): every 3-clique {a, b, c} of the graph adds
+// coef * sin(theta_b + theta_c - 2 theta_a) to out[a] (and the two rotations),
+// coef = 2 K2 / N^2 (ordered (j, k) pairs).  fp64 atomics.
+__global__ void triangles_sin_kernel(const int64_t *tri, int64_t n_tri, const double *theta,
+                                     double coef, double *out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_tri) return;
+  const int64_t a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
+  const double ta = theta[a], tb = theta[b], tc = theta[c];
+  atomicAdd(out + a, coef * sin((tb + tc) - 2.0 * ta));
+  atomicAdd(out + b, coef * sin((ta + tc) - 2.0 * tb));
+  atomicAdd(out + c, coef * sin((ta + tb) - 2.0 * tc));
+}
+
 static inline unsigned grid_for(int64_t n) {
   return (unsigned)((n + TW_THREADS - 1) / TW_THREADS);
 }
@@ -477,5 +492,15 @@ extern "C" int cdk_spin_field_sums(const int64_t *spins, int64_t n, int64_t *f,
   CDK_CHECK_LAUNCH("spin_sum_kernel");
   spin_fill_kernel<<<grid_for(n), TW_THREADS, 0, st>>>(total, n, f);
   CDK_CHECK_LAUNCH("spin_fill_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_triangles_sin(const int64_t *tri, int64_t n_tri, const double *theta,
+                                 double coef, double *out, void *stream) {
+  if (n_tri < 0) return set_error("triangles_sin: bad n_tri"), CDK_INPUT;
+  if (n_tri == 0) return CDK_OK;
+  triangles_sin_kernel<<<grid_for(n_tri), TW_THREADS, 0, as_stream(stream)>>>(tri, n_tri, theta,
+                                                                               coef, out);
+  CDK_CHECK_LAUNCH("triangles_sin_kernel");
   return CDK_OK;
 }

@@ -4,26 +4,24 @@
                      sparse correction with the exact coupling) + intrinsic term,
                      one fused kernel (cdk_kuramoto_rhs).
 * ``eval_rhs_naive`` SPEC.md:368-374 — direct sum over the graph's edges with the
-                     exact coupling (cdk_pairs_trig over the full edge list,
-                     sgn = +1).  Memory guard N > 2^15 as SPEC.md:614.
+                     exact coupling (naive.NaiveEngine: cdk_pairs_trig /
+                     cdk_pairs_cs over the full edge list, sgn = +1, plus
+                     cdk_triangles_sin for the triadic model).
+                     Memory guard N > 2^15 as SPEC.md:614.
 
 Both take and return states in ORIGINAL node order (numpy).
 """
 
 from __future__ import annotations
 
-import math
-
 import numpy as np
 
-from . import _kernels
 from .engine import KuramotoEngine
-from .errors import InputError, MemoryGuardError
+from .errors import InputError
 from .graph import Decomposition, Graph
 from .models import Kuramoto
+from .naive import NAIVE_N_CAP  # noqa: F401  (re-exported: the SPEC's memory guard)
 from .plan import DeviceGraph
-
-NAIVE_N_CAP = 2**15
 
 
 def _engine(model: Kuramoto, dec: Decomposition) -> KuramotoEngine:
@@ -124,14 +122,15 @@ def eval_rhs_cia(model, dec: Decomposition, state) -> np.ndarray:
 
 
 def eval_rhs_naive(model, graph: Graph, state) -> np.ndarray:
-    if not isinstance(model, Kuramoto):
-        raise InputError(f"eval_rhs_naive: unsupported model {type(model).__name__}")
-    if graph.n_nodes > NAIVE_N_CAP:
-        raise MemoryGuardError(f"naive mode refuses N = {graph.n_nodes} > {NAIVE_N_CAP} "
-                               "(O(N^2) edge list; SPEC.md:614)")
+    """Direct sum over ``graph``'s edges with the exact coupling
+    for every model on the path: Kuramoto, higher-order Kuramoto (pairs +
+    3-cliques) and Cucker-Smale (state [N, 4]).  States in the graph's node
+    order; device kernels (naive.NaiveEngine); MemoryGuardError above 2^15."""
+    from .naive import NaiveEngine
+
     x = np.asarray(state, dtype=np.float64)
-    out = np.array(model.omega, dtype=np.float64, copy=True)
-    e = graph.edges
-    _kernels.pairs_trig(e[:, 0], e[:, 1], x, 1.0 / model.norm_value(), np.zeros(2),
-                        np.array([0.0, model.coupling]), math.pi, np.ones(e.shape[0]), out)
-    return out
+    eng = NaiveEngine(model, graph)
+    want = (graph.n_nodes, 4) if eng.kind == "cs" else (graph.n_nodes,)
+    if x.shape != want:
+        raise InputError(f"state must have shape {want}")
+    return eng.rhs(x).cpu().numpy()

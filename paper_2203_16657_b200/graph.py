@@ -135,6 +135,31 @@ class Decomposition:
         np.add.at(b, (s.iv[off_diag], s.iu[off_diag]), sg[off_diag])
         return b
 
+    def graph(self) -> "Graph":
+        """The graph D + S describes, as an edge list in PERMUTED order (the
+        direct-sum / naive-mode input; O(sum lambda_c^2) memory: small and
+        mid-size N only).  Vectorised: complete intra blocks minus the missing
+        pairs, plus the inter pairs."""
+        if "graph" not in self._cache:
+            n = self.n_nodes
+            s = self.correction
+            od = s.iu != s.iv
+            lo = np.minimum(s.iu[od], s.iv[od])
+            hi = np.maximum(s.iu[od], s.iv[od])
+            miss = np.sort(lo[s.sgn[od] < 0] * n + hi[s.sgn[od] < 0])
+            keys = [lo[s.sgn[od] > 0] * n + hi[s.sgn[od] > 0]]
+            off = self.offsets
+            for c in range(self.partition.n_comm):
+                lam = int(off[c + 1] - off[c])
+                if lam < 2:
+                    continue
+                a, b = np.triu_indices(lam, 1)
+                k = (a + off[c]) * n + (b + off[c])
+                keys.append(k[~np.isin(k, miss, assume_unique=False)])
+            key = np.unique(np.concatenate(keys)) if keys else np.empty(0, np.int64)
+            self._cache["graph"] = Graph(int(n), np.stack([key // n, key % n], axis=1))
+        return self._cache["graph"]
+
     def directed(self):
         """Directed S without the diagonal: (rows, cols, sign) int64/int64/int8."""
         if "directed" not in self._cache:

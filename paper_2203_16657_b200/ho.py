@@ -147,6 +147,7 @@ class HoDeviceGraph:
         self.miss_tri = missing_triangles(dec)
         self.span_tri = spanning_triangles(dec)
         tptr, tjk = triangle_pairs(n, self.miss_tri, self.span_tri)
+        self.tri_pairs = int(tptr[-1])  # triangle incidences one RHS evaluates
 
         def up(a):
             return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
