@@ -349,6 +349,42 @@ CDK_API int cdk_ho_status(const cdk_ho_graph *g, const void *workspace, cdk_run_
                           void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* Higher-harmonics Kuramoto: coupling  */
+/*   h(x) = sum_{a=0..p} d_cos[a] cos(a x) + d_sin[a] sin(a x), p <= 8,      */
+/* CIA with 2p+1 Fourier modes in E1 (replaces order_params_blocks +         */
+/* dense_complex/dense_real with p harmonics, _kernels.py:34-73,124-204) and  */
+/* the exact h on the sparse correction (replaces pairs_trig,                 */
+/* _kernels.py:246-283,353-362), fused into RK4 (reduce + stage per stage).   */
+/* ------------------------------------------------------------------------ */
+typedef struct cdk_hh_graph {
+  int64_t n_rows;
+  int32_t n_rblk;
+  int32_t n_comm;
+  int32_t p;                     /* harmonics, 1..8 */
+  int32_t reserved;
+  const int64_t *rblk_row0;      /* [n_rblk+1] */
+  const int32_t *rblk_comm;      /* [n_rblk], -1 = NONE pool */
+  const int32_t *comm_rblk_off;  /* [n_comm+1] */
+  const int64_t *comm_off;       /* [n_comm+1] community row offsets */
+  const int64_t *miss_ptr;       /* [n_rows+1] proper missing intra edges (sign -1) */
+  const int32_t *miss_col;
+  const int64_t *inter_ptr;      /* [n_rows+1] inter / pool edges (sign +1) */
+  const int32_t *inter_col;
+  const double *d_cos;           /* [p+1] (coupling constant folded in) */
+  const double *d_sin;           /* [p+1] */
+} cdk_hh_graph;
+
+CDK_API size_t cdk_hh_workspace_bytes(const cdk_hh_graph *g);
+CDK_API int cdk_hh_prepare(const cdk_hh_graph *g, const double *theta, void *workspace,
+                           void *stream);
+CDK_API int cdk_hh_rhs(const cdk_hh_graph *g, const double *theta, const double *omega,
+                       double inv_n, double *out, void *workspace, void *stream);
+CDK_API int cdk_hh_rk4(const cdk_hh_graph *g, double *theta, const double *omega, double inv_n,
+                       double dt, int64_t n_steps, void *workspace, void *stream);
+CDK_API int cdk_hh_status(const cdk_hh_graph *g, const void *workspace, cdk_run_status *out,
+                          void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* Cucker-Smale flocking, 2-D (BASELINE config 4)                            */
 /*   s' = v,  v'_m = inv_n sum_l a_ml eta(|s_l - s_m|^2)(v_l - v_m),         */
 /*   eta(y) = K / (sigma2 + y)^beta.                                          */

@@ -64,6 +64,40 @@ def kuramoto_rhs_cia(kern, theta, omega, offsets, iu, iv, sgn, coupling, norm, o
     return out
 
 
+def harmonics_tables(d_cos, d_sin):
+    """Complex coefficients d_a (a = -p..p) of h(x) = sum_a d_cos[a] cos(a x)
+    + d_sin[a] sin(a x): d_0 = d_cos[0], d_a = (d_cos[a] - i d_sin[a]) / 2,
+    d_-a = conj(d_a) (SPEC.md:169-176 conversion)."""
+    p = len(d_cos) - 1
+    d = {0: complex(d_cos[0], 0.0)}
+    for a in range(1, p + 1):
+        d[a] = complex(d_cos[a], -d_sin[a]) / 2.0
+        d[-a] = d[a].conjugate()
+    return d
+
+
+def harmonics_rhs_cia(kern, theta, omega, offsets, iu, iv, sgn, d_cos, d_sin, norm):
+    """Higher-harmonics Kuramoto, CIA form over the
+    reference kernels: E1 order_params_blocks (p modes) + dense_complex with
+    tbl[c, p - a] = d_a r_a, E2 pairs_trig with the p harmonics (exact h)."""
+    d_cos = np.asarray(d_cos, np.float64)
+    d_sin = np.asarray(d_sin, np.float64)
+    p = d_cos.shape[0] - 1
+    d = harmonics_tables(d_cos, d_sin)
+    out = np.array(omega, dtype=np.float64, copy=True)
+    r = kern.order_params_blocks(theta, offsets, p, math.pi, norm)
+    tbl = np.zeros_like(r)
+    for a in range(-p, p + 1):
+        tbl[:, p - a] = d[a] * r[:, p + a]
+    n_viol, max_imag = kern.dense_complex(theta, offsets, tbl, math.pi, out)
+    if n_viol:
+        from paper_2203_16657_b200.errors import ImagResidueError
+
+        raise ImagResidueError(f"{n_viol} nodes above IMAG_TOL (max {max_imag:g})")
+    kern.pairs_trig(iu, iv, theta, 1.0 / norm, d_cos, d_sin, math.pi, sgn, out)
+    return out
+
+
 def kuramoto_rhs_naive(kern, theta, omega, eu, ev, coupling, norm):
     """Direct sum over the graph's edge list (eu < ev), exact sin."""
     _, d_cos, d_sin = kuramoto_tables(coupling)

@@ -40,6 +40,11 @@ def __getattr__(name):  # lazy: these import torch / the CUDA library
         from . import ho
 
         return getattr(ho, name)
+    if name in ("HigherHarmonicsKuramoto", "higher_harmonics_model",
+                "harmonics_model_from_coupling", "HhEngine"):
+        from . import harmonics
+
+        return getattr(harmonics, name)
     if name in ("CuckerSmale", "CSEngine"):
         from . import cs
 

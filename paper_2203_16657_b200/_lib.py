@@ -92,6 +92,26 @@ class CdkHoGraph(ctypes.Structure):
     ]
 
 
+class CdkHhGraph(ctypes.Structure):
+    _fields_ = [
+        ("n_rows", I64),
+        ("n_rblk", I32),
+        ("n_comm", I32),
+        ("p", I32),
+        ("reserved", I32),
+        ("rblk_row0", P),
+        ("rblk_comm", P),
+        ("comm_rblk_off", P),
+        ("comm_off", P),
+        ("miss_ptr", P),
+        ("miss_col", P),
+        ("inter_ptr", P),
+        ("inter_col", P),
+        ("d_cos", P),
+        ("d_sin", P),
+    ]
+
+
 class CdkCsGraph(ctypes.Structure):
     _fields_ = [
         ("n_rows", I64),
@@ -169,6 +189,11 @@ _SIGS = {
     "cdk_ho_rhs": [ctypes.POINTER(CdkHoGraph), P, P, D, D, P, P, P],
     "cdk_ho_rk4": [ctypes.POINTER(CdkHoGraph), P, P, D, D, D, I64, P, P],
     "cdk_ho_status": [ctypes.POINTER(CdkHoGraph), P, ctypes.POINTER(CdkRunStatus), P],
+    "cdk_hh_workspace_bytes": [ctypes.POINTER(CdkHhGraph)],
+    "cdk_hh_prepare": [ctypes.POINTER(CdkHhGraph), P, P, P],
+    "cdk_hh_rhs": [ctypes.POINTER(CdkHhGraph), P, P, D, P, P, P],
+    "cdk_hh_rk4": [ctypes.POINTER(CdkHhGraph), P, P, D, D, I64, P, P],
+    "cdk_hh_status": [ctypes.POINTER(CdkHhGraph), P, ctypes.POINTER(CdkRunStatus), P],
     "cdk_cs_workspace_bytes": [ctypes.POINTER(CdkCsGraph)],
     "cdk_cs_prepare": [ctypes.POINTER(CdkCsGraph), P, P],
     "cdk_cs_rhs": [ctypes.POINTER(CdkCsGraph), P, P, D, D, D, D, P, P, P],
@@ -203,6 +228,7 @@ _RESTYPES = {
     "cdk_debug_set_profile_buffer": None,
     "cdk_host_triangles": I64,
     "cdk_ho_workspace_bytes": ctypes.c_size_t,
+    "cdk_hh_workspace_bytes": ctypes.c_size_t,
     "cdk_cs_workspace_bytes": ctypes.c_size_t,
 }
 

@@ -1057,22 +1057,10 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
                              // (measured: 14336 nodes, 224 KB, is 3% slower on config 2)
 #endif
 #ifndef CDK_ELL_DEPTH
-#define CDK_ELL_DEPTH 6  // 16-byte chunks per lane in flight ahead of the gathers (6-8 best)
+#define CDK_ELL_DEPTH 8  // 16-byte chunks per lane in flight (cp.async ring in shared memory)
 #endif
 #ifndef CDK_ELL_XCOLS
 #define CDK_ELL_XCOLS 12  // inter columns per lane loaded before the intra loop (multiple of 4)
-#endif
-#ifndef CDK_ELL_XLEAD
-#define CDK_ELL_XLEAD 0  // chunks before a unit's end at which its remaining inter gathers go out
-#endif
-#ifndef CDK_ELL_PF
-#define CDK_ELL_PF 0  // chunks prefetched into L1 beyond the register queue (0: off)
-#endif
-#ifndef CDK_ELL_MPF
-#define CDK_ELL_MPF 0  // claim the next unit and load its metadata at the start of the current one
-#endif
-#ifndef CDK_ELL_XUNIT
-#define CDK_ELL_XUNIT 0  // 1: chunk queue runs across a warp's consecutive work units (slower)
 #endif
 #ifndef CDK_ELL_RK4_RT
 #define CDK_ELL_RK4_RT 1  // persistent RK4: one stage body with a runtime mode (0: four inlined)
@@ -1087,7 +1075,6 @@ constexpr int ELL_XCOLS = CDK_ELL_XCOLS;
 #endif
 constexpr int ELL_XEARLY = CDK_ELL_XEARLY;
 constexpr int ELL_LDSB = CDK_ELL_LDSB;
-constexpr int ELL_XLEAD = CDK_ELL_XLEAD;
 #ifndef CDK_ELL_MINBLOCKS
 #define CDK_ELL_MINBLOCKS 1  // resident ELL CTAs per SM (the planner launches SMs x this many)
 #endif
@@ -1100,8 +1087,34 @@ constexpr int ELL_DEPTH = CDK_ELL_DEPTH;
 constexpr int ELL_WARPS = ELL_THREADS / 32;
 constexpr int ELL_GROUPS = ELL_THREADS / 8;
 
+static_assert((CDK_ELL_DEPTH & (CDK_ELL_DEPTH - 1)) == 0, "CDK_ELL_DEPTH: a power of two");
+// dynamic shared memory: the z window (+ one zero slot per bank group), then
+// each warp's chunk ring (ELL_DEPTH x 512 bytes: one 16-byte chunk per lane)
+__host__ __device__ inline size_t ell_ring_offset(int smem_nodes) {
+  return ((size_t)smem_nodes + 8) * 16;  // smem_nodes is a multiple of 8: 128-byte aligned
+}
 __host__ __device__ inline size_t ell_smem_bytes(int smem_nodes) {
-  return ((size_t)smem_nodes + 8) * 16;
+  return ell_ring_offset(smem_nodes) + (size_t)ELL_WARPS * ELL_DEPTH * 512;
+}
+
+// cp.async (16 bytes, L2 only): the chunk stream lands in shared memory
+// without occupying registers while in flight
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ void prefetch_l2(const void *p, uint64_t bytes) {
@@ -1198,21 +1211,19 @@ __device__ __forceinline__ UnitChunks unit_chunks(const cdk_graph &g, int u, int
   return r;
 }
 
-// One work unit (an rblock, or one part of a split rblock).  The warp's chunk
-// queue cq runs across units: while the last chunks of this unit are
-// gathered, the first chunks of the warp's next unit (nx_u, claimed at the
-// start of this one) are already loading, so no unit starts with an empty
-// pipeline.  On entry cq[d] holds chunk d of this unit for d >= need (the
-// prefix was not known when the previous unit refilled); on exit `need` is
-// the next unit's invalid prefix.
+// One work unit (an rblock, or one part of a split rblock): lane = row.  The
+// unit's chunk stream runs through the warp's ring in shared memory
+// (cp.async, ELL_DEPTH chunks in flight per lane, one commit group per
+// chunk): no registers held by loads in flight, no register moves between
+// queue slots (a move of a register whose load is pending stalls the warp on
+// that load), and the depth is free of register pressure.
 template <bool STAGED>
 __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, const StageVar &v,
                                            int rb,
                                            int part, int nparts,
                                            uint32_t zs_addr, const double2 *zs, int64_t w0,
                                            const double2 *__restrict__ zglob, double2 R,
-                                           uint4 (&cq)[ELL_DEPTH], int &need,
-                                           const UnitChunks &uc, const UnitChunks &nx_u,
+                                           const UnitChunks &uc, uint32_t ring,
                                            const int4 *mt = nullptr) {
   const cdk_graph &g = a.g;
   const int lane = threadIdx.x & 31;
@@ -1255,37 +1266,31 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     xz[q] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
   // intra chunks: ELL_DEPTH in flight ahead of the one being gathered
   const uint4 *__restrict__ cp = uc.cp;
-  const uint4 padv = make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
-  for (int d = 0; d < ELL_DEPTH; ++d)
-    if (d < need && d < nch) cq[d] = ldg(cp + 32 * d);
-  need = ELL_DEPTH - nch > 0 ? ELL_DEPTH - nch : 0;
+  for (int d = 0; d < ELL_DEPTH; ++d) {
+    if (d < nch) cp_async16(ring + d * 512, cp + 32 * d);
+    cp_async_commit();
+  }
   double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
   double2 xw[ELL_XCOLS > 4 ? ELL_XCOLS - 4 : 1];
-  const int xtrig = (ELL_XLEAD > 0 && ELL_XCOLS > 4 && nx > 4)
-                        ? (nch > ELL_XLEAD ? nch - ELL_XLEAD : 0) : -1;
   auto issue_xw = [&]() {
 #pragma unroll
     for (int q = 4; q < ELL_XCOLS; ++q)
       xw[q - 4] = (jx[q] >= 0) ? ldz(z_in + jx[q]) : make_double2(0.0, 0.0);
   };
   for (int c = 0; c < nch; ++c) {
-    if (c == xtrig) issue_xw();  // the rest of the inter gathers, a few chunks before the end
-    const uint4 w = cq[0];
-#pragma unroll
-    for (int d = 0; d + 1 < ELL_DEPTH; ++d) cq[d] = cq[d + 1];
-    const int t = c + ELL_DEPTH;
-#if CDK_ELL_PF > 0  // L1 prefetch CDK_ELL_PF chunks beyond the register queue
-    if (t + CDK_ELL_PF < nch)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(cp + 32 * (t + CDK_ELL_PF)));
-#endif
-    cq[ELL_DEPTH - 1] = (t < nch) ? ldg(cp + 32 * t)
-                        : (t - nch < nx_u.nch) ? ldg(nx_u.cp + 32 * (t - nch)) : padv;
+    cp_async_wait<ELL_DEPTH - 1>();  // chunk c has landed (groups complete in order)
+    const uint32_t slot = ring + (uint32_t)(c & (ELL_DEPTH - 1)) * 512u;
+    const uint4 w = lds_u4(slot);
     if (STAGED) {
       ell_gather8_smem(w, zs_addr, ar, ai, br, bi);
     } else {
       ell_gather8_global(w, zglob, ar, ai, br, bi);
     }
+    // refill after the gathers issued: their addresses came from w, so the
+    // slot has been read before the async copy overwrites it
+    if (c + ELL_DEPTH < nch) cp_async16(slot, cp + 32 * (c + ELL_DEPTH));
+    cp_async_commit();
   }
   double sr = -(ar + br), si = -(ai + bi);  // intra-missing entries: sign -1
 #pragma unroll
@@ -1295,7 +1300,7 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
   }
   if (ELL_XCOLS > ELL_XEARLY && nx > ELL_XEARLY) {
     if (ELL_XEARLY == 4) {
-      if (xtrig < 0 || nch == 0) issue_xw();
+      issue_xw();
 #pragma unroll
       for (int q = 4; q < ELL_XCOLS; ++q) {
         sr += xw[q - 4].x;
@@ -1401,6 +1406,7 @@ struct EllSmem {
   int *next;    // rblock claim counter
   double2 *sP;  // [ELL_PART_CAP] the segment's rblock partials (community sums)
   int4 *meta;   // [2 * ELL_META_CAP] the segment's unit records (cdk_graph.ell_meta)
+  uint32_t ring;  // this lane's slot 0 of its warp's chunk ring (shared address)
 };
 
 // MODE: 0 RHS, 1..4 RK4 stage, 5 Euler (a runtime value: constant-folded in
@@ -1478,8 +1484,6 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
     const double2 *zglob = v.z_in + g.seg_base[s];
     const int uB = g.seg_unit[s + 1];
     int u = g.seg_unit[s] + warp;
-    uint4 cq[ELL_DEPTH];
-    int need = ELL_DEPTH;
     if (g.ell_meta) {  // packed metadata: the unit's description travels in registers
       const bool mloc = staged && uB - g.seg_unit[s] <= ELL_META_CAP;  // records in smem
       const int4 *meta = mloc ? sm.meta - 2 * g.seg_unit[s]
@@ -1490,38 +1494,26 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
         mb = meta[2 * u + 1];
       }
       while (u < uB) {
-        int nxt = 0;
-        int4 na = make_int4(0, 0, 0, 0), nb = na;
-#if CDK_ELL_MPF  // claim the next unit and fetch its description up front
-        if (lane == 0) nxt = atomicAdd(sm.next, 1);
-        nxt = __shfl_sync(FULL, nxt, 0);
-        if (nxt < uB) {
-          na = meta[2 * nxt];
-          nb = meta[2 * nxt + 1];
-        }
-#endif
         const int ci = mb.w & 0xFF;  // community relative to the segment's first (255: pool)
         const double2 R = (ci != 0xFF) ? sm.sR[ci] : make_double2(0.0, 0.0);
         const UnitChunks uc{reinterpret_cast<const uint4 *>(g.ell_col) + (uint32_t)ma.x + lane,
                             mb.x};
-        const UnitChunks nu{nullptr, 0};
         const int4 mt[2] = {ma, mb};
-        need = ELL_DEPTH;
         if (staged) {
           ell_rblock<true>(MODE, a, v, ma.w, (mb.w >> 8) & 0xFF, (mb.w >> 16) & 0xFF, zs_addr,
-                           sm.zs, w0, zglob, R, cq, need, uc, nu, mt);
+                           sm.zs, w0, zglob, R, uc, sm.ring, mt);
         } else {
           ell_rblock<false>(MODE, a, v, ma.w, (mb.w >> 8) & 0xFF, (mb.w >> 16) & 0xFF, zs_addr,
-                            sm.zs, w0, zglob, R, cq, need, uc, nu, mt);
+                            sm.zs, w0, zglob, R, uc, sm.ring, mt);
         }
-#if !CDK_ELL_MPF
+        int nxt = 0;
         if (lane == 0) nxt = atomicAdd(sm.next, 1);
         nxt = __shfl_sync(FULL, nxt, 0);
+        int4 na = make_int4(0, 0, 0, 0), nb = na;
         if (nxt < uB) {
           na = meta[2 * nxt];
           nb = meta[2 * nxt + 1];
         }
-#endif
         u = nxt;
         ma = na;
         mb = nb;
@@ -1529,52 +1521,22 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
       __syncthreads();  // window and counters reused by the next segment
       continue;
     }
-    UnitChunks uc{nullptr, 0};
-    if (u < uB) uc = unit_chunks(g, u, lane);
     while (u < uB) {
-      UnitChunks nu{nullptr, 0};
-#if CDK_ELL_XUNIT
-      int nxt = 0;  // claim the next unit first: its chunks stream in behind this one's
-      if (lane == 0) nxt = atomicAdd(sm.next, 1);
-      nxt = __shfl_sync(FULL, nxt, 0);
-      if (nxt < uB) nu = unit_chunks(g, nxt, lane);
-#endif
-      int rb, part, nparts;
-      double2 R;
-      int4 mt[2];
-      if (g.ell_meta) {  // rblock, rows, inter range and community in one round trip
-        mt[0] = ldg(reinterpret_cast<const int4 *>(g.ell_meta) + 2 * u);
-        mt[1] = ldg(reinterpret_cast<const int4 *>(g.ell_meta) + 2 * u + 1);
-        rb = mt[0].w;
-        part = (mt[1].w >> 8) & 0xFF;
-        nparts = (mt[1].w >> 16) & 0xFF;
-        const int ci = mt[1].w & 0xFF;  // community relative to the segment's first (255: pool)
-        R = (ci != 0xFF) ? sm.sR[ci] : make_double2(0.0, 0.0);
-      } else {
-        rb = g.ell_units[2 * u];
-        const int code = g.ell_units[2 * u + 1];
-        part = code & 0xFFFF;
-        nparts = code >> 16;
-        const int c = g.rblk_comm[rb];
-        R = (c >= 0) ? sm.sR[c - cA] : make_double2(0.0, 0.0);
-      }
-      const int4 *mp = g.ell_meta ? mt : nullptr;
+      const UnitChunks uc = unit_chunks(g, u, lane);
+      const int rb = g.ell_units[2 * u];
+      const int code = g.ell_units[2 * u + 1];
+      const int c = g.rblk_comm[rb];
+      const double2 R = (c >= 0) ? sm.sR[c - cA] : make_double2(0.0, 0.0);
       if (staged) {
-        ell_rblock<true>(MODE, a, v, rb, part, nparts, zs_addr, sm.zs, w0, zglob, R, cq, need,
-                         uc, nu, mp);
+        ell_rblock<true>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob,
+                         R, uc, sm.ring);
       } else {
-        ell_rblock<false>(MODE, a, v, rb, part, nparts, zs_addr, sm.zs, w0, zglob, R, cq, need,
-                          uc, nu, mp);
+        ell_rblock<false>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob,
+                          R, uc, sm.ring);
       }
-#if !CDK_ELL_XUNIT
       int nxt = 0;
       if (lane == 0) nxt = atomicAdd(sm.next, 1);
-      nxt = __shfl_sync(FULL, nxt, 0);
-      if (nxt < uB) nu = unit_chunks(g, nxt, lane);
-      need = ELL_DEPTH;
-#endif
-      u = nxt;
-      uc = nu;
+      u = __shfl_sync(FULL, nxt, 0);
     }
     __syncthreads();  // window and counters reused by the next segment
   }
@@ -1591,6 +1553,8 @@ __device__ __forceinline__ EllSmem ell_init(unsigned char *smem_raw, uint64_t *b
   sm.bar = bar;
   sm.sR = sR;
   sm.next = next;
+  sm.ring = smem_u32(smem_raw + ell_ring_offset(smem_nodes)) +
+            (uint32_t)((threadIdx.x >> 5) * ELL_DEPTH * 512 + (threadIdx.x & 31) * 16);
   if (threadIdx.x == 0) mbar_init(bar, 1);
   if (threadIdx.x < 8) sm.zs[smem_nodes + threadIdx.x] = make_double2(0.0, 0.0);
   __syncthreads();

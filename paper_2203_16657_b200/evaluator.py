@@ -63,12 +63,32 @@ def _ho_engine(model, dec: Decomposition):
     return eng
 
 
+def _hh_engine(model, dec: Decomposition):
+    from .harmonics import HhDeviceGraph, HhEngine
+
+    cached = dec._cache.get("hh_engine")
+    if cached is not None and cached[0] is model:
+        return cached[1]
+    dg = dec._cache.get("hh_graph")
+    if dg is None:
+        dg = dec._cache["hh_graph"] = HhDeviceGraph(dec)
+    perm = dec.partition.perm
+    eng = HhEngine(dec, np.asarray(model.omega)[perm], model.d_cos, model.d_sin,
+                   norm=model.norm_value(), graph=dg)
+    dec._cache["hh_engine"] = (model, eng)
+    return eng
+
+
 def engine_for(model, dec: Decomposition):
-    """The device engine of a model (Kuramoto or higher-order Kuramoto)."""
+    """The device engine of a model (Kuramoto, higher-harmonics Kuramoto or
+    higher-order Kuramoto)."""
+    from .harmonics import HigherHarmonicsKuramoto
     from .ho import HigherOrderKuramoto
 
     if isinstance(model, Kuramoto):
         return _engine(model, dec)
+    if isinstance(model, HigherHarmonicsKuramoto):
+        return _hh_engine(model, dec)
     if isinstance(model, HigherOrderKuramoto):
         return _ho_engine(model, dec)
     raise InputError(f"unsupported model {type(model).__name__}")

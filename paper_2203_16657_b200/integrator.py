@@ -86,7 +86,7 @@ class Trajectory:
             comp = np.tile(np.arange(d), n)
             for r in range(n_rec):
                 vals = st[r].reshape(-1)
-                f.writelines(f"{self.times[r]!r},{a},{b},{v!r}\n"
+                f.writelines(f"{float(self.times[r])!r},{a},{b},{v!r}\n"
                              for a, b, v in zip(node.tolist(), comp.tolist(), vals.tolist()))
             f.write("\nstep,seconds\n")
             f.writelines(f"{k + 1},{s!r}\n" for k, s in enumerate(self.step_seconds.tolist()))

@@ -8,7 +8,8 @@ of the reference kernels — the same realisation SURVEY §3.2 measured
 (``pairs_trig``/``pairs_cs`` with sgn = +1):
 
 * Kuramoto           out = omega + K/N sum_{(u,v) in E} sin(x_v - x_u) (both ends)
-                     -> cdk_pairs_trig, d_sin = (0, K)
+                     -> cdk_pairs_trig, d_sin = (0, K); higher harmonics: the
+                     model's d_cos/d_sin (p harmonics, exact h)
 * higher-order       + 2 K2/N^2 sum_{triangles {a,b,c}} sin(x_b + x_c - 2 x_a) (+ rotations)
                      -> cdk_pairs_trig (K1) + cdk_triangles_sin
 * Cucker-Smale       s' = v, v' = (1/N) sum_{(u,v)} eta(|s_v - s_u|^2) (v_v - v_u) (both ends)
@@ -70,6 +71,7 @@ class NaiveEngine:
         import torch
 
         from .cs import CuckerSmale
+        from .harmonics import HigherHarmonicsKuramoto
         from .ho import HigherOrderKuramoto
         from .models import Kuramoto
 
@@ -87,15 +89,22 @@ class NaiveEngine:
         self.n_edges = int(e.shape[0])
         self.tri = None
         self.n_tri = 0
-        if isinstance(model, (Kuramoto, HigherOrderKuramoto)):
+        if isinstance(model, (Kuramoto, HigherOrderKuramoto, HigherHarmonicsKuramoto)):
             self.kind = "ho" if isinstance(model, HigherOrderKuramoto) else "kuramoto"
             if model.n() != self.n:
                 raise InputError("omega shape does not match the graph")
             self.omega = torch.as_tensor(np.asarray(model.omega, np.float64), device=self.device)
             self.norm = model.norm_value()
-            k1 = model.coupling if self.kind == "kuramoto" else model.k1
-            self.d_cos = torch.zeros(2, dtype=torch.float64, device=self.device)
-            self.d_sin = torch.tensor([0.0, float(k1)], dtype=torch.float64, device=self.device)
+            if isinstance(model, HigherHarmonicsKuramoto):  # h = p harmonics
+                self.d_cos = torch.as_tensor(np.asarray(model.d_cos, np.float64),
+                                             device=self.device)
+                self.d_sin = torch.as_tensor(np.asarray(model.d_sin, np.float64),
+                                             device=self.device)
+            else:
+                k1 = model.coupling if self.kind == "kuramoto" else model.k1
+                self.d_cos = torch.zeros(2, dtype=torch.float64, device=self.device)
+                self.d_sin = torch.tensor([0.0, float(k1)], dtype=torch.float64,
+                                          device=self.device)
             if self.kind == "ho":
                 t = triangles(graph)
                 self.n_tri = int(t.shape[0])

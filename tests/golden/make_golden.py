@@ -226,8 +226,48 @@ def f4_fixtures():
     print("kernels_f4.npz written")
 
 
+def harmonics_fixture():
+    """Higher-harmonics Kuramoto, p = 4 random coefficients
+    on a planted 4 x 125 graph with a NONE pool of 12 nodes: one CIA RHS, one
+    direct-sum RHS and 200 CIA RK4 steps (dt 0.01), all over the real
+    reference kernels (oracle.cia.harmonics_rhs_cia orchestration)."""
+    from paper_2203_16657_b200 import graph as G
+
+    rng = np.random.Generator(np.random.PCG64(4040))
+    g, part = G.planted_partition_graph([125, 125, 125, 125], 0.9, 0.01, 44)
+    a = part.assignment.copy()
+    a[rng.choice(a.shape[0], 12, replace=False)] = -1
+    part = G.Partition.from_assignment(a)
+    dec = G.decompose(g, part)
+    n = g.n_nodes
+    d_cos = rng.standard_normal(5)
+    d_sin = rng.standard_normal(5)
+    d_sin[0] = 0.0
+    omega = rng.standard_normal(n)
+    theta0 = rng.uniform(-math.pi, math.pi, n)
+    s = dec.correction
+    perm = dec.partition.perm
+    om_p, th_p = omega[perm], theta0[perm]
+
+    def rhs(x):
+        return cia.harmonics_rhs_cia(ref, x, om_p, dec.offsets, s.iu, s.iv, s.sgn, d_cos, d_sin,
+                                     n)
+
+    k_cia = rhs(th_p)
+    eg = dec.graph().edges
+    k_naive = om_p.copy()
+    ref.pairs_trig(eg[:, 0], eg[:, 1], th_p, 1.0 / n, d_cos, d_sin, math.pi,
+                   np.ones(eg.shape[0]), k_naive)
+    fin, _ = cia.rk4_integrate(rhs, th_p, 0.01, 200)
+    np.savez_compressed(os.path.join(HERE, "harmonics.npz"), dec_sha256=np.array(dec_hash(dec)),
+                        assignment=a, d_cos=d_cos, d_sin=d_sin, omega=omega, theta0=theta0,
+                        rhs_cia=k_cia, rhs_naive=k_naive, final=fin, steps=np.array(200),
+                        dt=np.array(0.01))
+    print("harmonics.npz written; |cia - naive| =", np.abs(k_cia - k_naive).max())
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kernels", "cfg1", "cfg2", "f4"]
+    which = sys.argv[1:] or ["kernels", "cfg1", "cfg2", "f4", "harmonics"]
     for w in which:
         {"kernels": kernel_fixtures, "cfg1": cfg1_fixture, "cfg2": cfg2_fixture,
-         "f4": f4_fixtures}[w]()
+         "f4": f4_fixtures, "harmonics": harmonics_fixture}[w]()
