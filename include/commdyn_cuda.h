@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 13
+#define CDK_ABI_VERSION 14
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -397,7 +397,7 @@ typedef struct cdk_cs_graph {
   int64_t n_rows;
   int64_t n_comm;
   int32_t n_rblk;
-  int32_t reserved;
+  int32_t max_comm;             /* largest community (moments pass: CTAs per community) */
   const int64_t *comm_off;      /* [n_comm+1] */
   const int64_t *rblk_row0;     /* [n_rblk+1] */
   const int32_t *rblk_comm;     /* [n_rblk] */
@@ -407,7 +407,13 @@ typedef struct cdk_cs_graph {
   const int32_t *inter_col;
   const double *mu;             /* [n_comm][2] community centres */
   const double *inv_L;          /* [n_comm] 1 / scale */
-  const double *T;              /* [n_comm][153][153] contraction tensors */
+  /* contraction T_c[r][s] = chat_c[k(r,s)] * t_coef: one shared sparse
+   * pattern (1365 nonzeros of 153 x 153, CSR by r) + 9 fit coefficients per
+   * community (the dense per-community tensors are never formed on the device) */
+  const double *chat;           /* [n_comm][9] P2 fit coefficients */
+  const int32_t *t_ptr;         /* [154] */
+  const int32_t *t_col;         /* s | k << 8 */
+  const double *t_coef;         /* binomial coefficient x sign */
 } cdk_cs_graph;
 
 CDK_API size_t cdk_cs_workspace_bytes(const cdk_cs_graph *g);

@@ -117,7 +117,7 @@ class CdkCsGraph(ctypes.Structure):
         ("n_rows", I64),
         ("n_comm", I64),
         ("n_rblk", I32),
-        ("reserved", I32),
+        ("max_comm", I32),
         ("comm_off", P),
         ("rblk_row0", P),
         ("rblk_comm", P),
@@ -127,7 +127,10 @@ class CdkCsGraph(ctypes.Structure):
         ("inter_col", P),
         ("mu", P),
         ("inv_L", P),
-        ("T", P),
+        ("chat", P),
+        ("t_ptr", P),
+        ("t_col", P),
+        ("t_coef", P),
     ]
 
 
@@ -233,7 +236,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 13
+ABI_VERSION = 14
 
 _lock = threading.Lock()
 _lib = None

@@ -91,6 +91,26 @@ def _contraction_basis() -> np.ndarray:
     return _BASIS
 
 
+def contraction_pattern():
+    """The shared sparsity of T_c (module docstring): for output monomial r the
+    nonzero inputs s with their degree k(r, s) and coefficient B[k, r, s].
+    CSR by r: (t_ptr int32[NMON+1], t_col int32 = s | k << 8, t_coef f64);
+    T_c[r, s] = chat_c[k] * t_coef exactly as contraction_tensor forms it."""
+    B = _contraction_basis()
+    nz = B != 0
+    if np.any(nz.sum(axis=0) > 1):
+        raise AssertionError("contraction basis: more than one degree per (r, s)")
+    k_of = np.argmax(nz, axis=0)  # [r, s]
+    any_nz = nz.any(axis=0)
+    ptr = np.zeros(NMON + 1, dtype=np.int32)
+    ptr[1:] = np.cumsum(any_nz.sum(axis=1))
+    r_idx, s_idx = np.nonzero(any_nz)  # row-major: r ascending, s ascending
+    k = k_of[r_idx, s_idx]
+    col = (s_idx | (k << 8)).astype(np.int32)
+    coef = B[k, r_idx, s_idx]
+    return ptr, col, coef
+
+
 def contraction_tensor(chat) -> np.ndarray:
     """T[pq, ij] of the module docstring (NMON x NMON)."""
     return np.tensordot(np.asarray(chat, np.float64), _contraction_basis(), axes=(0, 0))
@@ -158,20 +178,25 @@ class CsDeviceGraph:
             "rblk_row0": up(lay.rblk_row0), "rblk_comm": up(lay.rblk_comm),
             "miss_ptr": up(mptr), "miss_col": up(mcol if mcol.size else np.zeros(1, np.int32)),
             "inter_ptr": up(xptr), "inter_col": up(xcol if xcol.size else np.zeros(1, np.int32)),
-            "mu": up(plan.mu), "inv_L": up(1.0 / plan.L), "T": up(plan.T),
+            "mu": up(plan.mu), "inv_L": up(1.0 / plan.L), "chat": up(plan.chat),
         }
+        tp, tc, tcoef = contraction_pattern()
+        self._t.update(t_ptr=up(tp), t_col=up(tc), t_coef=up(tcoef))
         t = self._t
         self.n_rows = n
         self.n_comm = dec.partition.n_comm
         self.device = dev
         self.plan = plan
         self.struct = _lib.CdkCsGraph(
-            n_rows=n, n_comm=self.n_comm, n_rblk=lay.n_rblk, reserved=0,
+            n_rows=n, n_comm=self.n_comm, n_rblk=lay.n_rblk,
+            max_comm=int(np.diff(dec.offsets).max()) if self.n_comm else 0,
             comm_off=t["comm_off"].data_ptr(), rblk_row0=t["rblk_row0"].data_ptr(),
             rblk_comm=t["rblk_comm"].data_ptr(), miss_ptr=t["miss_ptr"].data_ptr(),
             miss_col=t["miss_col"].data_ptr(), inter_ptr=t["inter_ptr"].data_ptr(),
             inter_col=t["inter_col"].data_ptr(), mu=t["mu"].data_ptr(),
-            inv_L=t["inv_L"].data_ptr(), T=t["T"].data_ptr())
+            inv_L=t["inv_L"].data_ptr(), chat=t["chat"].data_ptr(),
+            t_ptr=t["t_ptr"].data_ptr(), t_col=t["t_col"].data_ptr(),
+            t_coef=t["t_coef"].data_ptr())
 
 
 class CSEngine:

@@ -36,8 +36,12 @@ struct CsArgs {
   const int32_t *inter_col;
   const double2 *mu;
   const double *inv_L;
-  const double *T;          // [M][153][153]
-  double *M;                // [M][3][153]
+  const double *chat;       // [M][9]
+  const int32_t *t_ptr;     // [154] shared contraction pattern (CSR by output monomial)
+  const int32_t *t_col;     // input monomial | k << 8
+  const double *t_coef;
+  double *M;                // [M][mom_split][3][153] partial moments (node chunks)
+  int32_t mom_split;        // CTAs per community in the moments pass
   double *H;                // [M][3][153]
   const double2 *s_in, *v_in;  // stage state
   double2 *s_out, *v_out;
@@ -55,24 +59,30 @@ __device__ __forceinline__ double eta_exact(double d2, double K, double sigma2, 
   return K / pow(x, beta);
 }
 
+// moments of node chunk q of community c: CTA (c, q) sums nodes
+// [b + q * CS_MOM_NODES, ...) in node order, two independent accumulator
+// chains per thread; the contraction adds the chunks' partials in q order
+constexpr int CS_MOM_NODES = 256;
 __global__ void __launch_bounds__(256) cs_moments_kernel(const CsArgs a) {
   __shared__ double px[128][CS_D2 + 1];
   __shared__ double py[128][CS_D2 + 1];
   __shared__ double pf[128][3];
-  const int c = blockIdx.x;
-  const int64_t b = a.comm_off[c], e = a.comm_off[c + 1];
+  const int c = blockIdx.x, q = blockIdx.y;
+  const int64_t cb = a.comm_off[c], ce = a.comm_off[c + 1];
+  const int64_t b = cb + (int64_t)q * CS_MOM_NODES;
+  const int64_t e = min(ce, b + CS_MOM_NODES);
   const double2 mu = a.mu[c];
   const double il = a.inv_L[c];
-  double acc[2] = {0.0, 0.0};
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [output][chain]
   const int o0 = threadIdx.x, o1 = threadIdx.x + 256;
   for (int64_t base = b; base < e; base += 128) {
     const int cnt = (int)min((int64_t)128, e - base);
     __syncthreads();
     if (threadIdx.x < cnt) {
       const int n = threadIdx.x;
-      const double2 s = a.s_in[base + n];
+      const double2 sv = a.s_in[base + n];
       const double2 v = a.v_in[base + n];
-      const double x = (s.x - mu.x) * il, y = (s.y - mu.y) * il;
+      const double x = (sv.x - mu.x) * il, y = (sv.y - mu.y) * il;
       double xp = 1.0, yp = 1.0;
       for (int k = 0; k <= CS_D2; ++k) {
         px[n][k] = xp;
@@ -86,30 +96,52 @@ __global__ void __launch_bounds__(256) cs_moments_kernel(const CsArgs a) {
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int o = q ? o1 : o0;
+    for (int u = 0; u < 2; ++u) {
+      const int o = u ? o1 : o0;
       if (o < CS_NOUT) {
         const int f = o / CS_NMON, r = o % CS_NMON;
         const int i = c_mono_i[r], j = c_mono_j[r];
-        double s = acc[q];
-        for (int n = 0; n < cnt; ++n) s += px[n][i] * py[n][j] * pf[n][f];
-        acc[q] = s;
+        double s0 = acc[u][0], s1 = acc[u][1];
+        int n = 0;
+        for (; n + 1 < cnt; n += 2) {
+          s0 += px[n][i] * py[n][j] * pf[n][f];
+          s1 += px[n + 1][i] * py[n + 1][j] * pf[n + 1][f];
+        }
+        if (n < cnt) s0 += px[n][i] * py[n][j] * pf[n][f];
+        acc[u][0] = s0;
+        acc[u][1] = s1;
       }
     }
   }
-  if (o0 < CS_NOUT) a.M[(int64_t)c * CS_NOUT + o0] = acc[0];
-  if (o1 < CS_NOUT) a.M[(int64_t)c * CS_NOUT + o1] = acc[1];
+  double *Mq = a.M + ((int64_t)c * a.mom_split + q) * CS_NOUT;
+  if (o0 < CS_NOUT) Mq[o0] = acc[0][0] + acc[0][1];
+  if (o1 < CS_NOUT) Mq[o1] = acc[1][0] + acc[1][1];
 }
 
+// H^f_c = T_c M^f_c with T_c[r][s] = chat_c[k(r,s)] t_coef[r,s]: the shared
+// 1365-entry pattern and 9 coefficients per community replace the dense
+// 153 x 153 tensor per community (19 MB per stage of mostly zeros on config 4)
 __global__ void __launch_bounds__(512) cs_contract_kernel(const CsArgs a) {
+  __shared__ double Ms[CS_NOUT];
+  __shared__ double ch[9];
   const int c = blockIdx.x;
   const int o = threadIdx.x;
+  if (o < CS_NOUT) {
+    const double *Mc = a.M + (int64_t)c * a.mom_split * CS_NOUT;
+    double m = 0.0;
+    for (int q = 0; q < a.mom_split; ++q) m += Mc[(int64_t)q * CS_NOUT + o];  // chunk order
+    Ms[o] = m;
+  }
+  if (o < 9) ch[o] = a.chat[(int64_t)c * 9 + o];
+  __syncthreads();
   if (o >= CS_NOUT) return;
   const int f = o / CS_NMON, r = o % CS_NMON;
-  const double *Tr = a.T + ((int64_t)c * CS_NMON + r) * CS_NMON;
-  const double *Mf = a.M + (int64_t)c * CS_NOUT + f * CS_NMON;
+  const double *Mf = Ms + f * CS_NMON;
   double s = 0.0;
-  for (int q = 0; q < CS_NMON; ++q) s += Tr[q] * Mf[q];
+  for (int e = __ldg(a.t_ptr + r); e < __ldg(a.t_ptr + r + 1); ++e) {
+    const int sc = __ldg(a.t_col + e);
+    s += (ch[sc >> 8] * __ldg(a.t_coef + e)) * Mf[sc & 0xFF];
+  }
   a.H[(int64_t)c * CS_NOUT + o] = s;
 }
 
@@ -243,6 +275,12 @@ __global__ void cs_reset_status_kernel(cdk_run_status *st) {
 }
 __global__ void cs_advance_kernel(cdk_run_status *st, int64_t n) { st->steps_done += n; }
 
+// CTAs per community in the moments pass (g->max_comm: the largest community)
+static int cs_mom_split(const cdk_cs_graph *g) {
+  const int64_t mx = g->max_comm > 0 ? g->max_comm : 1;
+  return (int)((mx + CS_MOM_NODES - 1) / CS_MOM_NODES);
+}
+
 struct CsWs {
   double2 *s[2], *v[2], *ks, *kv;
   double *M, *H;
@@ -265,7 +303,7 @@ static CsWs cs_carve(const cdk_cs_graph *g, void *base, size_t *total) {
   }
   w.ks = (double2 *)take(n * 16);
   w.kv = (double2 *)take(n * 16);
-  w.M = (double *)take(m * CS_NOUT * 8);
+  w.M = (double *)take(m * (size_t)cs_mom_split(g) * CS_NOUT * 8);
   w.H = (double *)take(m * CS_NOUT * 8);
   w.status = (cdk_run_status *)take(sizeof(cdk_run_status));
   if (total) *total = off;
@@ -309,8 +347,12 @@ static CsArgs cs_args(const cdk_cs_graph *g, const CsWs &w, double K, double sig
   a.inter_col = g->inter_col;
   a.mu = reinterpret_cast<const double2 *>(g->mu);
   a.inv_L = g->inv_L;
-  a.T = g->T;
+  a.chat = g->chat;
+  a.t_ptr = g->t_ptr;
+  a.t_col = g->t_col;
+  a.t_coef = g->t_coef;
   a.M = w.M;
+  a.mom_split = cs_mom_split(g);
   a.H = w.H;
   a.ks = w.ks;
   a.kv = w.kv;
@@ -332,7 +374,7 @@ static unsigned cs_row_grid(int64_t n) {
 template <int MODE>
 static int cs_stage(CsArgs a, cudaStream_t st) {
   if (a.n_comm > 0) {
-    cs_moments_kernel<<<a.n_comm, 256, 0, st>>>(a);
+    cs_moments_kernel<<<dim3(a.n_comm, a.mom_split), 256, 0, st>>>(a);
     CDK_CHECK_LAUNCH("cs_moments_kernel");
     cs_contract_kernel<<<a.n_comm, 512, 0, st>>>(a);
     CDK_CHECK_LAUNCH("cs_contract_kernel");

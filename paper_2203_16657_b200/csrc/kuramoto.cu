@@ -1057,7 +1057,7 @@ __global__ void __launch_bounds__(NTHREADS, CDK_STAGE_MINBLOCKS) kuramoto_rk4_ke
                              // (measured: 14336 nodes, 224 KB, is 3% slower on config 2)
 #endif
 #ifndef CDK_ELL_DEPTH
-#define CDK_ELL_DEPTH 8  // 16-byte chunks per lane in flight (cp.async ring in shared memory)
+#define CDK_ELL_DEPTH 4  // chunks per lane in flight (cp.async ring in shared memory; measured 4 > 8 on config 2)
 #endif
 #ifndef CDK_ELL_XCOLS
 #define CDK_ELL_XCOLS 12  // inter columns per lane loaded before the intra loop (multiple of 4)
@@ -1070,11 +1070,7 @@ constexpr int ELL_XCOLS = CDK_ELL_XCOLS;
 #ifndef CDK_ELL_XEARLY
 #define CDK_ELL_XEARLY 4  // inter z gathers issued before the intra loop (4 <= . <= XCOLS)
 #endif
-#ifndef CDK_ELL_LDSB
-#define CDK_ELL_LDSB 8  // shared-memory gathers in flight per lane (8 or 4)
-#endif
 constexpr int ELL_XEARLY = CDK_ELL_XEARLY;
-constexpr int ELL_LDSB = CDK_ELL_LDSB;
 #ifndef CDK_ELL_MINBLOCKS
 #define CDK_ELL_MINBLOCKS 1  // resident ELL CTAs per SM (the planner launches SMs x this many)
 #endif
@@ -1129,25 +1125,23 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint64_t bytes) {
   }
 }
 
-// 8 entries of one chunk from the window: unconditional (pads hit zero slots)
+// 8 entries of one chunk from the window: unconditional (pads hit zero slots);
+// all 8 loads in flight, then their adds
 __device__ __forceinline__ void ell_gather8_smem(const uint4 w, uint32_t zs_addr, double &ar,
                                                  double &ai, double &br, double &bi) {
   const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  double2 z[8];
 #pragma unroll
-  for (int k0 = 0; k0 < 8; k0 += ELL_LDSB) {  // ELL_LDSB loads in flight, then their adds
-    double2 z[ELL_LDSB];
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+    z[k] = lds_d2(zs_addr + (u << 4));
+  }
 #pragma unroll
-    for (int k = 0; k < ELL_LDSB; ++k) {
-      const uint32_t u = (wv[(k0 + k) >> 1] >> (((k0 + k) & 1) * 16)) & 0xFFFFu;
-      z[k] = lds_d2(zs_addr + (u << 4));
-    }
-#pragma unroll
-    for (int k = 0; k < ELL_LDSB; k += 2) {
-      ar += z[k].x;
-      ai += z[k].y;
-      br += z[k + 1].x;
-      bi += z[k + 1].y;
-    }
+  for (int k = 0; k < 8; k += 2) {
+    ar += z[k].x;
+    ai += z[k].y;
+    br += z[k + 1].x;
+    bi += z[k + 1].y;
   }
 }
 
@@ -1411,6 +1405,28 @@ struct EllSmem {
 
 // MODE: 0 RHS, 1..4 RK4 stage, 5 Euler (a runtime value: constant-folded in
 // the per-stage kernels, one uniform branch per row in the persistent one)
+#ifdef CDK_PROFILE
+// intra-CTA drain of one segment: each warp's finish time after the segment
+// became ready; prof[14 n_cta + 4 cta + {0: sum over warps of (last finish -
+// own finish), 1: (last finish - ready) x warps, 2: segments}] (ns)
+__device__ void ell_prof_drain(const StageArgs &a, unsigned long long t_ready) {
+  __shared__ unsigned long long fin[ELL_WARPS];
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if ((threadIdx.x & 31) == 0) fin[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0 && a.prof) {
+    unsigned long long mx = 0, sum = 0;
+    for (int w = 0; w < ELL_WARPS; ++w) mx = fin[w] > mx ? fin[w] : mx;
+    for (int w = 0; w < ELL_WARPS; ++w) sum += mx - fin[w];
+    unsigned long long *p = a.prof + 14 * gridDim.x + 4 * blockIdx.x;
+    atomicAdd(p, sum);
+    atomicAdd(p + 1, (mx - t_ready) * ELL_WARPS);
+    atomicAdd(p + 2, 1ull);
+  }
+}
+#endif
+
 __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, const StageVar &v,
                                          const EllSmem &sm, uint32_t &phase) {
   const cdk_graph &g = a.g;
@@ -1480,6 +1496,8 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
     }
 #ifdef CDK_PROFILE
     if (tid == 0 && a.prof && s == segA) a.prof[6 * blockIdx.x + 1] = clock64();  // ready (raw)
+    unsigned long long t_ready;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
 #endif
     const double2 *zglob = v.z_in + g.seg_base[s];
     const int uB = g.seg_unit[s + 1];
@@ -1518,6 +1536,9 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
         ma = na;
         mb = nb;
       }
+#ifdef CDK_PROFILE
+      ell_prof_drain(a, t_ready);
+#endif
       __syncthreads();  // window and counters reused by the next segment
       continue;
     }

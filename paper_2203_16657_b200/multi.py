@@ -372,7 +372,9 @@ def bench_main(args):
     cfg = getattr(args, "config", "cfg2")
     # fused exchange (NVLink P2P stores + peer barrier) when every peer is
     # reachable; CDK_P2P=0 falls back to the NCCL all-gather after each stage
-    p2p = os.environ.get("CDK_P2P", "1") != "0" and world > 1 and all(
+    from .settings import settings
+
+    p2p = settings().p2p and world > 1 and all(
         torch.cuda.can_device_access_peer(local, q) for q in range(torch.cuda.device_count())
         if q != local)
     if cfg == "cfg5":

@@ -156,19 +156,19 @@ def ell_window_nodes() -> int:
     from ._lib import load_library
 
     cap = int(load_library().cdk_kuramoto_ell_window_nodes())
-    env = _os.environ.get("CDK_ELL_WINDOW")
-    return min(cap, int(env) // WIN_ALIGN * WIN_ALIGN) if env else cap
+    w = settings().ell_window
+    return min(cap, w // WIN_ALIGN * WIN_ALIGN) if w > 0 else cap
 
 
 def ell_enabled() -> bool:
     """lane-per-row ELL kernels for graphs without the inter sweep (CDK_ELL=0: off)"""
-    return _os.environ.get("CDK_ELL", "1") != "0"
+    return settings().ell
 
 
 def ell_calibrate_iters() -> int:
     """measured re-cuts of the ELL CTA ranges at DeviceGraph construction
     (CDK_ELL_CALIBRATE, 0 = off)"""
-    return int(_os.environ.get("CDK_ELL_CALIBRATE", 4))
+    return settings().ell_calibrate
 
 
 def ctas_per_sm() -> int:
@@ -179,18 +179,18 @@ def ctas_per_sm() -> int:
     return int(load_library().cdk_kuramoto_stage_ctas_per_sm())
 
 
-import os as _os
+from .settings import settings
 
-ROWS_CAP = int(_os.environ.get("CDK_ROWS_CAP", 1536))  # rows per segment (multiple of 8)
+ROWS_CAP = settings().rows_cap  # rows per segment (multiple of 8)
 # shared-memory budget of the stage kernel (CDK_SMEM_BUDGET: experiments with
 # a smaller carve-out, which leaves more L1 for in-flight global loads)
-SMEM_BUDGET = int(_os.environ.get("CDK_SMEM_BUDGET", 232448 - 2048))
+SMEM_BUDGET = settings().smem_budget
 SEG_MAX_COMM = 64  # communities per staged segment (csrc/kuramoto.cu SEG_MAX_COMM)
 MAX_PASS = 4  # window passes per community (cdk_graph.intra_split packs 3 sub-run starts)
 XS_MAX = 16384  # staged inter columns per segment (cdk_graph.xs_cap), upper bound
 # fixed cost of a segment in cost-model units (~9k cycles per segment in the
 # per-CTA profile fit at ~0.22 cycles per unit); SCHED_ITERS re-cuts with it
-SEG_COST = float(_os.environ.get("CDK_SEG_COST", 40000))
+SEG_COST = settings().seg_cost
 SCHED_ITERS = 6
 XS_MIN = 1024
 
@@ -378,7 +378,7 @@ def build_schedule(lay: HostLayout, sm_count: int = DEFAULT_SMS, rows_cap: int =
     # window to the widest staged community and give the rest of the budget
     # to the segment's inter-column slice (row pipeline reads them from smem)
     xs_cap = 0
-    if (not ell and _os.environ.get("CDK_XS", "1") != "0" and not multi.any()
+    if (not ell and settings().xs and not multi.any()
             and lay.nnz_inter > 0 and stageable.any()):
         need = int((win_hi - win_lo)[stageable].max())
         rem = smem_budget - stage_smem_bytes(need, rows_cap)
@@ -530,10 +530,10 @@ class EllLayout:
 # config 2, tools/prof_ell.py): intra slot (one LDS.128 lane, 1/8 of a
 # wavefront), inter slot (a global z gather), per-rblock fixed work
 # (pointers, epilogue, sincos, partial) and per-segment staging
-ELL_SLOT_COST = float(_os.environ.get("CDK_ELL_SLOT_COST", 0.144))
-ELL_XSLOT_COST = float(_os.environ.get("CDK_ELL_XSLOT_COST", 0.39))
-ELL_RBLK_COST = float(_os.environ.get("CDK_ELL_RBLK_COST", 100.0))
-ELL_SEG_COST = float(_os.environ.get("CDK_ELL_SEG_COST", 6500.0))
+ELL_SLOT_COST = settings().ell_slot_cost
+ELL_XSLOT_COST = settings().ell_xslot_cost
+ELL_RBLK_COST = settings().ell_rblk_cost
+ELL_SEG_COST = settings().ell_seg_cost
 
 
 def _ell_call(lay: HostLayout, col, staged, shift, zero_slot, ell_off, out):
@@ -646,7 +646,7 @@ def _ell_meta(lay: HostLayout, sch: Schedule, ell_off, xell_off, units, seg_unit
 # chunks per work unit of split rblocks; 0 = no splitting (the default: the
 # split parts meet through a device-scope fence that stalls on the warp's
 # in-flight chunk loads, measured slower on config 2)
-ELL_UNIT_CH = int(_os.environ.get("CDK_ELL_UNIT", 0))
+ELL_UNIT_CH = settings().ell_unit_ch
 
 
 def _ell_units(ell_off, xell_off, sch: Schedule):
@@ -699,11 +699,12 @@ def _comm_modes(lay: HostLayout):
     xl = (lay.inter_ptr[off[1:]] - lay.inter_ptr[off[:-1]]) / lam
     # 8 lanes everywhere: a per-community 4/8 choice split config 2 into 24%
     # more segments and cost 15% (segments cannot mix lane counts)
-    lpr = np.full(lens.shape[0], int(os.environ.get("CDK_LPR", 8)), dtype=np.int32)
-    fx = os.environ.get("CDK_INTER_PHASE")
-    sep = (np.full(lens.shape[0], fx == "1") if fx in ("0", "1") else xl > INTER_PHASE_MIN)
+    st = settings()
+    lpr = np.full(lens.shape[0], st.lpr, dtype=np.int32)
+    fx = st.inter_phase
+    sep = (np.full(lens.shape[0], fx == 1) if fx in (0, 1) else xl > INTER_PHASE_MIN)
     mode = (lpr | np.where(sep, SEG_INTER_PHASE, 0)).astype(np.int32)
-    pool = int(os.environ.get("CDK_LPR", 8)) | (SEG_INTER_PHASE if fx == "1" else 0)
+    pool = st.lpr | (SEG_INTER_PHASE if fx == 1 else 0)
     return mode, int(pool)
 
 
@@ -743,11 +744,9 @@ INTER_BLOCK_BYTES = 40e6  # target z bytes per column block
 def inter_blocking(n_rows: int) -> tuple[int, int]:
     """(inter_blocks, inter_block_nodes) for a graph of n_rows (CDK_INTER_BLOCKS
     overrides the block count; 0 disables)."""
-    import os
-
-    forced = os.environ.get("CDK_INTER_BLOCKS")
+    forced = settings().inter_blocks
     if forced is not None:
-        nb = int(forced)
+        nb = forced
     elif n_rows * 16 > INTER_SWEEP_BYTES:
         nb = int(min(4, max(2, np.ceil(n_rows * 16 / INTER_BLOCK_BYTES))))
     else:
@@ -914,7 +913,7 @@ class DeviceGraph:
             self._t["seg_unit"] = up(e.seg_unit)
             self._t["ell_part_base"] = up(e.ell_part_base if e.ell_part_base.size
                                           else np.full(1, -1, np.int32))
-            if e.ell_meta is not None and _os.environ.get("CDK_ELL_META", "1") != "0":
+            if e.ell_meta is not None and settings().ell_meta:
                 self._t["ell_meta"] = up(e.ell_meta if e.ell_meta.size else np.zeros(8, np.int32))
         _attach_inter_split(self, lay.n_rows)
         t = self._t

@@ -11,7 +11,7 @@ from paper_2203_16657_b200.engine import KuramotoEngine
 c = configs.config2(); dec = c.decomposition(); omega, theta0 = c.state()
 eng = KuramotoEngine(dec, omega, coupling=c.coupling, norm=c.n)
 n_cta = eng.graph.schedule.n_cta
-prof = torch.zeros(14 * n_cta, dtype=torch.int64, device="cuda")
+prof = torch.zeros(18 * n_cta, dtype=torch.int64, device="cuda")
 eng.lib.cdk_debug_set_profile_buffer(prof.data_ptr())
 eng.set_state(theta0)
 for rep in range(3):
@@ -19,7 +19,10 @@ for rep in range(3):
     ev[0].record(); eng.rk4(c.dt, 3); ev[1].record()
     torch.cuda.synchronize()
     print(f"rep {rep}: 3 RK4 steps {ev[0].elapsed_time(ev[1])*1e3:.1f} us")
-T = prof[6 * n_cta:].view(n_cta, 8).cpu().numpy().astype(np.float64)
+T = prof[6 * n_cta:14 * n_cta].view(n_cta, 8).cpu().numpy().astype(np.float64)
+D = prof[14 * n_cta:].view(n_cta, 4).cpu().numpy().astype(np.float64)
+print(f"intra-CTA drain: {D[:, 0].sum() / max(D[:, 1].sum(), 1):.3f} of warp time after segment ready "
+      f"({D[:, 2].sum():.0f} segments)")
 T -= T.min()
 for st in range(4):
     s0, s1 = T[:, 2 * st], T[:, 2 * st + 1]
