@@ -89,6 +89,10 @@ class CdkHoGraph(ctypes.Structure):
         ("inter_col", P),
         ("tri_ptr", P),
         ("tri_jk", P),
+        ("n_cta", I32),
+        ("win_cap", I32),
+        ("cta_rb", P),
+        ("cta_win", P),
     ]
 
 
@@ -170,6 +174,7 @@ _SIGS = {
     "cdk_nn_recurrence": [P, I64, I64, D, I64, P, P],
     "cdk_spin_field_sums": [P, I64, P, P, P],
     "cdk_triangles_sin": [P, I64, P, D, P, P],
+    "cdk_rank_one": [P, P, P, I64, D, P, P, P],
     "cdk_kuramoto_workspace_bytes": [ctypes.POINTER(CdkGraph)],
     "cdk_kuramoto_prepare": [ctypes.POINTER(CdkGraph), P, P, P],
     "cdk_kuramoto_rhs": [ctypes.POINTER(CdkGraph), P, P, D, P, P, P],
@@ -236,7 +241,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 14
+ABI_VERSION = 16
 
 _lock = threading.Lock()
 _lib = None

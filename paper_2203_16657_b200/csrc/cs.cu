@@ -60,12 +60,19 @@ __device__ __forceinline__ double eta_exact(double d2, double K, double sigma2, 
 }
 
 // moments of node chunk q of community c: CTA (c, q) sums nodes
-// [b + q * CS_MOM_NODES, ...) in node order, two independent accumulator
-// chains per thread; the contraction adds the chunks' partials in q order
+// [b + q * CS_MOM_NODES, ...) in node order.  Thread t owns the outputs
+// (f, i, j0..j0+3) (a "quad" of consecutive y powers): per node it forms
+// x^i f once and adds it times four y powers — 1.5 shared loads and 1.25
+// fp64 ops per output instead of 3 and 2, four independent chains.  The
+// contraction adds the chunks' partials in q order.
 constexpr int CS_MOM_NODES = 256;
-__global__ void __launch_bounds__(256) cs_moments_kernel(const CsArgs a) {
+constexpr int CS_NQUAD = 135;  // sum_i ceil((17 - i) / 4) x 3 functions
+__constant__ unsigned char c_quad_f[CS_NQUAD];
+__constant__ unsigned char c_quad_i[CS_NQUAD];
+__constant__ unsigned char c_quad_j[CS_NQUAD];
+__global__ void __launch_bounds__(160) cs_moments_kernel(const CsArgs a) {
   __shared__ double px[128][CS_D2 + 1];
-  __shared__ double py[128][CS_D2 + 1];
+  __shared__ double py[128][CS_D2 + 4];  // 3 zero pads: a quad may run past j = 16 - i
   __shared__ double pf[128][3];
   const int c = blockIdx.x, q = blockIdx.y;
   const int64_t cb = a.comm_off[c], ce = a.comm_off[c + 1];
@@ -73,13 +80,14 @@ __global__ void __launch_bounds__(256) cs_moments_kernel(const CsArgs a) {
   const int64_t e = min(ce, b + CS_MOM_NODES);
   const double2 mu = a.mu[c];
   const double il = a.inv_L[c];
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [output][chain]
-  const int o0 = threadIdx.x, o1 = threadIdx.x + 256;
+  const int t = threadIdx.x;
+  const bool act = t < CS_NQUAD;
+  const int f = act ? c_quad_f[t] : 0, i = act ? c_quad_i[t] : 0, j0 = act ? c_quad_j[t] : 0;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
   for (int64_t base = b; base < e; base += 128) {
     const int cnt = (int)min((int64_t)128, e - base);
     __syncthreads();
-    if (threadIdx.x < cnt) {
-      const int n = threadIdx.x;
+    for (int n = t; n < cnt; n += blockDim.x) {
       const double2 sv = a.s_in[base + n];
       const double2 v = a.v_in[base + n];
       const double x = (sv.x - mu.x) * il, y = (sv.y - mu.y) * il;
@@ -90,32 +98,30 @@ __global__ void __launch_bounds__(256) cs_moments_kernel(const CsArgs a) {
         xp *= x;
         yp *= y;
       }
+      py[n][CS_D2 + 1] = py[n][CS_D2 + 2] = py[n][CS_D2 + 3] = 0.0;
       pf[n][0] = 1.0;
       pf[n][1] = v.x;
       pf[n][2] = v.y;
     }
     __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int o = u ? o1 : o0;
-      if (o < CS_NOUT) {
-        const int f = o / CS_NMON, r = o % CS_NMON;
-        const int i = c_mono_i[r], j = c_mono_j[r];
-        double s0 = acc[u][0], s1 = acc[u][1];
-        int n = 0;
-        for (; n + 1 < cnt; n += 2) {
-          s0 += px[n][i] * py[n][j] * pf[n][f];
-          s1 += px[n + 1][i] * py[n + 1][j] * pf[n + 1][f];
-        }
-        if (n < cnt) s0 += px[n][i] * py[n][j] * pf[n][f];
-        acc[u][0] = s0;
-        acc[u][1] = s1;
+    if (act) {
+      for (int n = 0; n < cnt; ++n) {
+        const double xf = px[n][i] * pf[n][f];
+        acc0 += xf * py[n][j0];
+        acc1 += xf * py[n][j0 + 1];
+        acc2 += xf * py[n][j0 + 2];
+        acc3 += xf * py[n][j0 + 3];
       }
     }
   }
-  double *Mq = a.M + ((int64_t)c * a.mom_split + q) * CS_NOUT;
-  if (o0 < CS_NOUT) Mq[o0] = acc[0][0] + acc[0][1];
-  if (o1 < CS_NOUT) Mq[o1] = acc[1][0] + acc[1][1];
+  if (act) {
+    double *Mq = a.M + ((int64_t)c * a.mom_split + q) * CS_NOUT + f * CS_NMON + c_mono_row[i];
+    const int nj = CS_D2 - i + 1;  // valid j of this i: 0..16-i
+    Mq[j0] = acc0;
+    if (j0 + 1 < nj) Mq[j0 + 1] = acc1;
+    if (j0 + 2 < nj) Mq[j0 + 2] = acc2;
+    if (j0 + 3 < nj) Mq[j0 + 3] = acc3;
+  }
 }
 
 // H^f_c = T_c M^f_c with T_c[r][s] = chat_c[k(r,s)] t_coef[r,s]: the shared
@@ -145,18 +151,52 @@ __global__ void __launch_bounds__(512) cs_contract_kernel(const CsArgs a) {
   a.H[(int64_t)c * CS_NOUT + o] = s;
 }
 
-#ifndef CDK_CS_UNROLL
-#define CDK_CS_UNROLL 2  // sparse-correction loops: entries in flight per lane
+#ifndef CDK_CS_BATCH
+#define CDK_CS_BATCH 4  // sparse-correction entries per lane in flight
 #endif
-constexpr int CS_UNROLL = CDK_CS_UNROLL;
+#ifndef CDK_CS_MINB
+#define CDK_CS_MINB 1  // resident cs_rows CTAs per SM the build targets
+#endif
+constexpr int CS_BATCH = CDK_CS_BATCH;
 #ifndef CDK_CS_LPR
 #define CDK_CS_LPR 4  // lanes per row of cs_rows (1, 2, 4, 8); measured 4 (+ unroll 2) best
 #endif
 constexpr int CS_LPR = CDK_CS_LPR;
 
+// sum over entries p = p0, p0 + CS_LPR, ... < p1 of eta(|s_j - s_m|^2)(v_j - v_m)
+// added onto (ax, ay) in entry order
+__device__ __forceinline__ void cs_sparse_sum(const CsArgs &a, const int32_t *__restrict__ col,
+                                              int64_t p0, int64_t p1, double2 sm, double2 vm,
+                                              double &ax, double &ay) {
+  for (int64_t p = p0; p < p1; p += CS_BATCH * CS_LPR) {
+    int jb[CS_BATCH];
+#pragma unroll
+    for (int b = 0; b < CS_BATCH; ++b) {
+      const int64_t q = p + (int64_t)b * CS_LPR;
+      jb[b] = q < p1 ? __ldg(col + q) : -1;
+    }
+    double2 sj[CS_BATCH], vj[CS_BATCH];
+#pragma unroll
+    for (int b = 0; b < CS_BATCH; ++b) {
+      const int j = jb[b] >= 0 ? jb[b] : 0;
+      sj[b] = __ldg(a.s_in + j);
+      vj[b] = __ldg(a.v_in + j);
+    }
+#pragma unroll
+    for (int b = 0; b < CS_BATCH; ++b) {
+      if (jb[b] >= 0) {
+        const double dx = sj[b].x - sm.x, dy = sj[b].y - sm.y;
+        const double w = eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta);
+        ax += w * (vj[b].x - vm.x);
+        ay += w * (vj[b].y - vm.y);
+      }
+    }
+  }
+}
+
 // MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.
 template <int MODE>
-__global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
+__global__ void __launch_bounds__(256, CDK_CS_MINB) cs_rows_kernel(const CsArgs a) {
   const int lane = threadIdx.x & 31, t = lane & (CS_LPR - 1);
   const unsigned gmask = CS_LPR == 32 ? 0xFFFFFFFFu
                                       : (((1u << CS_LPR) - 1u) << (lane & ~(CS_LPR - 1)));
@@ -200,26 +240,14 @@ __global__ void __launch_bounds__(256) cs_rows_kernel(const CsArgs a) {
         xp *= x8;
       }
     }
-    // exact sparse correction
+    // exact sparse correction: CS_BATCH columns per lane load first, then
+    // all their (s_j, v_j) gathers go out together (the column -> address ->
+    // gather chain is the loop's critical path); fixed per-lane order
     double ax = 0.0, ay = 0.0;
-#pragma unroll CS_UNROLL
-    for (int64_t p = a.miss_ptr[i] + t; p < a.miss_ptr[i + 1]; p += CS_LPR) {
-      const int j = a.miss_col[p];
-      const double2 sj = a.s_in[j], vj = a.v_in[j];
-      const double dx = sj.x - sm.x, dy = sj.y - sm.y;
-      const double w = eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta);
-      ax -= w * (vj.x - vm.x);
-      ay -= w * (vj.y - vm.y);
-    }
-#pragma unroll CS_UNROLL
-    for (int64_t p = a.inter_ptr[i] + t; p < a.inter_ptr[i + 1]; p += CS_LPR) {
-      const int j = a.inter_col[p];
-      const double2 sj = a.s_in[j], vj = a.v_in[j];
-      const double dx = sj.x - sm.x, dy = sj.y - sm.y;
-      const double w = eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta);
-      ax += w * (vj.x - vm.x);
-      ay += w * (vj.y - vm.y);
-    }
+    cs_sparse_sum(a, a.miss_col, a.miss_ptr[i] + t, a.miss_ptr[i + 1], sm, vm, ax, ay);
+    ax = -ax;
+    ay = -ay;
+    cs_sparse_sum(a, a.inter_col, a.inter_ptr[i] + t, a.inter_ptr[i + 1], sm, vm, ax, ay);
 #pragma unroll
     for (int o = CS_LPR / 2; o > 0; o >>= 1) {
       g0 += __shfl_xor_sync(gmask, g0, o);
@@ -324,7 +352,23 @@ static int cs_tables() {
     }
   }
   row[CS_D2 + 1] = (short)k;
+  unsigned char qf[CS_NQUAD], qi[CS_NQUAD], qj[CS_NQUAD];
+  int nq = 0;
+  for (int f = 0; f < 3; ++f)
+    for (int i = 0; i <= CS_D2; ++i)
+      for (int j = 0; j <= CS_D2 - i; j += 4, ++nq) {
+        qf[nq] = (unsigned char)f;
+        qi[nq] = (unsigned char)i;
+        qj[nq] = (unsigned char)j;
+      }
+  if (nq != CS_NQUAD) {
+    set_error("cs quad table size");
+    return CDK_INPUT;
+  }
   cudaError_t e = cudaMemcpyToSymbol(c_mono_i, mi, sizeof(mi));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_quad_f, qf, sizeof(qf));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_quad_i, qi, sizeof(qi));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_quad_j, qj, sizeof(qj));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mono_j, mj, sizeof(mj));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mono_row, row, sizeof(row));
   if (e != cudaSuccess) return cuda_status(e, "cs constant tables");
@@ -374,7 +418,7 @@ static unsigned cs_row_grid(int64_t n) {
 template <int MODE>
 static int cs_stage(CsArgs a, cudaStream_t st) {
   if (a.n_comm > 0) {
-    cs_moments_kernel<<<dim3(a.n_comm, a.mom_split), 256, 0, st>>>(a);
+    cs_moments_kernel<<<dim3(a.n_comm, a.mom_split), 160, 0, st>>>(a);
     CDK_CHECK_LAUNCH("cs_moments_kernel");
     cs_contract_kernel<<<a.n_comm, 512, 0, st>>>(a);
     CDK_CHECK_LAUNCH("cs_contract_kernel");

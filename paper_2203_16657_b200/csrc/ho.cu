@@ -17,6 +17,8 @@
 // pass 2 (U from P, triangle pairs, community sums Z, Z2, W from canonical
 // partials, epilogue).  Row groups of 8 lanes, warp per rblock, all
 // reductions fixed-order (bitwise deterministic).
+#include <climits>
+
 #include "common.cuh"
 
 namespace cdk {
@@ -35,6 +37,11 @@ struct HoArgs {
   const int32_t *inter_col;
   const int64_t *tri_ptr;        // [n+1] triangle pairs per row
   const int2 *tri_jk;            // (j,k); j < 0 marks an inter triangle (j = -j-1)
+  const int32_t *cta_rb;         // [n_cta+1] rblock range of each CTA (one community or pool)
+  const int64_t *cta_win;        // [n_cta][2] staged node window (w1 == w0: unstaged)
+  int32_t n_cta;
+  int32_t win_cap;               // largest staged window (nodes)
+  double2 *T;                    // [n] triangle sums of this stage (ho_tri_kernel)
   // state
   const double2 *z_in;
   double2 *z_out;
@@ -103,26 +110,37 @@ __device__ __forceinline__ void group_reduce(double2 &v, unsigned gmask) {
 #define CDK_HO_UNROLL 16  // lane = row gather loops: entries in flight per lane (4: 0.68, 8: 0.42, 16: 0.375, 32: 0.39 ms per cfg3 step)
 #endif
 constexpr int HO_UNROLL = CDK_HO_UNROLL;
-#ifndef CDK_HO_LANE_ROW
-#define CDK_HO_LANE_ROW 1  // gathers: lane = row (1) or 8 lanes per row, 4 rows at a time (0)
-#endif
+constexpr int HO_WARPS = 8;  // 256 threads; a CTA owns <= 8 rblocks of one community
+
+// Both passes: CTA q owns rblocks [cta_rb[q], cta_rb[q+1]) of one community
+// (or of the NONE pool), a warp per rblock, lane = row (32 independent
+// gather streams per warp).  A community no wider than the window cap is
+// staged in shared memory first (z, and P for pass 2), so its missing-edge
+// and missing-triangle gathers are LDS instead of random L2 loads; spanning
+// triangles and inter entries read global memory.  The arithmetic does not
+// depend on staging (same values, same order): bitwise identical results.
+__device__ __forceinline__ void ho_stage_window(double2 *dst, const double2 *src, int64_t w0,
+                                                int64_t w1) {
+  for (int64_t k = threadIdx.x; k < w1 - w0; k += blockDim.x) dst[k] = __ldcg(src + w0 + k);
+}
+
 // pass 1: Y, V (missing), X (inter), P = z Y, rblock partials of P
-__global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
-  const int lane = threadIdx.x & 31, t = lane & 7, grp = lane >> 3;
-  const unsigned gmask = 0xFFu << (lane & 24);
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int rb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; rb < a.n_rblk; rb += warps) {
+template <bool ST>
+__device__ __forceinline__ void ho_pass1_rows(const HoArgs &a, const double2 *zs, int64_t w0,
+                                              int rbA, int rbB) {
+  const int lane = threadIdx.x & 31;
+  for (int rb = rbA + (int)(threadIdx.x >> 5); rb < rbB; rb += HO_WARPS) {
     const int64_t row0 = a.rblk_row0[rb];
     const int nr = (int)(a.rblk_row0[rb + 1] - row0);
     double2 myP = make_double2(0.0, 0.0);
-#if CDK_HO_LANE_ROW
-    if (lane < nr) {  // lane = row (see pass 2)
+    if (lane < nr) {
       const int64_t i = row0 + lane;
       double2 y = make_double2(0.0, 0.0), v = y, x = y;
       const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
 #pragma unroll HO_UNROLL
       for (int64_t p = m0; p < m1; ++p) {
-        const double2 z = __ldg(a.z_in + a.miss_col[p]);
+        const int j = a.miss_col[p];
+        const double2 z = ST ? zs[j - w0] : __ldg(a.z_in + j);
         y = cadd(y, z);
         v = cadd(v, cmul(z, z));
       }
@@ -132,55 +150,79 @@ __global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
       a.Y[i] = y;
       a.V[i] = v;
       a.X[i] = x;
-      myP = cmul(__ldg(a.z_in + i), y);
+      myP = cmul(ST ? zs[i - w0] : __ldg(a.z_in + i), y);
       a.P[i] = myP;
     }
-    (void)t;
-    (void)grp;
-#else
-    for (int q = 0; q < 8; ++q) {
-      const int r = 4 * q + grp;
-      double2 y = make_double2(0.0, 0.0), v = y, x = y;
-      if (r < nr) {
-        const int64_t i = row0 + r;
-        for (int64_t p = a.miss_ptr[i] + t; p < a.miss_ptr[i + 1]; p += 8) {
-          const double2 z = __ldg(a.z_in + a.miss_col[p]);
-          y = cadd(y, z);
-          v = cadd(v, cmul(z, z));
-        }
-        for (int64_t p = a.inter_ptr[i] + t; p < a.inter_ptr[i + 1]; p += 8)
-          x = cadd(x, __ldg(a.z_in + a.inter_col[p]));
-      }
-      group_reduce(y, FULL);
-      group_reduce(v, FULL);
-      group_reduce(x, FULL);
-      double2 pr = make_double2(0.0, 0.0);
-      if (r < nr && t == 0) {
-        const int64_t i = row0 + r;
-        a.Y[i] = y;
-        a.V[i] = v;
-        a.X[i] = x;
-        pr = cmul(__ldg(a.z_in + i), y);
-        a.P[i] = pr;
-      }
-      // lane L of the warp collects row L's P
-      const double px = __shfl_sync(FULL, pr.x, (lane & 3) * 8);
-      const double py = __shfl_sync(FULL, pr.y, (lane & 3) * 8);
-      if ((lane >> 2) == q) myP = make_double2(px, py);
-    }
-#endif
-    (void)gmask;
     const double2 part = rblock_partial(myP);
     if (lane == 0) a.pP[rb] = part;
   }
 }
 
+__global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
+  extern __shared__ __align__(16) double2 ho_sm[];
+  const int rbA = a.cta_rb[blockIdx.x], rbB = a.cta_rb[blockIdx.x + 1];
+  const int64_t w0 = a.cta_win[2 * blockIdx.x], w1 = a.cta_win[2 * blockIdx.x + 1];
+  if (w1 > w0) {
+    ho_stage_window(ho_sm, a.z_in, w0, w1);
+    __syncthreads();
+    ho_pass1_rows<true>(a, ho_sm, w0, rbA, rbB);
+  } else {
+    ho_pass1_rows<false>(a, ho_sm, w0, rbA, rbB);
+  }
+}
+
+// Triangle sums T_i = sum over the row's (j, k) pairs of -2 z_j z_k (missing-
+// graph triangles) or +2 z_j z_k (spanning triangles).  Rows have ~125 pairs
+// with a wide spread (max 338 on config 3), so lane = row inside the pass
+// kernels (one warp per rblock, ~10 warps per SM) left the gathers latency-
+// bound; here every row gets an 8-lane group over its CSR run (coalesced
+// 64-byte index reads, 4 pairs in flight per lane) and the grid covers all
+// rows at full occupancy.  Fixed per-lane order + xor butterfly.
+constexpr int HO_TRI_BATCH = 4;
+__global__ void __launch_bounds__(256) ho_tri_kernel(const HoArgs a) {
+  const int t = threadIdx.x & 7;
+  const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  if (i >= a.n_rows) return;  // whole 8-lane groups exit together
+  double tx = 0.0, ty = 0.0;
+  const int64_t q0 = a.tri_ptr[i], q1 = a.tri_ptr[i + 1];
+  for (int64_t p = q0 + t; p < q1; p += 8 * HO_TRI_BATCH) {
+    int2 jk[HO_TRI_BATCH];
+#pragma unroll
+    for (int b = 0; b < HO_TRI_BATCH; ++b)
+      jk[b] = (p + 8 * b < q1) ? __ldg(a.tri_jk + p + 8 * b) : make_int2(INT_MIN, 0);
+    double2 zj[HO_TRI_BATCH], zk[HO_TRI_BATCH];
+#pragma unroll
+    for (int b = 0; b < HO_TRI_BATCH; ++b) {
+      const bool pad = jk[b].x == INT_MIN;
+      const int j = pad ? 0 : (jk[b].x < 0 ? -jk[b].x - 1 : jk[b].x);
+      zj[b] = __ldg(a.z_in + j);
+      zk[b] = __ldg(a.z_in + (pad ? 0 : jk[b].y));
+    }
+#pragma unroll
+    for (int b = 0; b < HO_TRI_BATCH; ++b) {
+      if (jk[b].x != INT_MIN) {
+        const double2 w = cmul(zj[b], zk[b]);
+        const double s = jk[b].x < 0 ? 2.0 : -2.0;  // spanning +2, missing -2
+        tx += s * w.x;
+        ty += s * w.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    tx += __shfl_xor_sync(gmask, tx, o);
+    ty += __shfl_xor_sync(gmask, ty, o);
+  }
+  if (t == 0) a.T[i] = make_double2(tx, ty);
+}
+
 // pass 2: U, triangles, community sums, epilogue (MODE 0 rhs, 1..4 RK4, 5 Euler)
-template <int MODE>
-__global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
-  const int lane = threadIdx.x & 31, t = lane & 7, grp = lane >> 3;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int rb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; rb < a.n_rblk; rb += warps) {
+template <int MODE, bool ST>
+__device__ __forceinline__ void ho_pass2_rows(const HoArgs &a, const double2 *zs,
+                                              const double2 *Ps, int64_t w0, int rbA, int rbB) {
+  const int lane = threadIdx.x & 31;
+  for (int rb = rbA + (int)(threadIdx.x >> 5); rb < rbB; rb += HO_WARPS) {
     const int64_t row0 = a.rblk_row0[rb];
     const int nr = (int)(a.rblk_row0[rb + 1] - row0);
     const int c = a.rblk_comm[rb];
@@ -192,62 +234,21 @@ __global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
       Wc = comm_sum(a.pP, b0, b1, lane);
     }
     double2 myU = make_double2(0.0, 0.0), myT = myU;
-#if CDK_HO_LANE_ROW
-    // lane = row: 32 independent gather streams per warp (the warp count is
-    // one per rblock, so memory-level parallelism has to come from the lanes)
     if (lane < nr) {
       const int64_t i = row0 + lane;
       const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
 #pragma unroll HO_UNROLL
-      for (int64_t p = m0; p < m1; ++p) myU = cadd(myU, __ldcg(a.P + a.miss_col[p]));
-      const int64_t q0 = a.tri_ptr[i], q1 = a.tri_ptr[i + 1];
-#pragma unroll HO_UNROLL
-      for (int64_t p = q0; p < q1; ++p) {
-        const int2 jk = a.tri_jk[p];
-        const bool inter = jk.x < 0;
-        const int j = inter ? -jk.x - 1 : jk.x;
-        const double2 w = cmul(__ldg(a.z_in + j), __ldg(a.z_in + jk.y));
-        const double s = inter ? 2.0 : -2.0;  // missing -2 z_j z_k, spanning +2 z_j z_k
-        myT = cadd(myT, make_double2(s * w.x, s * w.y));
+      for (int64_t p = m0; p < m1; ++p) {
+        const int j = a.miss_col[p];
+        myU = cadd(myU, ST ? Ps[j - w0] : __ldcg(a.P + j));
       }
+      myT = __ldcg(a.T + i);  // the row's triangle sum (ho_tri_kernel)
     }
-    (void)t;
-    (void)grp;
-#else
-    for (int q = 0; q < 8; ++q) {
-      const int r = 4 * q + grp;
-      double2 u = make_double2(0.0, 0.0), tri = u;
-      if (r < nr) {
-        const int64_t i = row0 + r;
-        for (int64_t p = a.miss_ptr[i] + t; p < a.miss_ptr[i + 1]; p += 8)
-          u = cadd(u, __ldcg(a.P + a.miss_col[p]));
-        for (int64_t p = a.tri_ptr[i] + t; p < a.tri_ptr[i + 1]; p += 8) {
-          const int2 jk = a.tri_jk[p];
-          const bool inter = jk.x < 0;
-          const int j = inter ? -jk.x - 1 : jk.x;
-          const double2 w = cmul(__ldg(a.z_in + j), __ldg(a.z_in + jk.y));
-          // missing triangles enter S with -2 z_j z_k, spanning ones with +2 z_j z_k
-          const double s = inter ? 2.0 : -2.0;
-          tri = cadd(tri, make_double2(s * w.x, s * w.y));
-        }
-      }
-      group_reduce(u, FULL);
-      group_reduce(tri, FULL);
-      const double ux = __shfl_sync(FULL, u.x, (lane & 3) * 8);
-      const double uy = __shfl_sync(FULL, u.y, (lane & 3) * 8);
-      const double tx = __shfl_sync(FULL, tri.x, (lane & 3) * 8);
-      const double ty = __shfl_sync(FULL, tri.y, (lane & 3) * 8);
-      if ((lane >> 2) == q) {
-        myU = make_double2(ux, uy);
-        myT = make_double2(tx, ty);
-      }
-    }
-#endif
     // epilogue: lane = row
     double2 zn = make_double2(0.0, 0.0), zn2 = zn;
     if (lane < nr) {
       const int64_t i = row0 + lane;
-      const double2 zi = __ldg(a.z_in + i);
+      const double2 zi = ST ? zs[i - w0] : __ldg(a.z_in + i);
       const double2 Y = __ldcg(a.Y + i), V = __ldcg(a.V + i), X = __ldcg(a.X + i);
       double2 S = myT;
       double2 pair = make_double2(X.x - Y.x, X.y - Y.y);
@@ -302,6 +303,22 @@ __global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
   }
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
+  extern __shared__ __align__(16) double2 ho_sm[];
+  const int rbA = a.cta_rb[blockIdx.x], rbB = a.cta_rb[blockIdx.x + 1];
+  const int64_t w0 = a.cta_win[2 * blockIdx.x], w1 = a.cta_win[2 * blockIdx.x + 1];
+  if (w1 > w0) {
+    double2 *zs = ho_sm, *Ps = ho_sm + (w1 - w0);
+    ho_stage_window(zs, a.z_in, w0, w1);
+    ho_stage_window(Ps, a.P, w0, w1);
+    __syncthreads();
+    ho_pass2_rows<MODE, true>(a, zs, Ps, w0, rbA, rbB);
+  } else {
+    ho_pass2_rows<MODE, false>(a, ho_sm, ho_sm, w0, rbA, rbB);
+  }
+}
+
 // z = exp(i theta), rblock partials of z and z^2
 __global__ void __launch_bounds__(256) ho_prepare_kernel(const HoArgs a, const double *theta,
                                                          double2 *z, double2 *pz, double2 *pz2) {
@@ -327,7 +344,7 @@ __global__ void __launch_bounds__(256) ho_prepare_kernel(const HoArgs a, const d
 }
 
 struct HoWs {
-  double2 *z[2], *Y, *V, *X, *P, *pz[2], *pz2[2], *pP;
+  double2 *z[2], *Y, *V, *X, *P, *T, *pz[2], *pz2[2], *pP;
   double *ksum;
   cdk_run_status *status;
 };
@@ -348,6 +365,7 @@ static HoWs ho_carve(int64_t n, int32_t n_rblk, void *base, size_t *total) {
   w.V = (double2 *)take(nz * 16);
   w.X = (double2 *)take(nz * 16);
   w.P = (double2 *)take(nz * 16);
+  w.T = (double2 *)take(nz * 16);
   w.pz[0] = (double2 *)take(nb * 16);
   w.pz[1] = (double2 *)take(nb * 16);
   w.pz2[0] = (double2 *)take(nb * 16);
@@ -368,8 +386,12 @@ __global__ void ho_reset_status_kernel(cdk_run_status *st) {
 __global__ void ho_advance_kernel(cdk_run_status *st, int64_t n) { st->steps_done += n; }
 
 static int ho_check(const cdk_ho_graph *g) {
-  if (!g || g->n_rows < 0 || g->n_rblk < 0 || g->n_comm < 0) {
+  if (!g || g->n_rows < 0 || g->n_rblk < 0 || g->n_comm < 0 || g->n_cta < 0) {
     set_error("cdk_ho_graph: invalid sizes");
+    return CDK_INPUT;
+  }
+  if (g->win_cap < 0 || g->win_cap > CDK_HO_WIN_MAX || (g->n_cta > 0 && !(g->cta_rb && g->cta_win))) {
+    set_error("cdk_ho_graph: need cta_rb/cta_win and 0 <= win_cap <= CDK_HO_WIN_MAX");
     return CDK_INPUT;
   }
   return CDK_OK;
@@ -390,6 +412,11 @@ static HoArgs ho_args(const cdk_ho_graph *g, const HoWs &w, double *theta, const
   a.inter_col = g->inter_col;
   a.tri_ptr = g->tri_ptr;
   a.tri_jk = reinterpret_cast<const int2 *>(g->tri_jk);
+  a.cta_rb = g->cta_rb;
+  a.cta_win = g->cta_win;
+  a.n_cta = g->n_cta;
+  a.win_cap = g->win_cap;
+  a.T = w.T;
   a.Y = w.Y;
   a.V = w.V;
   a.X = w.X;
@@ -418,10 +445,28 @@ static int ho_stage(HoArgs a, int src, const HoWs &w, cudaStream_t st) {
   a.pz2_in = w.pz2[src];
   a.pz_out = w.pz[src ^ 1];
   a.pz2_out = w.pz2[src ^ 1];
-  const unsigned grid = ho_grid(a.n_rblk);
-  ho_pass1_kernel<<<grid, 256, 0, st>>>(a);
+  const size_t sm1 = (size_t)a.win_cap * 16, sm2 = 2 * sm1;
+  static int attr1 = -1, attr2 = -1;  // per MODE instantiation
+  if (sm1 > (size_t)attr1) {
+    cudaError_t e = cudaFuncSetAttribute(ho_pass1_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ho_pass1)");
+    attr1 = (int)sm1;
+  }
+  if (sm2 > (size_t)attr2) {
+    cudaError_t e = cudaFuncSetAttribute(ho_pass2_kernel<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ho_pass2)");
+    attr2 = (int)sm2;
+  }
+  if (a.n_cta == 0) return CDK_OK;
+  if (a.n_rows > 0) {
+    ho_tri_kernel<<<(unsigned)((a.n_rows * 8 + 255) / 256), 256, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("ho_tri_kernel");
+  }
+  ho_pass1_kernel<<<a.n_cta, 256, sm1, st>>>(a);
   CDK_CHECK_LAUNCH("ho_pass1_kernel");
-  ho_pass2_kernel<MODE><<<grid, 256, 0, st>>>(a);
+  ho_pass2_kernel<MODE><<<a.n_cta, 256, sm2, st>>>(a);
   CDK_CHECK_LAUNCH("ho_pass2_kernel");
   return CDK_OK;
 }

@@ -1236,6 +1236,8 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
   }
   const int64_t i = r0 + lane;
   const bool valid = i < r1;
+  DBG_CHECK(r1 <= g.n_rows && r1 - r0 <= 32, "rblock %d: rows [%lld, %lld) vs n_rows %lld", rb,
+            (long long)r0, (long long)r1, (long long)g.n_rows);
   // this unit's chunks (part of a split rblock) and inter entries (part 0)
   const int nch = uc.nch;
   // epilogue inputs: in flight during the gathers
@@ -1254,6 +1256,11 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
   int jx[ELL_XCOLS];
 #pragma unroll
   for (int q = 0; q < ELL_XCOLS; ++q) jx[q] = (q < nx) ? ldg(xc + 32 * q) : -1;
+#ifdef CDK_DEBUG
+  for (int q = 0; q < ELL_XCOLS; ++q)
+    DBG_CHECK(jx[q] < g.n_rows, "rblock %d: inter column %d >= n_rows %lld", rb, jx[q],
+              (long long)g.n_rows);
+#endif
   double2 xz[ELL_XEARLY];
 #pragma unroll
   for (int q = 0; q < ELL_XEARLY; ++q)
@@ -1276,6 +1283,16 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     cp_async_wait<ELL_DEPTH - 1>();  // chunk c has landed (groups complete in order)
     const uint32_t slot = ring + (uint32_t)(c & (ELL_DEPTH - 1)) * 512u;
     const uint4 w = lds_u4(slot);
+#ifdef CDK_DEBUG
+    if (STAGED) {  // every window index lands in the window or its 8 zero slots
+      const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t u = (wv[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+        DBG_CHECK(u < (uint32_t)g.smem_nodes + 8u, "rblock %d chunk %d: window index %u >= %d + 8",
+                  rb, c, u, g.smem_nodes);
+      }
+    }
+#endif
     if (STAGED) {
       ell_gather8_smem(w, zs_addr, ar, ai, br, bi);
     } else {

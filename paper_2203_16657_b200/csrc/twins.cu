@@ -323,6 +323,47 @@ __global__ void triangles_sin_kernel(const int64_t *tri, int64_t n_tri, const do
   atomicAdd(out + c, coef * sin((ta + tb) - 2.0 * tc));
 }
 
+// Appendix B.1 rank-one coupling: r = inv_n sum_l beta_l
+// e^{i x_l} (fixed-order two-level sum: per-block partials, then block order),
+// out_m = alpha_m r e^{-i x_m} (complex, interleaved).
+__global__ void rank_one_partial_kernel(const double *beta, const double *x, int64_t n,
+                                        double2 *part) {
+  __shared__ double sh[33];
+  double sr = 0.0, si = 0.0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < n;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    double s, c;
+    sincos(x[l], &s, &c);
+    sr += beta[l] * c;
+    si += beta[l] * s;
+  }
+  const double br = block_sum(sr, sh);
+  const double bi = block_sum(si, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(br, bi);
+}
+
+__global__ void rank_one_apply_kernel(const double *alpha, const double *x, int64_t n,
+                                      const double2 *part, int n_part, double inv_n,
+                                      double2 *out) {
+  __shared__ double2 r_sh;
+  if (threadIdx.x == 0) {
+    double rr = 0.0, ri = 0.0;
+    for (int q = 0; q < n_part; ++q) {  // block order
+      rr += part[q].x;
+      ri += part[q].y;
+    }
+    r_sh = make_double2(rr * inv_n, ri * inv_n);
+  }
+  __syncthreads();
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  double s, c;
+  sincos(x[m], &s, &c);
+  const double2 r = r_sh;
+  // alpha r e^{-ix}
+  out[m] = make_double2(alpha[m] * (r.x * c + r.y * s), alpha[m] * (r.y * c - r.x * s));
+}
+
 static inline unsigned grid_for(int64_t n) {
   return (unsigned)((n + TW_THREADS - 1) / TW_THREADS);
 }
@@ -502,5 +543,20 @@ extern "C" int cdk_triangles_sin(const int64_t *tri, int64_t n_tri, const double
   triangles_sin_kernel<<<grid_for(n_tri), TW_THREADS, 0, as_stream(stream)>>>(tri, n_tri, theta,
                                                                                coef, out);
   CDK_CHECK_LAUNCH("triangles_sin_kernel");
+  return CDK_OK;
+}
+
+extern "C" int cdk_rank_one(const double *alpha, const double *beta, const double *x, int64_t n,
+                            double inv_n, double *out, void *scratch, void *stream) {
+  if (n < 0) return set_error("rank_one: bad n"), CDK_INPUT;
+  if (n == 0) return CDK_OK;
+  cudaStream_t st = as_stream(stream);
+  constexpr int NPART = 148;  // scratch: NPART double2
+  auto *part = reinterpret_cast<double2 *>(scratch);
+  rank_one_partial_kernel<<<NPART, TW_THREADS, 0, st>>>(beta, x, n, part);
+  CDK_CHECK_LAUNCH("rank_one_partial_kernel");
+  rank_one_apply_kernel<<<grid_for(n), TW_THREADS, 0, st>>>(
+      alpha, x, n, part, NPART, inv_n, reinterpret_cast<double2 *>(out));
+  CDK_CHECK_LAUNCH("rank_one_apply_kernel");
   return CDK_OK;
 }
