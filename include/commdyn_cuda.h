@@ -39,7 +39,7 @@ extern "C" {
 #define CDK_INPUT 2
 #define CDK_CUDA 3
 
-#define CDK_ABI_VERSION 16
+#define CDK_ABI_VERSION 17
 #define CDK_INTRA_PAD 0xFFFFu /* padding entry in intra_col */
 
 /* ------------------------------------------------------------------------ */
@@ -340,15 +340,7 @@ typedef struct cdk_ho_graph {
   const int32_t *inter_col;      /* global columns */
   const int64_t *tri_ptr;        /* [n_rows+1] triangle pairs per row */
   const int32_t *tri_jk;         /* int32 pairs (j,k); j < 0: spanning triangle, j = -j-1 */
-  /* CTA work table: CTA q owns rblocks [cta_rb[q], cta_rb[q+1]) (<= 8, one
-   * community or the pool) and stages node window [cta_win[2q], cta_win[2q+1])
-   * of z (and P) in shared memory (empty window: global gathers) */
-  int32_t n_cta;
-  int32_t win_cap;               /* largest window, <= CDK_HO_WIN_MAX nodes */
-  const int32_t *cta_rb;         /* [n_cta+1] */
-  const int64_t *cta_win;        /* [n_cta][2] */
 } cdk_ho_graph;
-#define CDK_HO_WIN_MAX 6144
 
 CDK_API size_t cdk_ho_workspace_bytes(const cdk_ho_graph *g);
 CDK_API int cdk_ho_prepare(const cdk_ho_graph *g, const double *theta, void *workspace,

@@ -89,10 +89,6 @@ class CdkHoGraph(ctypes.Structure):
         ("inter_col", P),
         ("tri_ptr", P),
         ("tri_jk", P),
-        ("n_cta", I32),
-        ("win_cap", I32),
-        ("cta_rb", P),
-        ("cta_win", P),
     ]
 
 
@@ -241,7 +237,7 @@ _RESTYPES = {
 }
 
 EXPORTED = tuple(_SIGS)
-ABI_VERSION = 16
+ABI_VERSION = 17
 
 _lock = threading.Lock()
 _lib = None

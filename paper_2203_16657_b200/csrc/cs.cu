@@ -151,13 +151,11 @@ __global__ void __launch_bounds__(512) cs_contract_kernel(const CsArgs a) {
   a.H[(int64_t)c * CS_NOUT + o] = s;
 }
 
-#ifndef CDK_CS_BATCH
-#define CDK_CS_BATCH 4  // sparse-correction entries per lane in flight
-#endif
-#ifndef CDK_CS_MINB
-#define CDK_CS_MINB 1  // resident cs_rows CTAs per SM the build targets
-#endif
-constexpr int CS_BATCH = CDK_CS_BATCH;
+// sparse-correction entries per lane in flight, and resident cs_rows CTAs per
+// SM (register cap 80): measured on config 4, batch 2 x 3 CTAs 0.556 ms per
+// step, batch 4 x 3 0.564, batch 4 x 2 (114 registers) 0.624, batch 1 0.729
+constexpr int CS_BATCH = 2;
+constexpr int CS_MINB = 3;
 #ifndef CDK_CS_LPR
 #define CDK_CS_LPR 4  // lanes per row of cs_rows (1, 2, 4, 8); measured 4 (+ unroll 2) best
 #endif
@@ -196,7 +194,7 @@ __device__ __forceinline__ void cs_sparse_sum(const CsArgs &a, const int32_t *__
 
 // MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.
 template <int MODE>
-__global__ void __launch_bounds__(256, CDK_CS_MINB) cs_rows_kernel(const CsArgs a) {
+__global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
   const int lane = threadIdx.x & 31, t = lane & (CS_LPR - 1);
   const unsigned gmask = CS_LPR == 32 ? 0xFFFFFFFFu
                                       : (((1u << CS_LPR) - 1u) << (lane & ~(CS_LPR - 1)));

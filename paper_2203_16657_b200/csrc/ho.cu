@@ -13,9 +13,8 @@
 //   W_c = sum_{j in c} z_j Y_j, U_i = sum_j m_ij z_j Y_j,
 //   T_i = 2 sum over missing-graph triangles {i,j,k} of z_j z_k;
 // triangles spanning communities (or the NONE pool) are listed explicitly.
-// Per RHS: pass 1 (Y, V, inter sum X, P = z Y, rblock partials of P) and
-// pass 2 (U from P, triangle pairs, community sums Z, Z2, W from canonical
-// partials, epilogue).  Row groups of 8 lanes, warp per rblock, all
+// Per RHS (see the kernel comment below): row sums Y, V, X, T and P = z Y;
+// canonical rblock partials of P; U; community sums and the epilogue.  All
 // reductions fixed-order (bitwise deterministic).
 #include <climits>
 
@@ -37,11 +36,7 @@ struct HoArgs {
   const int32_t *inter_col;
   const int64_t *tri_ptr;        // [n+1] triangle pairs per row
   const int2 *tri_jk;            // (j,k); j < 0 marks an inter triangle (j = -j-1)
-  const int32_t *cta_rb;         // [n_cta+1] rblock range of each CTA (one community or pool)
-  const int64_t *cta_win;        // [n_cta][2] staged node window (w1 == w0: unstaged)
-  int32_t n_cta;
-  int32_t win_cap;               // largest staged window (nodes)
-  double2 *T;                    // [n] triangle sums of this stage (ho_tri_kernel)
+  double2 *T, *U;                // [n] triangle and U sums of this stage
   // state
   const double2 *z_in;
   double2 *z_out;
@@ -106,123 +101,130 @@ __device__ __forceinline__ void group_reduce(double2 &v, unsigned gmask) {
   }
 }
 
-#ifndef CDK_HO_UNROLL
-#define CDK_HO_UNROLL 16  // lane = row gather loops: entries in flight per lane (4: 0.68, 8: 0.42, 16: 0.375, 32: 0.39 ms per cfg3 step)
-#endif
-constexpr int HO_UNROLL = CDK_HO_UNROLL;
-constexpr int HO_WARPS = 8;  // 256 threads; a CTA owns <= 8 rblocks of one community
+// Per stage: every sum over a row's lists runs in 8-lane groups over the
+// row's CSR runs (coalesced index reads, HO_BATCH entries in flight per
+// lane, fixed per-lane order + xor butterfly) on a grid of all rows (full
+// occupancy: rows hold ~50 missing edges and ~125 triangle pairs on config 3
+// with a wide spread, and the lane-per-row passes of round 1 ran ~10 warps
+// per SM, latency-bound); only what needs a whole rblock — the canonical
+// partials and the epilogue — runs warp per rblock, lane = row.
+//   ho_rowsum: Y, V (missing), X (inter), T (triangle pairs), P = z Y
+//   ho_ppart:  canonical rblock partials of P
+//   ho_usum:   U = sum over missing edges of P_j
+//   ho_epi:    community sums Z, Z2, W from canonical partials + RK4 epilogue
+// entries per lane in flight and resident ho_rowsum CTAs per SM (64-register
+// cap): measured on config 3, batch 2 x 4 CTAs 0.252 ms per step, batch 4 x 4
+// 0.255, batch 4 or 8 x 2 CTAs 0.284
+constexpr int HO_BATCH = 2;
+constexpr int HO_ROWSUM_MINB = 4;
 
-// Both passes: CTA q owns rblocks [cta_rb[q], cta_rb[q+1]) of one community
-// (or of the NONE pool), a warp per rblock, lane = row (32 independent
-// gather streams per warp).  A community no wider than the window cap is
-// staged in shared memory first (z, and P for pass 2), so its missing-edge
-// and missing-triangle gathers are LDS instead of random L2 loads; spanning
-// triangles and inter entries read global memory.  The arithmetic does not
-// depend on staging (same values, same order): bitwise identical results.
-__device__ __forceinline__ void ho_stage_window(double2 *dst, const double2 *src, int64_t w0,
-                                                int64_t w1) {
-  for (int64_t k = threadIdx.x; k < w1 - w0; k += blockDim.x) dst[k] = __ldcg(src + w0 + k);
-}
-
-// pass 1: Y, V (missing), X (inter), P = z Y, rblock partials of P
-template <bool ST>
-__device__ __forceinline__ void ho_pass1_rows(const HoArgs &a, const double2 *zs, int64_t w0,
-                                              int rbA, int rbB) {
-  const int lane = threadIdx.x & 31;
-  for (int rb = rbA + (int)(threadIdx.x >> 5); rb < rbB; rb += HO_WARPS) {
-    const int64_t row0 = a.rblk_row0[rb];
-    const int nr = (int)(a.rblk_row0[rb + 1] - row0);
-    double2 myP = make_double2(0.0, 0.0);
-    if (lane < nr) {
-      const int64_t i = row0 + lane;
-      double2 y = make_double2(0.0, 0.0), v = y, x = y;
-      const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
-#pragma unroll HO_UNROLL
-      for (int64_t p = m0; p < m1; ++p) {
-        const int j = a.miss_col[p];
-        const double2 z = ST ? zs[j - w0] : __ldg(a.z_in + j);
-        y = cadd(y, z);
-        v = cadd(v, cmul(z, z));
-      }
-      const int64_t x0 = a.inter_ptr[i], x1 = a.inter_ptr[i + 1];
-#pragma unroll HO_UNROLL
-      for (int64_t p = x0; p < x1; ++p) x = cadd(x, __ldg(a.z_in + a.inter_col[p]));
-      a.Y[i] = y;
-      a.V[i] = v;
-      a.X[i] = x;
-      myP = cmul(ST ? zs[i - w0] : __ldg(a.z_in + i), y);
-      a.P[i] = myP;
-    }
-    const double2 part = rblock_partial(myP);
-    if (lane == 0) a.pP[rb] = part;
+__device__ __forceinline__ void group_reduce8(double2 &v, unsigned gmask) {
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(gmask, v.x, o);
+    v.y += __shfl_xor_sync(gmask, v.y, o);
   }
 }
 
-__global__ void __launch_bounds__(256) ho_pass1_kernel(const HoArgs a) {
-  extern __shared__ __align__(16) double2 ho_sm[];
-  const int rbA = a.cta_rb[blockIdx.x], rbB = a.cta_rb[blockIdx.x + 1];
-  const int64_t w0 = a.cta_win[2 * blockIdx.x], w1 = a.cta_win[2 * blockIdx.x + 1];
-  if (w1 > w0) {
-    ho_stage_window(ho_sm, a.z_in, w0, w1);
-    __syncthreads();
-    ho_pass1_rows<true>(a, ho_sm, w0, rbA, rbB);
-  } else {
-    ho_pass1_rows<false>(a, ho_sm, w0, rbA, rbB);
-  }
-}
-
-// Triangle sums T_i = sum over the row's (j, k) pairs of -2 z_j z_k (missing-
-// graph triangles) or +2 z_j z_k (spanning triangles).  Rows have ~125 pairs
-// with a wide spread (max 338 on config 3), so lane = row inside the pass
-// kernels (one warp per rblock, ~10 warps per SM) left the gathers latency-
-// bound; here every row gets an 8-lane group over its CSR run (coalesced
-// 64-byte index reads, 4 pairs in flight per lane) and the grid covers all
-// rows at full occupancy.  Fixed per-lane order + xor butterfly.
-constexpr int HO_TRI_BATCH = 4;
-__global__ void __launch_bounds__(256) ho_tri_kernel(const HoArgs a) {
+__global__ void __launch_bounds__(256, HO_ROWSUM_MINB) ho_rowsum_kernel(const HoArgs a) {
   const int t = threadIdx.x & 7;
   const unsigned gmask = 0xFFu << (threadIdx.x & 24);
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   if (i >= a.n_rows) return;  // whole 8-lane groups exit together
-  double tx = 0.0, ty = 0.0;
+  double2 y = make_double2(0.0, 0.0), v = y, x = y, tr = y;
+  const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
+  for (int64_t p = m0 + t; p < m1; p += 8 * HO_BATCH) {
+    int jb[HO_BATCH];
+#pragma unroll
+    for (int b = 0; b < HO_BATCH; ++b) jb[b] = (p + 8 * b < m1) ? __ldg(a.miss_col + p + 8 * b) : -1;
+    double2 zb[HO_BATCH];
+#pragma unroll
+    for (int b = 0; b < HO_BATCH; ++b) zb[b] = __ldg(a.z_in + (jb[b] >= 0 ? jb[b] : 0));
+#pragma unroll
+    for (int b = 0; b < HO_BATCH; ++b)
+      if (jb[b] >= 0) {
+        y = cadd(y, zb[b]);
+        v = cadd(v, cmul(zb[b], zb[b]));
+      }
+  }
+  const int64_t x0 = a.inter_ptr[i], x1 = a.inter_ptr[i + 1];
+  for (int64_t p = x0 + t; p < x1; p += 8) x = cadd(x, __ldg(a.z_in + a.inter_col[p]));
   const int64_t q0 = a.tri_ptr[i], q1 = a.tri_ptr[i + 1];
-  for (int64_t p = q0 + t; p < q1; p += 8 * HO_TRI_BATCH) {
-    int2 jk[HO_TRI_BATCH];
+  for (int64_t p = q0 + t; p < q1; p += 8 * HO_BATCH) {
+    int2 jk[HO_BATCH];
 #pragma unroll
-    for (int b = 0; b < HO_TRI_BATCH; ++b)
+    for (int b = 0; b < HO_BATCH; ++b)
       jk[b] = (p + 8 * b < q1) ? __ldg(a.tri_jk + p + 8 * b) : make_int2(INT_MIN, 0);
-    double2 zj[HO_TRI_BATCH], zk[HO_TRI_BATCH];
+    double2 zj[HO_BATCH], zk[HO_BATCH];
 #pragma unroll
-    for (int b = 0; b < HO_TRI_BATCH; ++b) {
+    for (int b = 0; b < HO_BATCH; ++b) {
       const bool pad = jk[b].x == INT_MIN;
       const int j = pad ? 0 : (jk[b].x < 0 ? -jk[b].x - 1 : jk[b].x);
       zj[b] = __ldg(a.z_in + j);
       zk[b] = __ldg(a.z_in + (pad ? 0 : jk[b].y));
     }
 #pragma unroll
-    for (int b = 0; b < HO_TRI_BATCH; ++b) {
+    for (int b = 0; b < HO_BATCH; ++b)
       if (jk[b].x != INT_MIN) {
         const double2 w = cmul(zj[b], zk[b]);
-        const double s = jk[b].x < 0 ? 2.0 : -2.0;  // spanning +2, missing -2
-        tx += s * w.x;
-        ty += s * w.y;
+        const double sg = jk[b].x < 0 ? 2.0 : -2.0;  // spanning +2, missing -2
+        tr.x += sg * w.x;
+        tr.y += sg * w.y;
       }
-    }
   }
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) {
-    tx += __shfl_xor_sync(gmask, tx, o);
-    ty += __shfl_xor_sync(gmask, ty, o);
+  group_reduce8(y, gmask);
+  group_reduce8(v, gmask);
+  group_reduce8(x, gmask);
+  group_reduce8(tr, gmask);
+  if (t == 0) {
+    a.Y[i] = y;
+    a.V[i] = v;
+    a.X[i] = x;
+    a.T[i] = tr;
+    a.P[i] = cmul(__ldg(a.z_in + i), y);
   }
-  if (t == 0) a.T[i] = make_double2(tx, ty);
 }
 
-// pass 2: U, triangles, community sums, epilogue (MODE 0 rhs, 1..4 RK4, 5 Euler)
-template <int MODE, bool ST>
-__device__ __forceinline__ void ho_pass2_rows(const HoArgs &a, const double2 *zs,
-                                              const double2 *Ps, int64_t w0, int rbA, int rbB) {
+__global__ void __launch_bounds__(256) ho_ppart_kernel(const HoArgs a) {
   const int lane = threadIdx.x & 31;
-  for (int rb = rbA + (int)(threadIdx.x >> 5); rb < rbB; rb += HO_WARPS) {
+  const int rb = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (rb >= a.n_rblk) return;
+  const int64_t row0 = a.rblk_row0[rb];
+  const int nr = (int)(a.rblk_row0[rb + 1] - row0);
+  const double2 pv = lane < nr ? __ldcg(a.P + row0 + lane) : make_double2(0.0, 0.0);
+  const double2 part = rblock_partial(pv);
+  if (lane == 0) a.pP[rb] = part;
+}
+
+__global__ void __launch_bounds__(256) ho_usum_kernel(const HoArgs a) {
+  const int t = threadIdx.x & 7;
+  const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  if (i >= a.n_rows) return;
+  double2 u = make_double2(0.0, 0.0);
+  const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
+  for (int64_t p = m0 + t; p < m1; p += 8 * HO_BATCH) {
+    int jb[HO_BATCH];
+#pragma unroll
+    for (int b = 0; b < HO_BATCH; ++b) jb[b] = (p + 8 * b < m1) ? __ldg(a.miss_col + p + 8 * b) : -1;
+    double2 pb[HO_BATCH];
+#pragma unroll
+    for (int b = 0; b < HO_BATCH; ++b) pb[b] = __ldcg(a.P + (jb[b] >= 0 ? jb[b] : 0));
+#pragma unroll
+    for (int b = 0; b < HO_BATCH; ++b)
+      if (jb[b] >= 0) u = cadd(u, pb[b]);
+  }
+  group_reduce8(u, gmask);
+  if (t == 0) a.U[i] = u;
+}
+
+// community sums from canonical partials + the RK4 epilogue (lane = row)
+template <int MODE>
+__global__ void __launch_bounds__(256) ho_epi_kernel(const HoArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int rb = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (rb >= a.n_rblk) return;
+  {
     const int64_t row0 = a.rblk_row0[rb];
     const int nr = (int)(a.rblk_row0[rb + 1] - row0);
     const int c = a.rblk_comm[rb];
@@ -233,22 +235,13 @@ __device__ __forceinline__ void ho_pass2_rows(const HoArgs &a, const double2 *zs
       Z2c = comm_sum(a.pz2_in, b0, b1, lane);
       Wc = comm_sum(a.pP, b0, b1, lane);
     }
-    double2 myU = make_double2(0.0, 0.0), myT = myU;
-    if (lane < nr) {
-      const int64_t i = row0 + lane;
-      const int64_t m0 = a.miss_ptr[i], m1 = a.miss_ptr[i + 1];
-#pragma unroll HO_UNROLL
-      for (int64_t p = m0; p < m1; ++p) {
-        const int j = a.miss_col[p];
-        myU = cadd(myU, ST ? Ps[j - w0] : __ldcg(a.P + j));
-      }
-      myT = __ldcg(a.T + i);  // the row's triangle sum (ho_tri_kernel)
-    }
+    const double2 myU = lane < nr ? __ldcg(a.U + row0 + lane) : make_double2(0.0, 0.0);
+    const double2 myT = lane < nr ? __ldcg(a.T + row0 + lane) : make_double2(0.0, 0.0);
     // epilogue: lane = row
     double2 zn = make_double2(0.0, 0.0), zn2 = zn;
     if (lane < nr) {
       const int64_t i = row0 + lane;
-      const double2 zi = ST ? zs[i - w0] : __ldg(a.z_in + i);
+      const double2 zi = __ldg(a.z_in + i);
       const double2 Y = __ldcg(a.Y + i), V = __ldcg(a.V + i), X = __ldcg(a.X + i);
       double2 S = myT;
       double2 pair = make_double2(X.x - Y.x, X.y - Y.y);
@@ -303,22 +296,6 @@ __device__ __forceinline__ void ho_pass2_rows(const HoArgs &a, const double2 *zs
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) ho_pass2_kernel(const HoArgs a) {
-  extern __shared__ __align__(16) double2 ho_sm[];
-  const int rbA = a.cta_rb[blockIdx.x], rbB = a.cta_rb[blockIdx.x + 1];
-  const int64_t w0 = a.cta_win[2 * blockIdx.x], w1 = a.cta_win[2 * blockIdx.x + 1];
-  if (w1 > w0) {
-    double2 *zs = ho_sm, *Ps = ho_sm + (w1 - w0);
-    ho_stage_window(zs, a.z_in, w0, w1);
-    ho_stage_window(Ps, a.P, w0, w1);
-    __syncthreads();
-    ho_pass2_rows<MODE, true>(a, zs, Ps, w0, rbA, rbB);
-  } else {
-    ho_pass2_rows<MODE, false>(a, ho_sm, ho_sm, w0, rbA, rbB);
-  }
-}
-
 // z = exp(i theta), rblock partials of z and z^2
 __global__ void __launch_bounds__(256) ho_prepare_kernel(const HoArgs a, const double *theta,
                                                          double2 *z, double2 *pz, double2 *pz2) {
@@ -344,7 +321,7 @@ __global__ void __launch_bounds__(256) ho_prepare_kernel(const HoArgs a, const d
 }
 
 struct HoWs {
-  double2 *z[2], *Y, *V, *X, *P, *T, *pz[2], *pz2[2], *pP;
+  double2 *z[2], *Y, *V, *X, *P, *T, *U, *pz[2], *pz2[2], *pP;
   double *ksum;
   cdk_run_status *status;
 };
@@ -366,6 +343,7 @@ static HoWs ho_carve(int64_t n, int32_t n_rblk, void *base, size_t *total) {
   w.X = (double2 *)take(nz * 16);
   w.P = (double2 *)take(nz * 16);
   w.T = (double2 *)take(nz * 16);
+  w.U = (double2 *)take(nz * 16);
   w.pz[0] = (double2 *)take(nb * 16);
   w.pz[1] = (double2 *)take(nb * 16);
   w.pz2[0] = (double2 *)take(nb * 16);
@@ -386,12 +364,8 @@ __global__ void ho_reset_status_kernel(cdk_run_status *st) {
 __global__ void ho_advance_kernel(cdk_run_status *st, int64_t n) { st->steps_done += n; }
 
 static int ho_check(const cdk_ho_graph *g) {
-  if (!g || g->n_rows < 0 || g->n_rblk < 0 || g->n_comm < 0 || g->n_cta < 0) {
+  if (!g || g->n_rows < 0 || g->n_rblk < 0 || g->n_comm < 0) {
     set_error("cdk_ho_graph: invalid sizes");
-    return CDK_INPUT;
-  }
-  if (g->win_cap < 0 || g->win_cap > CDK_HO_WIN_MAX || (g->n_cta > 0 && !(g->cta_rb && g->cta_win))) {
-    set_error("cdk_ho_graph: need cta_rb/cta_win and 0 <= win_cap <= CDK_HO_WIN_MAX");
     return CDK_INPUT;
   }
   return CDK_OK;
@@ -412,11 +386,8 @@ static HoArgs ho_args(const cdk_ho_graph *g, const HoWs &w, double *theta, const
   a.inter_col = g->inter_col;
   a.tri_ptr = g->tri_ptr;
   a.tri_jk = reinterpret_cast<const int2 *>(g->tri_jk);
-  a.cta_rb = g->cta_rb;
-  a.cta_win = g->cta_win;
-  a.n_cta = g->n_cta;
-  a.win_cap = g->win_cap;
   a.T = w.T;
+  a.U = w.U;
   a.Y = w.Y;
   a.V = w.V;
   a.X = w.X;
@@ -445,29 +416,24 @@ static int ho_stage(HoArgs a, int src, const HoWs &w, cudaStream_t st) {
   a.pz2_in = w.pz2[src];
   a.pz_out = w.pz[src ^ 1];
   a.pz2_out = w.pz2[src ^ 1];
-  const size_t sm1 = (size_t)a.win_cap * 16, sm2 = 2 * sm1;
-  static int attr1 = -1, attr2 = -1;  // per MODE instantiation
-  if (sm1 > (size_t)attr1) {
-    cudaError_t e = cudaFuncSetAttribute(ho_pass1_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ho_pass1)");
-    attr1 = (int)sm1;
-  }
-  if (sm2 > (size_t)attr2) {
-    cudaError_t e = cudaFuncSetAttribute(ho_pass2_kernel<MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ho_pass2)");
-    attr2 = (int)sm2;
-  }
-  if (a.n_cta == 0) return CDK_OK;
+  const unsigned row_grid = (unsigned)((a.n_rows * 8 + 255) / 256);
+  const unsigned rb_grid = (unsigned)(((int64_t)a.n_rblk * 32 + 255) / 256);
   if (a.n_rows > 0) {
-    ho_tri_kernel<<<(unsigned)((a.n_rows * 8 + 255) / 256), 256, 0, st>>>(a);
-    CDK_CHECK_LAUNCH("ho_tri_kernel");
+    ho_rowsum_kernel<<<row_grid, 256, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("ho_rowsum_kernel");
   }
-  ho_pass1_kernel<<<a.n_cta, 256, sm1, st>>>(a);
-  CDK_CHECK_LAUNCH("ho_pass1_kernel");
-  ho_pass2_kernel<MODE><<<a.n_cta, 256, sm2, st>>>(a);
-  CDK_CHECK_LAUNCH("ho_pass2_kernel");
+  if (a.n_rblk > 0) {
+    ho_ppart_kernel<<<rb_grid, 256, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("ho_ppart_kernel");
+  }
+  if (a.n_rows > 0) {
+    ho_usum_kernel<<<row_grid, 256, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("ho_usum_kernel");
+  }
+  if (a.n_rblk > 0) {
+    ho_epi_kernel<MODE><<<rb_grid, 256, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("ho_epi_kernel");
+  }
   return CDK_OK;
 }
 

@@ -135,35 +135,6 @@ def triangle_pairs(n: int, miss_tri: np.ndarray, span_tri: np.ndarray):
     return ptr, jk.astype(np.int32)
 
 
-HO_WIN_MAX = 6144  # include/commdyn_cuda.h CDK_HO_WIN_MAX
-HO_CTA_RBLK = 8  # rblocks per CTA (one warp each; csrc/ho.cu HO_WARPS)
-
-
-def ho_cta_table(lay):
-    """CTA work table of the pass kernels: each CTA owns <= 8 consecutive
-    rblocks of one community (or of the NONE pool) and stages that
-    community's node window when it fits (<= HO_WIN_MAX nodes).
-    Returns (cta_rb int32[n_cta+1], cta_win int64[n_cta, 2], win_cap)."""
-    off = lay.comm_off
-    cro = lay.comm_rblk_off
-    m = lay.n_comm
-    starts, wins = [], []
-    for c in range(m):
-        b0, b1 = int(cro[c]), int(cro[c + 1])
-        lam = int(off[c + 1] - off[c])
-        w = (int(off[c]), int(off[c + 1])) if lam <= HO_WIN_MAX else (0, 0)
-        for b in range(b0, b1, HO_CTA_RBLK):
-            starts.append(b)
-            wins.append(w)
-    for b in range(int(cro[m]) if m else 0, lay.n_rblk, HO_CTA_RBLK):  # NONE pool
-        starts.append(b)
-        wins.append((0, 0))
-    cta_rb = np.asarray(starts + [lay.n_rblk], dtype=np.int32)
-    cta_win = np.asarray(wins, dtype=np.int64).reshape(-1, 2)
-    win_cap = int((cta_win[:, 1] - cta_win[:, 0]).max()) if cta_win.size else 0
-    return cta_rb, cta_win, win_cap
-
-
 class HoDeviceGraph:
     def __init__(self, dec: Decomposition, device=None):
         import torch
@@ -188,9 +159,6 @@ class HoDeviceGraph:
             "inter_ptr": up(xptr), "inter_col": up(xcol if xcol.size else np.zeros(1, np.int32)),
             "tri_ptr": up(tptr), "tri_jk": up(tjk),
         }
-        cta_rb, cta_win, win_cap = ho_cta_table(lay)
-        self._t.update(cta_rb=up(cta_rb), cta_win=up(cta_win if cta_win.size
-                                                          else np.zeros(2, np.int64)))
         t = self._t
         self.n_rows = n
         self.device = dev
@@ -200,8 +168,7 @@ class HoDeviceGraph:
             comm_rblk_off=t["comm_rblk_off"].data_ptr(), miss_ptr=t["miss_ptr"].data_ptr(),
             miss_col=t["miss_col"].data_ptr(), inter_ptr=t["inter_ptr"].data_ptr(),
             inter_col=t["inter_col"].data_ptr(), tri_ptr=t["tri_ptr"].data_ptr(),
-            tri_jk=t["tri_jk"].data_ptr(), n_cta=int(cta_rb.shape[0] - 1), win_cap=win_cap,
-            cta_rb=t["cta_rb"].data_ptr(), cta_win=t["cta_win"].data_ptr())
+            tri_jk=t["tri_jk"].data_ptr())
 
 
 class HOEngine:
