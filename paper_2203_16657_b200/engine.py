@@ -50,17 +50,30 @@ class KuramotoEngine:
         self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         self._gp = ctypes.byref(self.graph.struct)
         self._rhs_ws = None
+        self._pinned = None  # host staging buffer for uploads from numpy
+
+    def _upload(self, dst, host) -> None:
+        """numpy (or host tensor) -> device view ``dst`` through a pinned staging
+        buffer (an async copy at full PCIe/C2C rate instead of a pageable one)."""
+        import torch
+
+        if torch.is_tensor(host):
+            dst.copy_(host.to(torch.float64), non_blocking=True)
+            return
+        if self._pinned is None:
+            self._pinned = torch.empty(self.n, dtype=torch.float64, pin_memory=True)
+        torch.cuda.current_stream(self.device).synchronize()  # staging buffer free again
+        self._pinned.numpy()[:] = np.asarray(host, dtype=np.float64)
+        dst.copy_(self._pinned, non_blocking=True)
 
     def set_params(self, omega, coupling: float, norm: float) -> None:
         """New model parameters on the same graph and workspace (the public API
         reuses one engine per decomposition across model objects)."""
         import torch
 
-        omega = torch.as_tensor(np.asarray(omega, dtype=np.float64) if not torch.is_tensor(omega)
-                                else omega, dtype=torch.float64)
-        if omega.shape != (self.n,):
+        if tuple(np.shape(omega)) != (self.n,):
             raise InputError(f"omega must have shape ({self.n},)")
-        self.omega.copy_(omega, non_blocking=True)
+        self._upload(self.omega, omega)
         self.coupling = float(coupling)
         self.norm = float(norm)
         self.k_over_n = self.coupling / self.norm
@@ -69,11 +82,12 @@ class KuramotoEngine:
     def set_state(self, theta, stream=None) -> None:
         import torch
 
-        t = theta if torch.is_tensor(theta) else torch.from_numpy(np.ascontiguousarray(theta,
-                                                                                   np.float64))
-        if t.shape != (self.n,):
+        if tuple(np.shape(theta)) != (self.n,):
             raise InputError(f"state must have shape ({self.n},)")
-        self.theta.copy_(t.to(self.device, torch.float64), non_blocking=True)
+        if torch.is_tensor(theta):
+            self.theta.copy_(theta.to(self.device, torch.float64), non_blocking=True)
+        else:
+            self._upload(self.theta, theta)
         self.prepare(stream)
 
     def prepare(self, stream=None) -> None:

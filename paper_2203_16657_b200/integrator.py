@@ -106,6 +106,19 @@ def cia_kernel_evals_per_rhs(model, dec: Decomposition) -> int:
     return n
 
 
+def _to_host(snaps) -> np.ndarray:
+    """Stack the recorded device states into one pinned host buffer (async
+    copies, one synchronisation)."""
+    import torch
+
+    buf = torch.empty((len(snaps),) + tuple(snaps[0].shape), dtype=snaps[0].dtype,
+                      pin_memory=True)
+    for k, sn in enumerate(snaps):
+        buf[k].copy_(sn, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return buf.numpy()
+
+
 class _ChunkTimer:
     """CUDA events around each recording chunk (one persistent launch)."""
 
@@ -177,8 +190,8 @@ def integrate(model, dec, x0, plan: IntegrationPlan) -> Trajectory:
         done += chunk
         times.append(min(done * dt, plan.t_end) if done < n_steps else plan.t_end)
         snaps.append(eng.theta.clone())
+    states_perm = _to_host(snaps)  # one pinned D2H of all records
     eng.check()
-    states_perm = np.stack([s.cpu().numpy() for s in snaps]) if n_steps else snaps[0].cpu().numpy()[None]
     states = np.empty_like(states_perm)
     states[:, perm] = states_perm
     wall = time.perf_counter() - t0
