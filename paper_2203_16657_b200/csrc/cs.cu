@@ -226,15 +226,17 @@ __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
       double x8 = 1.0;  // x^CS_LPR
       for (int k = 0; k < CS_LPR; ++k) x8 *= x;
       for (int p = t; p <= CS_D2; p += CS_LPR) {
-        const int r0 = c_mono_row[p];
-        double yq = 1.0;
-        for (int q = 0; q <= CS_D2 - p; ++q) {
-          const double w = xp * yq;
-          g0 += Hc[r0 + q] * w;
-          gx += Hc[CS_NMON + r0 + q] * w;
-          gy += Hc[2 * CS_NMON + r0 + q] * w;
-          yq *= y;
+        // Horner in y for the three functions, then one x^p term each
+        const int r0 = c_mono_row[p], nq = CS_D2 - p;
+        double h0 = Hc[r0 + nq], hx = Hc[CS_NMON + r0 + nq], hy = Hc[2 * CS_NMON + r0 + nq];
+        for (int q = nq - 1; q >= 0; --q) {
+          h0 = fma(h0, y, Hc[r0 + q]);
+          hx = fma(hx, y, Hc[CS_NMON + r0 + q]);
+          hy = fma(hy, y, Hc[2 * CS_NMON + r0 + q]);
         }
+        g0 = fma(xp, h0, g0);
+        gx = fma(xp, hx, gx);
+        gy = fma(xp, hy, gy);
         xp *= x8;
       }
     }

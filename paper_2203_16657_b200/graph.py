@@ -173,8 +173,10 @@ class Decomposition:
 
     @property
     def nnz_dir(self) -> int:
-        s = self.correction
-        return int(2 * np.count_nonzero(s.iu != s.iv))
+        if "nnz_dir" not in self._cache:  # an 11 M-pair scan on config 2: once
+            s = self.correction
+            self._cache["nnz_dir"] = int(2 * np.count_nonzero(s.iu != s.iv))
+        return self._cache["nnz_dir"]
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,51 @@
+"""The planner/driver knobs live in one module (paper_2203_16657_b200/settings.py);
+bench.py --gpus N launches its own ranks when not under torchrun (CPU)."""
+
+import sys
+
+import pytest
+
+from paper_2203_16657_b200 import plan, settings
+
+
+def test_defaults_and_env_overrides(monkeypatch):
+    for k in ("CDK_ELL", "CDK_ELL_CALIBRATE", "CDK_INTER_BLOCKS", "CDK_P2P", "CDK_LPR"):
+        monkeypatch.delenv(k, raising=False)
+    d = settings.settings()
+    assert d == settings.Settings()
+    assert d.ell and d.ell_calibrate == 4 and d.inter_blocks is None and d.p2p
+    monkeypatch.setenv("CDK_ELL", "0")
+    monkeypatch.setenv("CDK_ELL_CALIBRATE", "0")
+    monkeypatch.setenv("CDK_INTER_BLOCKS", "3")
+    monkeypatch.setenv("CDK_P2P", "0")
+    s = settings.settings()
+    assert not s.ell and s.ell_calibrate == 0 and s.inter_blocks == 3 and not s.p2p
+    assert not plan.ell_enabled() and plan.ell_calibrate_iters() == 0
+    assert plan.inter_blocking(100000)[0] == 3
+
+
+def test_bench_spawns_ranks(monkeypatch):
+    sys.path.insert(0, ".")
+    import bench
+
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "7"])
+    assert bench.main() == 0
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "7"]
+
+
+def test_reference_arm_config_matches_ours():
+    sys.path.insert(0, ".")
+    import bench
+    from paper_2203_16657_b200 import configs
+
+    c = configs.config2()
+    dec = c.decomposition()
+    cfg = bench.cfg2_config(c, dec)
+    assert cfg["n_nodes"] == 200000 and cfg["nnz_dir"] == dec.nnz_dir
+    with pytest.raises(KeyError):
+        cfg["parallelism"]  # setup details live outside the compared config dict
