@@ -48,6 +48,7 @@ struct CsArgs {
   double2 *s0, *v0;         // step-start state (RK4 base; written at stage 4)
   double2 *ks, *kv;         // RK4 accumulators
   double2 *out;             // MODE 0: v'
+  double2 *sacc;            // [n] exact sparse correction of this stage (cs_sparse_kernel)
   cdk_run_status *status;   // reserved = domain violations
   double K, sigma2, beta, inv_n, h;
   int64_t step_rel;
@@ -192,6 +193,33 @@ __device__ __forceinline__ void cs_sparse_sum(const CsArgs &a, const int32_t *__
   }
 }
 
+// Exact sparse correction of every row (CS_LPR lanes per row, CS_BATCH
+// columns per lane loaded first, then all their (s_j, v_j) gathers; fixed
+// per-lane order + xor butterfly): its own launch, so the gather loop runs at
+// the occupancy its ~40 registers allow instead of the bivariate evaluation's
+// 80 (the gathers are latency-bound: long_scoreboard 56 % when fused).
+__global__ void __launch_bounds__(256, 4) cs_sparse_kernel(const CsArgs a) {
+  const int lane = threadIdx.x & 31, t = lane & (CS_LPR - 1);
+  const unsigned gmask = CS_LPR == 32 ? 0xFFFFFFFFu
+                                      : (((1u << CS_LPR) - 1u) << (lane & ~(CS_LPR - 1)));
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / CS_LPR;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / CS_LPR; i < a.n_rows;
+       i += ngroups) {
+    const double2 sm = a.s_in[i], vm = a.v_in[i];
+    double ax = 0.0, ay = 0.0;
+    cs_sparse_sum(a, a.miss_col, a.miss_ptr[i] + t, a.miss_ptr[i + 1], sm, vm, ax, ay);
+    ax = -ax;
+    ay = -ay;
+    cs_sparse_sum(a, a.inter_col, a.inter_ptr[i] + t, a.inter_ptr[i + 1], sm, vm, ax, ay);
+#pragma unroll
+    for (int o = CS_LPR / 2; o > 0; o >>= 1) {
+      ax += __shfl_xor_sync(gmask, ax, o);
+      ay += __shfl_xor_sync(gmask, ay, o);
+    }
+    if (t == 0) a.sacc[i] = make_double2(ax, ay);
+  }
+}
+
 // MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.
 template <int MODE>
 __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
@@ -240,23 +268,15 @@ __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
         xp *= x8;
       }
     }
-    // exact sparse correction: CS_BATCH columns per lane load first, then
-    // all their (s_j, v_j) gathers go out together (the column -> address ->
-    // gather chain is the loop's critical path); fixed per-lane order
-    double ax = 0.0, ay = 0.0;
-    cs_sparse_sum(a, a.miss_col, a.miss_ptr[i] + t, a.miss_ptr[i + 1], sm, vm, ax, ay);
-    ax = -ax;
-    ay = -ay;
-    cs_sparse_sum(a, a.inter_col, a.inter_ptr[i] + t, a.inter_ptr[i + 1], sm, vm, ax, ay);
 #pragma unroll
     for (int o = CS_LPR / 2; o > 0; o >>= 1) {
       g0 += __shfl_xor_sync(gmask, g0, o);
       gx += __shfl_xor_sync(gmask, gx, o);
       gy += __shfl_xor_sync(gmask, gy, o);
-      ax += __shfl_xor_sync(gmask, ax, o);
-      ay += __shfl_xor_sync(gmask, ay, o);
     }
     if (t == 0) {
+      const double2 sa = __ldcg(a.sacc + i);  // the row's exact sparse correction
+      const double ax = sa.x, ay = sa.y;
       if (out_of_domain) atomicAdd(reinterpret_cast<unsigned long long *>(&a.status->reserved), 1ull);
       const double accx = (gx - vm.x * g0) + ax, accy = (gy - vm.y * g0) + ay;
       const double2 acc = make_double2(accx * a.inv_n, accy * a.inv_n);
@@ -310,7 +330,7 @@ static int cs_mom_split(const cdk_cs_graph *g) {
 }
 
 struct CsWs {
-  double2 *s[2], *v[2], *ks, *kv;
+  double2 *s[2], *v[2], *ks, *kv, *sacc;
   double *M, *H;
   cdk_run_status *status;
 };
@@ -330,6 +350,7 @@ static CsWs cs_carve(const cdk_cs_graph *g, void *base, size_t *total) {
     w.v[k] = (double2 *)take(n * 16);
   }
   w.ks = (double2 *)take(n * 16);
+  w.sacc = (double2 *)take(n * 16);
   w.kv = (double2 *)take(n * 16);
   w.M = (double *)take(m * (size_t)cs_mom_split(g) * CS_NOUT * 8);
   w.H = (double *)take(m * CS_NOUT * 8);
@@ -396,6 +417,7 @@ static CsArgs cs_args(const cdk_cs_graph *g, const CsWs &w, double K, double sig
   a.t_col = g->t_col;
   a.t_coef = g->t_coef;
   a.M = w.M;
+  a.sacc = w.sacc;
   a.mom_split = cs_mom_split(g);
   a.H = w.H;
   a.ks = w.ks;
@@ -423,6 +445,8 @@ static int cs_stage(CsArgs a, cudaStream_t st) {
     cs_contract_kernel<<<a.n_comm, 512, 0, st>>>(a);
     CDK_CHECK_LAUNCH("cs_contract_kernel");
   }
+  cs_sparse_kernel<<<cs_row_grid(a.n_rows), 256, 0, st>>>(a);
+  CDK_CHECK_LAUNCH("cs_sparse_kernel");
   cs_rows_kernel<MODE><<<cs_row_grid(a.n_rows), 256, 0, st>>>(a);
   CDK_CHECK_LAUNCH("cs_rows_kernel");
   return CDK_OK;

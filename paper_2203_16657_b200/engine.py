@@ -51,6 +51,17 @@ class KuramotoEngine:
         self._gp = ctypes.byref(self.graph.struct)
         self._rhs_ws = None
         self._pinned = None  # host staging buffer for uploads from numpy
+        self._stage_dev = None  # device staging buffer for permuted uploads
+
+    def upload_permuted(self, dst, host, perm_dev) -> None:
+        """dst = host[perm] with the gather on the device: the host array goes up
+        in its own (original) order through the pinned staging buffer."""
+        import torch
+
+        if self._stage_dev is None:
+            self._stage_dev = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        self._upload(self._stage_dev, host)
+        torch.index_select(self._stage_dev, 0, perm_dev, out=dst)
 
     def _upload(self, dst, host) -> None:
         """numpy (or host tensor) -> device view ``dst`` through a pinned staging

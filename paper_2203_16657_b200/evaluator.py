@@ -24,6 +24,18 @@ from .naive import NAIVE_N_CAP  # noqa: F401  (re-exported: the SPEC's memory gu
 from .plan import DeviceGraph
 
 
+def perm_device(dec: Decomposition):
+    """(perm, inv_perm) of the decomposition as cached int64 device tensors."""
+    import torch
+
+    t = dec._cache.get("perm_dev")
+    if t is None:
+        p = dec.partition
+        t = dec._cache["perm_dev"] = (torch.as_tensor(p.perm, device="cuda"),
+                                      torch.as_tensor(p.inv_perm, device="cuda"))
+    return t
+
+
 def _engine(model: Kuramoto, dec: Decomposition) -> KuramotoEngine:
     """One engine (device graph + workspace) per decomposition; a different
     model object only re-uploads omega and the coupling constants."""
@@ -36,7 +48,10 @@ def _engine(model: Kuramoto, dec: Decomposition) -> KuramotoEngine:
         raise InputError("omega shape does not match the decomposition")
     if cached is not None:
         eng = cached[1]
-        eng.set_params(omega[perm], model.coupling, model.norm_value())
+        eng.upload_permuted(eng.omega, omega, perm_device(dec)[0])
+        eng.coupling = float(model.coupling)
+        eng.norm = float(model.norm_value())
+        eng.k_over_n = eng.coupling / eng.norm
     else:
         dg = dec._cache.get("device_graph")
         if dg is None:

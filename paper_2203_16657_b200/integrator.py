@@ -170,13 +170,21 @@ def integrate(model, dec, x0, plan: IntegrationPlan) -> Trajectory:
     lib = eng.lib
     launches0 = int(lib.cdk_launch_count())
     t0 = time.perf_counter()
-    eng.set_state(x0[perm])
+    fast = hasattr(eng, "upload_permuted")  # classical engine: permutations on the device
+    if fast:
+        from .evaluator import perm_device
+
+        p_dev, inv_dev = perm_device(dec)
+        eng.upload_permuted(eng.theta, x0, p_dev)
+        eng.prepare()
+    else:
+        eng.set_state(x0[perm])
     stride = plan.record_every if plan.record_every > 0 else n_steps
     advance = eng.rk4 if plan.scheme == "rk4" else eng.euler
     timer = _ChunkTimer()
 
     times = [0.0]
-    snaps = [eng.theta.clone()]
+    snaps = [] if fast else [eng.theta.clone()]  # fast: the initial record is x0 itself
     done = 0
     while done < n_steps:
         chunk = min(stride, n_steps - done)
@@ -190,10 +198,17 @@ def integrate(model, dec, x0, plan: IntegrationPlan) -> Trajectory:
         done += chunk
         times.append(min(done * dt, plan.t_end) if done < n_steps else plan.t_end)
         snaps.append(eng.theta.clone())
-    states_perm = _to_host(snaps)  # one pinned D2H of all records
+    if fast:  # records back in original order, gathered on the device
+        import torch
+
+        recs = _to_host([torch.index_select(sn, 0, inv_dev) for sn in snaps]) if snaps else \
+            np.zeros((0, dec.n_nodes))
+        states = np.concatenate([x0[None], recs]) if n_steps else x0[None].copy()
+    else:
+        states_perm = _to_host(snaps)  # one pinned D2H of all records
+        states = np.empty_like(states_perm)
+        states[:, perm] = states_perm
     eng.check()
-    states = np.empty_like(states_perm)
-    states[:, perm] = states_perm
     wall = time.perf_counter() - t0
     stages = 4 if plan.scheme == "rk4" else 1
     return Trajectory(np.asarray(times), states, wall, int(lib.cdk_launch_count()) - launches0,

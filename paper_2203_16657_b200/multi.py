@@ -253,6 +253,40 @@ class ShardedKuramotoEngine:
                                                          self.eng.workspace.data_ptr(), 1,
                                                          _lib.stream_ptr(stream)), "advance")
 
+    def verify_fused(self, theta0, dt: float, steps: int = 2) -> str:
+        """Run ``steps`` RK4 steps with the fused NVLink exchange and with the
+        NCCL all-gather from the same state; keep the fused path only if both
+        trajectories are bitwise equal on every rank and no peer-barrier
+        watchdog fired (any failure: every rank falls back to NCCL).  Returns
+        a one-line verdict for the bench record."""
+        import torch
+        import torch.distributed as dist
+
+        if self.peers is None:
+            return "NCCL all-gather (fused exchange not available)"
+        ok, why = 1, ""
+        try:
+            self.set_state(theta0)
+            self.rk4(dt, steps)
+            torch.cuda.synchronize()
+            if self.eng.status().reserved:
+                raise RuntimeError("peer barrier watchdog fired")
+            fused = self.gather_theta()
+        except Exception as exc:  # noqa: BLE001 - any fused-path failure -> NCCL
+            ok, why, fused = 0, str(exc).splitlines()[0][:120], None
+        peers, self.peers = self.peers, None
+        self.set_state(theta0)
+        self.rk4(dt, steps)
+        ref = self.gather_theta()
+        if ok and not torch.equal(fused, ref):
+            ok, why = 0, "fused and NCCL trajectories differ"
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.eng.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 1:
+            self.peers = peers
+            return f"fused NVLink exchange (verified bitwise vs NCCL over {steps} steps)"
+        return "NCCL all-gather (fused exchange rejected: " + (why or "on another rank") + ")"
+
     def gather_theta(self):
         """Full theta on every rank (own slices exchanged)."""
         th = self.eng.theta.clone()
@@ -367,7 +401,8 @@ def bench_main(args):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    from bench import METRIC, UNIT, ClockSampler, _peaks, algorithmic_bytes_per_rhs  # noqa: E402
+    from bench import (METRIC, UNIT, ClockSampler, _peaks,  # noqa: E402
+                       algorithmic_bytes_per_rhs, cfg2_config)
 
     cfg = getattr(args, "config", "cfg2")
     # fused exchange (NVLink P2P stores + peer barrier) when every peer is
@@ -393,6 +428,7 @@ def bench_main(args):
         nnz_local = eng.graph.layout.nnz_dir
         workload = "cfg2 Kuramoto CIA RK4, SBM N=200000, sharded by community"
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    exchange = eng.verify_fused(theta0, case.dt) if world > 1 else "single rank"
     lib = eng.eng.lib
     nnz_t = torch.tensor([nnz_local], dtype=torch.int64, device="cuda")
     dist.all_reduce(nnz_t)
@@ -443,12 +479,11 @@ def bench_main(args):
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "n_nodes": case.n, "nnz_dir": nnz,
-                       "parallelism": f"community shards x{world} " + (
-                           "(fused exchange: epilogue NVLink P2P stores + peer barrier)"
-                           if eng.peers is not None else "(NCCL all-gather of z per stage)"),
-                       "l2": "flushed before every timed step" if flush is not None
-                       else "inputs >> L2", "ranges": eng.ranges},
+            "config": (cfg2_config(case, dec) if cfg != "cfg5" else
+                       {"workload": workload, "n_nodes": case.n, "nnz_dir": nnz,
+                        "l2": "inputs >> L2"}),
+            "setup": {"parallelism": f"community shards x{world}", "exchange": exchange,
+                      "ranges": eng.ranges},
             "roofline": {"bound": "hbm", "achieved": b_rhs / world / (stage_ms / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s", "peak_kind": peak_kind,
                          "frac": b_rhs / world / (stage_ms / 1e3) / 1e9 / peak, "traffic": None,
