@@ -220,26 +220,42 @@ __global__ void __launch_bounds__(256, 4) cs_sparse_kernel(const CsArgs a) {
   }
 }
 
-// MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.
+// MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.  CTA b owns rows
+// [64 b, 64 b + 64) (CS_LPR lanes per row); the contraction outputs H of the
+// communities those rows belong to are staged in shared memory first (every
+// row reads all 459 values of its community's H).
+constexpr int CS_ROWS_PER_CTA = 256 / CS_LPR;
+constexpr int CS_H_SLOTS = 4;  // communities staged per CTA (more: read from global)
 template <int MODE>
 __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
+  __shared__ double Hs[CS_H_SLOTS][CS_NOUT];
+  __shared__ int cfirst;
   const int lane = threadIdx.x & 31, t = lane & (CS_LPR - 1);
   const unsigned gmask = CS_LPR == 32 ? 0xFFFFFFFFu
                                       : (((1u << CS_LPR) - 1u) << (lane & ~(CS_LPR - 1)));
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / CS_LPR;
-  // rows of communities first, then NONE pool rows (no dense part)
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / CS_LPR; i < a.n_rows;
-       i += ngroups) {
-    // community of row i (binary search over comm_off)
-    int c = -1;
-    if (a.n_comm > 0 && i < a.comm_off[a.n_comm]) {
-      int lo = 0, hi = a.n_comm;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (a.comm_off[mid] <= i) lo = mid; else hi = mid;
-      }
-      c = lo;
+  const int64_t r0 = (int64_t)blockIdx.x * CS_ROWS_PER_CTA;
+  const int64_t n_in = a.n_comm > 0 ? a.comm_off[a.n_comm] : 0;
+  auto comm_of = [&](int64_t i) {  // binary search over comm_off
+    int lo = 0, hi = a.n_comm;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.comm_off[mid] <= i) lo = mid; else hi = mid;
     }
+    return lo;
+  };
+  if (threadIdx.x == 0) cfirst = (r0 < n_in) ? comm_of(r0) : -1;
+  __syncthreads();
+  const int c0 = cfirst;
+  if (c0 >= 0) {
+    for (int k = threadIdx.x; k < CS_H_SLOTS * CS_NOUT; k += blockDim.x) {
+      const int cc = c0 + k / CS_NOUT;
+      if (cc < a.n_comm) Hs[k / CS_NOUT][k % CS_NOUT] = __ldcg(a.H + (int64_t)cc * CS_NOUT + k % CS_NOUT);
+    }
+  }
+  __syncthreads();
+  const int64_t i = r0 + threadIdx.x / CS_LPR;
+  if (i < a.n_rows) {
+    const int c = (i < n_in) ? comm_of(i) : -1;
     const double2 sm = a.s_in[i], vm = a.v_in[i];
     double g0 = 0.0, gx = 0.0, gy = 0.0;
     bool out_of_domain = false;
@@ -248,7 +264,7 @@ __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
       const double il = a.inv_L[c];
       const double x = (sm.x - mu.x) * il, y = (sm.y - mu.y) * il;
       out_of_domain = (x * x + y * y) > 1.0 + 1e-12;
-      const double *Hc = a.H + (int64_t)c * CS_NOUT;
+      const double *Hc = (c - c0 < CS_H_SLOTS) ? Hs[c - c0] : a.H + (int64_t)c * CS_NOUT;
       double xp = 1.0;
       for (int k = 0; k < t; ++k) xp *= x;
       double x8 = 1.0;  // x^CS_LPR
@@ -447,7 +463,8 @@ static int cs_stage(CsArgs a, cudaStream_t st) {
   }
   cs_sparse_kernel<<<cs_row_grid(a.n_rows), 256, 0, st>>>(a);
   CDK_CHECK_LAUNCH("cs_sparse_kernel");
-  cs_rows_kernel<MODE><<<cs_row_grid(a.n_rows), 256, 0, st>>>(a);
+  cs_rows_kernel<MODE><<<(unsigned)((a.n_rows + CS_ROWS_PER_CTA - 1) / CS_ROWS_PER_CTA), 256, 0,
+                         st>>>(a);
   CDK_CHECK_LAUNCH("cs_rows_kernel");
   return CDK_OK;
 }

@@ -49,3 +49,18 @@ def test_reference_arm_config_matches_ours():
     assert cfg["n_nodes"] == 200000 and cfg["nnz_dir"] == dec.nnz_dir
     with pytest.raises(KeyError):
         cfg["parallelism"]  # setup details live outside the compared config dict
+
+
+def test_package_backend_mirror():
+    """paper_2203_16657_b200._backend keeps the reference's API
+    (commdyn/_backend.py:41-56): one backend, 'cuda'; the CPU backends are
+    selected in the reference through commdyn_hook."""
+    from paper_2203_16657_b200 import _backend as b
+
+    assert b.backend() == "cuda" and b.USE_CUDA and not b.USE_NUMBA
+    for name in ("numba", "numpy", "fortran"):
+        with pytest.raises(ValueError):
+            b.set_backend(name)
+    info = b.info()
+    assert info["library"].endswith(".so") and info["abi_version"] >= 1
+    assert isinstance(b.available(), bool)
