@@ -435,11 +435,37 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if ell and dg.schedule.ell is not None:
+        res["l1_pipe"] = l1_pipe_floor(dg, n, launch_ms, clocks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline_sample(case, dec, omega, theta0, steps=args.cpu_steps)
     if rank == 0:
         print(json.dumps(res), flush=True)
     return 0
+
+
+def l1_pipe_floor(dg, n, launch_ms, clocks):
+    """The bound that binds the ELL kernel: the SM's L1/shared
+    data pipe moves one 128-byte wavefront per cycle, and every gather costs
+    wavefronts whatever its bytes.  Counted from the layout, per RHS:
+    window gathers 4 per LDS.128 of 32 slots; the chunk stream 8 per 32-lane
+    chunk (4 written by cp.async into the ring, 4 read back); inter z gathers
+    1 each (one 32-byte sector per lane) + their column loads; ~18 per rblock
+    of epilogue loads/stores.  floor = wavefronts / (SMs x SM clock)."""
+    import torch
+
+    e, lay = dg.schedule.ell, dg.layout
+    slots = int(e.slots())
+    xslots = int(e.xell_col.shape[0])
+    w_rhs = slots / 8 + slots / 32 + int(lay.nnz_inter) + xslots / 32 + 18 * lay.n_rblk
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mhz = float(clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 0.0)
+    floor_ms = 4 * w_rhs / (sms * mhz * 1e6) * 1e3 if mhz else None
+    return {"unit": "128-byte wavefronts", "per_launch": int(4 * w_rhs),
+            "gather_slots_per_rhs": slots, "sm_count": sms, "sm_mhz": mhz,
+            "floor_ms": floor_ms, "frac": (floor_ms / launch_ms) if floor_ms else None,
+            "note": "the HBM roofline does not bind this kernel (CSR stays in L2 across "
+                    "stages); the L1/shared wavefront rate does: frac = floor / timed step"}
 
 
 def cpu_baseline_cfg5(case, csr, dg, omega, theta0, rows: int = 20000):
