@@ -33,6 +33,44 @@ inline int cuda_status(cudaError_t e, const char *what) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// --- fork/join onto an auxiliary stream --------------------------------------
+// Two independent kernels of one stage overlap instead of queueing: aux_fork
+// makes the per-device auxiliary stream wait for everything issued on `st` so
+// far and returns it (nullptr if it cannot be set up: the caller then stays
+// on `st`); aux_join makes `st` wait for everything issued on it since.
+struct AuxFork {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+inline AuxFork *aux_fork(cudaStream_t st) {
+  static thread_local AuxFork f[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  AuxFork &x = f[dev];
+  if (!x.aux) {
+    int lo = 0, hi = 0;  // the side stream's (smaller) kernels go first when CTA slots free up
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&x.aux, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      x = AuxFork{};
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  if (cudaEventRecord(x.fork, st) != cudaSuccess ||
+      cudaStreamWaitEvent(x.aux, x.fork, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return &x;
+}
+inline int aux_join(AuxFork *f, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(f->join, f->aux);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, f->join, 0);
+  return cuda_status(e, "aux stream join");
+}
+
 // --- IEEE ops that must not be contracted into FMA (mirror numpy rounding) --
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }

@@ -42,6 +42,7 @@ struct CsArgs {
   const double *t_coef;
   double *M;                // [M][mom_split][3][153] partial moments (node chunks)
   int32_t mom_split;        // CTAs per community in the moments pass
+  int32_t max_comm;         // largest community (nodes)
   double *H;                // [M][3][153]
   const double2 *s_in, *v_in;  // stage state
   double2 *s_out, *v_out;
@@ -218,6 +219,92 @@ __global__ void __launch_bounds__(256, 4) cs_sparse_kernel(const CsArgs a) {
     }
     if (t == 0) a.sacc[i] = make_double2(ax, ay);
   }
+}
+
+// The same sums with the community's state staged in shared memory: a CTA
+// owns CS_WIN_RB consecutive rblocks, stages (s, v) of the first one's
+// community (<= CS_WIN_CAP nodes, 32 bytes each) with coalesced loads, and
+// the missing-edge gathers of that community's rows become LDS.128 pairs
+// (~0.33 cycles per 16 bytes per SM with random bank conflicts) instead of two
+// L1/L2 sector gathers per entry (~1 cycle each).  Inter entries, pool rows
+// and an rblock of another community (a CTA straddling a boundary) keep the
+// global path.  Same per-lane entry order, same butterfly: bitwise equal to
+// cs_sparse_kernel.
+constexpr int CS_WIN_RB = 4;      // rblocks (<= 128 rows) per CTA, CS_LPR lanes per row
+constexpr int CS_WIN_CAP = 3072;  // nodes: 96 KB of shared memory
+__device__ __forceinline__ void cs_sparse_sum_win(const CsArgs &a, const int32_t *__restrict__ col,
+                                                  int64_t p0, int64_t p1, double2 sm, double2 vm,
+                                                  const double2 *__restrict__ sS,
+                                                  const double2 *__restrict__ sV, int cb,
+                                                  double &ax, double &ay) {
+  for (int64_t p = p0; p < p1; p += CS_BATCH * CS_LPR) {
+    int jb[CS_BATCH];
+#pragma unroll
+    for (int b = 0; b < CS_BATCH; ++b) {
+      const int64_t q = p + (int64_t)b * CS_LPR;
+      jb[b] = q < p1 ? __ldg(col + q) : -1;
+    }
+    double2 sj[CS_BATCH], vj[CS_BATCH];
+#pragma unroll
+    for (int b = 0; b < CS_BATCH; ++b) {
+      const int j = jb[b] >= 0 ? jb[b] - cb : 0;
+      sj[b] = sS[j];
+      vj[b] = sV[j];
+    }
+#pragma unroll
+    for (int b = 0; b < CS_BATCH; ++b) {
+      if (jb[b] >= 0) {
+        const double dx = sj[b].x - sm.x, dy = sj[b].y - sm.y;
+        const double w = eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta);
+        ax += w * (vj[b].x - vm.x);
+        ay += w * (vj[b].y - vm.y);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * CS_WIN_RB * CS_LPR, 2) cs_sparse_win_kernel(const CsArgs a) {
+  extern __shared__ __align__(16) unsigned char cs_win_raw[];
+  const int lane = threadIdx.x & 31, t = lane & (CS_LPR - 1);
+  const unsigned gmask = CS_LPR == 32 ? 0xFFFFFFFFu
+                                      : (((1u << CS_LPR) - 1u) << (lane & ~(CS_LPR - 1)));
+  const int rb0 = blockIdx.x * CS_WIN_RB;
+  const int c0 = a.rblk_comm[rb0];
+  int64_t cb = 0, ce = 0;
+  if (c0 >= 0) {
+    cb = a.comm_off[c0];
+    ce = a.comm_off[c0 + 1];
+  }
+  const int nc = (int)(ce - cb);
+  double2 *sS = reinterpret_cast<double2 *>(cs_win_raw);
+  double2 *sV = sS + nc;
+  for (int k = threadIdx.x; k < nc; k += blockDim.x) {
+    sS[k] = a.s_in[cb + k];
+    sV[k] = a.v_in[cb + k];
+  }
+  __syncthreads();
+  const int g = threadIdx.x / CS_LPR;  // row slot of the CTA: rblock g / 32, row g % 32
+  const int rb = rb0 + (g >> 5);
+  if (rb >= a.n_rblk) return;
+  const int64_t i = a.rblk_row0[rb] + (g & 31);
+  if (i >= a.rblk_row0[rb + 1]) return;  // whole CS_LPR-lane groups leave together
+  const double2 sm = a.s_in[i], vm = a.v_in[i];
+  double ax = 0.0, ay = 0.0;
+  if (i >= cb && i < ce) {
+    cs_sparse_sum_win(a, a.miss_col, a.miss_ptr[i] + t, a.miss_ptr[i + 1], sm, vm, sS, sV, (int)cb,
+                      ax, ay);
+  } else {
+    cs_sparse_sum(a, a.miss_col, a.miss_ptr[i] + t, a.miss_ptr[i + 1], sm, vm, ax, ay);
+  }
+  ax = -ax;
+  ay = -ay;
+  cs_sparse_sum(a, a.inter_col, a.inter_ptr[i] + t, a.inter_ptr[i + 1], sm, vm, ax, ay);
+#pragma unroll
+  for (int o = CS_LPR / 2; o > 0; o >>= 1) {
+    ax += __shfl_xor_sync(gmask, ax, o);
+    ay += __shfl_xor_sync(gmask, ay, o);
+  }
+  if (t == 0) a.sacc[i] = make_double2(ax, ay);
 }
 
 // MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.  CTA b owns rows
@@ -435,6 +522,7 @@ static CsArgs cs_args(const cdk_cs_graph *g, const CsWs &w, double K, double sig
   a.M = w.M;
   a.sacc = w.sacc;
   a.mom_split = cs_mom_split(g);
+  a.max_comm = g->max_comm;
   a.H = w.H;
   a.ks = w.ks;
   a.kv = w.kv;
@@ -453,16 +541,39 @@ static unsigned cs_row_grid(int64_t n) {
   return (unsigned)(g > 0 ? g : 1);
 }
 
+// The community part of a stage (moments -> contraction, ~400 small CTAs at 3
+// warps per scheduler) and the exact sparse correction (every SM, gather
+// bound) are independent until cs_rows: the first runs on an auxiliary
+// stream forked from and joined back into the caller's with events, so the
+// two overlap instead of queueing (config 4: 47 us of the 138 us stage).
 template <int MODE>
 static int cs_stage(CsArgs a, cudaStream_t st) {
+  AuxFork *fk = a.n_comm > 0 ? aux_fork(st) : nullptr;
+  cudaStream_t sc = fk ? fk->aux : st;  // stream of the community part
   if (a.n_comm > 0) {
-    cs_moments_kernel<<<dim3(a.n_comm, a.mom_split), 160, 0, st>>>(a);
+    cs_moments_kernel<<<dim3(a.n_comm, a.mom_split), 160, 0, sc>>>(a);
     CDK_CHECK_LAUNCH("cs_moments_kernel");
-    cs_contract_kernel<<<a.n_comm, 512, 0, st>>>(a);
+    cs_contract_kernel<<<a.n_comm, 512, 0, sc>>>(a);
     CDK_CHECK_LAUNCH("cs_contract_kernel");
   }
-  cs_sparse_kernel<<<cs_row_grid(a.n_rows), 256, 0, st>>>(a);
-  CDK_CHECK_LAUNCH("cs_sparse_kernel");
+  if (a.max_comm > 0 && a.max_comm <= CS_WIN_CAP && a.n_rblk > 0) {
+    static bool optin = false;
+    const size_t smem = (size_t)a.max_comm * 32;
+    if (!optin) {
+      cudaError_t e = cudaFuncSetAttribute(cs_sparse_win_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           CS_WIN_CAP * 32);
+      if (e != cudaSuccess) return cuda_status(e, "cs_sparse_win_kernel shared memory");
+      optin = true;
+    }
+    cs_sparse_win_kernel<<<(unsigned)((a.n_rblk + CS_WIN_RB - 1) / CS_WIN_RB),
+                           32 * CS_WIN_RB * CS_LPR, smem, st>>>(a);
+    CDK_CHECK_LAUNCH("cs_sparse_win_kernel");
+  } else {
+    cs_sparse_kernel<<<cs_row_grid(a.n_rows), 256, 0, st>>>(a);
+    CDK_CHECK_LAUNCH("cs_sparse_kernel");
+  }
+  if (fk && aux_join(fk, st) != CDK_OK) return CDK_CUDA;  // cs_rows reads H
   cs_rows_kernel<MODE><<<(unsigned)((a.n_rows + CS_ROWS_PER_CTA - 1) / CS_ROWS_PER_CTA), 256, 0,
                          st>>>(a);
   CDK_CHECK_LAUNCH("cs_rows_kernel");

@@ -422,14 +422,18 @@ static int ho_stage(HoArgs a, int src, const HoWs &w, cudaStream_t st) {
     ho_rowsum_kernel<<<row_grid, 256, 0, st>>>(a);
     CDK_CHECK_LAUNCH("ho_rowsum_kernel");
   }
+  // the rblock partials of P (a few warps per SM) and the U sums both read
+  // the row sums' P and nothing of each other: side by side
+  AuxFork *fk = (a.n_rblk > 0 && a.n_rows > 0) ? aux_fork(st) : nullptr;
   if (a.n_rblk > 0) {
-    ho_ppart_kernel<<<rb_grid, 256, 0, st>>>(a);
+    ho_ppart_kernel<<<rb_grid, 256, 0, fk ? fk->aux : st>>>(a);
     CDK_CHECK_LAUNCH("ho_ppart_kernel");
   }
   if (a.n_rows > 0) {
     ho_usum_kernel<<<row_grid, 256, 0, st>>>(a);
     CDK_CHECK_LAUNCH("ho_usum_kernel");
   }
+  if (fk && aux_join(fk, st) != CDK_OK) return CDK_CUDA;
   if (a.n_rblk > 0) {
     ho_epi_kernel<MODE><<<rb_grid, 256, 0, st>>>(a);
     CDK_CHECK_LAUNCH("ho_epi_kernel");

@@ -106,13 +106,24 @@ def cia_kernel_evals_per_rhs(model, dec: Decomposition) -> int:
     return n
 
 
+_PINNED = {}  # (shape, dtype) -> pinned staging buffer of the last readback (<= 64 MB)
+
+
 def _to_host(snaps) -> np.ndarray:
     """Stack the recorded device states into one pinned host buffer (async
-    copies, one synchronisation)."""
+    copies, one synchronisation).  The buffer is kept for the next call of the
+    same shape (a pinned allocation costs more than a short trajectory's
+    readback): callers copy out of the returned view before returning."""
     import torch
 
-    buf = torch.empty((len(snaps),) + tuple(snaps[0].shape), dtype=snaps[0].dtype,
-                      pin_memory=True)
+    shape = (len(snaps),) + tuple(snaps[0].shape)
+    key = (shape, snaps[0].dtype)
+    buf = _PINNED.get(key)
+    if buf is None:
+        buf = torch.empty(shape, dtype=snaps[0].dtype, pin_memory=True)
+        if buf.numel() * buf.element_size() <= 64 << 20:
+            _PINNED.clear()
+            _PINNED[key] = buf
     for k, sn in enumerate(snaps):
         buf[k].copy_(sn, non_blocking=True)
     torch.cuda.current_stream().synchronize()
@@ -188,11 +199,14 @@ def integrate(model, dec, x0, plan: IntegrationPlan) -> Trajectory:
     done = 0
     while done < n_steps:
         chunk = min(stride, n_steps - done)
-        full = chunk if done + chunk < n_steps else chunk - 1
+        # the last step has its own size unless T is a multiple of dt (then
+        # the whole chunk is one persistent launch)
+        short_last = done + chunk == n_steps and dt_last != dt
+        full = chunk - 1 if short_last else chunk
         e0 = timer.start()
         if full > 0:
             advance(dt, full)
-        if done + chunk == n_steps:
+        if short_last:
             advance(dt_last, 1)
         timer.stop(e0, chunk)
         done += chunk
