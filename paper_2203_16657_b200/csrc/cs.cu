@@ -308,18 +308,25 @@ __global__ void __launch_bounds__(32 * CS_WIN_RB * CS_LPR, 2) cs_sparse_win_kern
 }
 
 // MODE 0: out = v'(s_in, v_in).  MODE 1..4: RK4 stage.  CTA b owns rows
-// [64 b, 64 b + 64) (CS_LPR lanes per row); the contraction outputs H of the
+// [CS_ROWS_PER_CTA b, ...) (CS_RLPR lanes per row); the contraction outputs H of the
 // communities those rows belong to are staged in shared memory first (every
 // row reads all 459 values of its community's H).
-constexpr int CS_ROWS_PER_CTA = 256 / CS_LPR;
+#ifndef CDK_CS_RLPR
+#define CDK_CS_RLPR 1  // lanes per row of cs_rows' bivariate evaluation
+#endif
+// With one lane per row every lane of a warp reads the same H entry of its
+// community (a broadcast: one wavefront per LDS instead of one per distinct
+// p residue), 459 LDS per 32 rows instead of per 8.
+constexpr int CS_RLPR = CDK_CS_RLPR;
+constexpr int CS_ROWS_PER_CTA = 256 / CS_RLPR;
 constexpr int CS_H_SLOTS = 4;  // communities staged per CTA (more: read from global)
 template <int MODE>
 __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
   __shared__ double Hs[CS_H_SLOTS][CS_NOUT];
   __shared__ int cfirst;
-  const int lane = threadIdx.x & 31, t = lane & (CS_LPR - 1);
-  const unsigned gmask = CS_LPR == 32 ? 0xFFFFFFFFu
-                                      : (((1u << CS_LPR) - 1u) << (lane & ~(CS_LPR - 1)));
+  const int lane = threadIdx.x & 31, t = lane & (CS_RLPR - 1);
+  const unsigned gmask = CS_RLPR == 32 ? 0xFFFFFFFFu
+                                      : (((1u << CS_RLPR) - 1u) << (lane & ~(CS_RLPR - 1)));
   const int64_t r0 = (int64_t)blockIdx.x * CS_ROWS_PER_CTA;
   const int64_t n_in = a.n_comm > 0 ? a.comm_off[a.n_comm] : 0;
   auto comm_of = [&](int64_t i) {  // binary search over comm_off
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
     }
   }
   __syncthreads();
-  const int64_t i = r0 + threadIdx.x / CS_LPR;
+  const int64_t i = r0 + threadIdx.x / CS_RLPR;
   if (i < a.n_rows) {
     const int c = (i < n_in) ? comm_of(i) : -1;
     const double2 sm = a.s_in[i], vm = a.v_in[i];
@@ -354,9 +361,9 @@ __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
       const double *Hc = (c - c0 < CS_H_SLOTS) ? Hs[c - c0] : a.H + (int64_t)c * CS_NOUT;
       double xp = 1.0;
       for (int k = 0; k < t; ++k) xp *= x;
-      double x8 = 1.0;  // x^CS_LPR
-      for (int k = 0; k < CS_LPR; ++k) x8 *= x;
-      for (int p = t; p <= CS_D2; p += CS_LPR) {
+      double x8 = 1.0;  // x^CS_RLPR
+      for (int k = 0; k < CS_RLPR; ++k) x8 *= x;
+      for (int p = t; p <= CS_D2; p += CS_RLPR) {
         // Horner in y for the three functions, then one x^p term each
         const int r0 = c_mono_row[p], nq = CS_D2 - p;
         double h0 = Hc[r0 + nq], hx = Hc[CS_NMON + r0 + nq], hy = Hc[2 * CS_NMON + r0 + nq];
@@ -372,7 +379,7 @@ __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
       }
     }
 #pragma unroll
-    for (int o = CS_LPR / 2; o > 0; o >>= 1) {
+    for (int o = CS_RLPR / 2; o > 0; o >>= 1) {
       g0 += __shfl_xor_sync(gmask, g0, o);
       gx += __shfl_xor_sync(gmask, gx, o);
       gy += __shfl_xor_sync(gmask, gy, o);
