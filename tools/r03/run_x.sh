@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_cs.py tests/test_gpu_long.py tests/test_gpu_naive.py tests/test_gpu_twins.py -x -q --timeout 600 > gpurun_out/rx_gputest.log 2>&1
+echo "rc=$?" >> gpurun_out/rx_gputest.log
+timeout 300 python tools/bench_cfg34.py --steps 50 --only cfg4 > gpurun_out/rx_cfg4.json 2>&1
