@@ -385,7 +385,7 @@ def run_ours(args):
 
         dec._cache["device_graph"] = dg
         e2e_times = []
-        for rep in range(2):
+        for rep in range(3):  # the first call builds the engine; min over the warm ones
             model = kuramoto_model(omega.copy(), case.coupling, case.n)
             flush_l2()
             torch.cuda.synchronize()

@@ -106,28 +106,37 @@ def cia_kernel_evals_per_rhs(model, dec: Decomposition) -> int:
     return n
 
 
-_PINNED = {}  # (shape, dtype) -> pinned staging buffer of the last readback (<= 64 MB)
+_WARMED = set()  # readback sizes with a spare pinned block on the free list
 
 
-def _to_host(snaps) -> np.ndarray:
+def _to_host(snaps, first=None) -> np.ndarray:
     """Stack the recorded device states into one pinned host buffer (async
-    copies, one synchronisation).  The buffer is kept for the next call of the
-    same shape (a pinned allocation costs more than a short trajectory's
-    readback): callers copy out of the returned view before returning."""
+    copies, one synchronisation) and return it as the trajectory's array;
+    ``first`` (a host array) becomes record 0.  The pinned block comes from
+    torch's caching host allocator: once an earlier trajectory has been
+    dropped the allocation is a free-list hit, and handing the buffer itself
+    to the caller saves a pageable copy of every record."""
     import torch
 
-    shape = (len(snaps),) + tuple(snaps[0].shape)
-    key = (shape, snaps[0].dtype)
-    buf = _PINNED.get(key)
-    if buf is None:
-        buf = torch.empty(shape, dtype=snaps[0].dtype, pin_memory=True)
-        if buf.numel() * buf.element_size() <= 64 << 20:
-            _PINNED.clear()
-            _PINNED[key] = buf
+    k0 = 0 if first is None else 1
+    shape = (len(snaps) + k0,) + tuple(snaps[0].shape if snaps else np.shape(first))
+    dtype = snaps[0].dtype if snaps else torch.float64
+    buf = torch.empty(shape, dtype=dtype, pin_memory=True)
+    nbytes = buf.numel() * buf.element_size()
+    if nbytes not in _WARMED and nbytes <= 64 << 20:
+        # a caller usually still holds the previous trajectory while the next
+        # one is computed: leave one spare block of this size on the
+        # allocator's free list so the second call does not pin fresh memory
+        _WARMED.add(nbytes)
+        del_me = torch.empty(shape, dtype=dtype, pin_memory=True)
+        del del_me
     for k, sn in enumerate(snaps):
-        buf[k].copy_(sn, non_blocking=True)
+        buf[k + k0].copy_(sn, non_blocking=True)
+    out = buf.numpy()
+    if first is not None:
+        out[0] = first  # host copy while the device copies are in flight
     torch.cuda.current_stream().synchronize()
-    return buf.numpy()
+    return out
 
 
 class _ChunkTimer:
@@ -215,9 +224,7 @@ def integrate(model, dec, x0, plan: IntegrationPlan) -> Trajectory:
     if fast:  # records back in original order, gathered on the device
         import torch
 
-        recs = _to_host([torch.index_select(sn, 0, inv_dev) for sn in snaps]) if snaps else \
-            np.zeros((0, dec.n_nodes))
-        states = np.concatenate([x0[None], recs]) if n_steps else x0[None].copy()
+        states = _to_host([torch.index_select(sn, 0, inv_dev) for sn in snaps], first=x0)
     else:
         states_perm = _to_host(snaps)  # one pinned D2H of all records
         states = np.empty_like(states_perm)
