@@ -180,7 +180,7 @@ typedef struct cdk_graph {
    * shared memory with the window, so the row pipeline reads inter columns
    * from shared memory and issues the z gathers two rows ahead.  0 = off. */
   int32_t xs_cap;               /* multiple of 16 */
-  int32_t n_ell_parts;          /* ELL split rblocks: partial-sum slots (see ell_units) */
+  int32_t reserved0;            /* 0 */
   const int64_t *seg_xr;        /* [2*n_seg] inter_ptr at the segment's first/last row, or NULL */
   /* Lane-per-row sliced layout ("ELL"; cdk_host_ell_intra).  When ell_off is
    * set the stage kernels run one warp per rblock, lane = row: the rblock's
@@ -196,19 +196,13 @@ typedef struct cdk_graph {
   const int64_t *xell_off;      /* [n_rblk+1] int32 units */
   const int32_t *xell_col;
   /* ELL work units: warps of segment s claim units seg_unit[s] ..
-   * seg_unit[s+1]-1 in order; unit u = rblock ell_units[2u], part
-   * q = ell_units[2u+1] & 0xFFFF of P = ell_units[2u+1] >> 16 (chunks
-   * [q nch / P, (q+1) nch / P); inter entries in part 0).  Parts of a split
-   * rblock (P > 1) meet in partial-sum slots ell_part_base[b] + q of the
-   * workspace; the last to arrive adds them in part order and runs the
-   * epilogue.  P depends on the rblock only (deterministic on every shard). */
-  const int32_t *ell_units;     /* [2 * n_units] */
+   * seg_unit[s+1]-1 in order (longest first); unit u is rblock ell_units[u]. */
+  const int32_t *ell_units;     /* [n_units] */
   const int32_t *seg_unit;      /* [n_seg+1] */
-  const int32_t *ell_part_base; /* [n_rblk], -1 = not split */
   /* packed ELL unit metadata (or NULL): unit u = int32[8] at ell_meta + 8u:
    * {first chunk (uint4 units), xell start, first row, rblock; chunks, inter
-   * entries per lane (0 for parts > 0), rows, ci | part << 8 | nparts << 16}
-   * with ci the rblock's community minus the segment's first (255: pool) */
+   * entries per lane, rows, ci} with ci the rblock's community minus the
+   * segment's first (255: pool) */
   const int32_t *ell_meta;
 } cdk_graph;
 

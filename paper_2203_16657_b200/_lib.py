@@ -50,7 +50,7 @@ class CdkGraph(ctypes.Structure):
         ("inter_block_nodes", I32),
         ("inter_split", P),
         ("xs_cap", I32),
-        ("n_ell_parts", I32),
+        ("reserved0", I32),
         ("seg_xr", P),
         ("ell_off", P),
         ("ell_col", P),
@@ -58,7 +58,6 @@ class CdkGraph(ctypes.Structure):
         ("xell_col", P),
         ("ell_units", P),
         ("seg_unit", P),
-        ("ell_part_base", P),
         ("ell_meta", P),
     ]
 

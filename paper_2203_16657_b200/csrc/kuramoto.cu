@@ -46,8 +46,6 @@ struct Workspace {
   unsigned int *bar;  // grid-barrier counter of the persistent kernel
   double2 *xacc;      // per-row inter sums (block-phased inter sweep only)
   unsigned int *peer_bar;  // fused multi-GPU exchange: this rank's barrier counter
-  double2 *ell_part;  // ELL split rblocks: partial sums [n_ell_parts][32]
-  int *ell_cnt;       // ELL split rblocks: arrival counters [n_rblk] (zero between stages)
 };
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -72,9 +70,6 @@ static Workspace carve(const cdk_graph *g, void *base, size_t *total) {
   w.bar = (unsigned int *)take(256);
   w.xacc = g->inter_blocks > 0 ? (double2 *)take(n * sizeof(double2)) : nullptr;
   w.peer_bar = (unsigned int *)take(256);
-  w.ell_part = g->n_ell_parts > 0 ? (double2 *)take((size_t)g->n_ell_parts * 32 * sizeof(double2))
-                                  : nullptr;
-  w.ell_cnt = g->n_ell_parts > 0 ? (int *)take(((size_t)g->n_rblk + 1) * sizeof(int)) : nullptr;
   if (total) *total = off;
   return w;
 }
@@ -104,8 +99,6 @@ struct StageArgs {
   int64_t step_rel;
   unsigned long long *prof;  // CDK_PROFILE builds: per-CTA phase cycles
   unsigned long long *cta_cycles;  // ELL stage kernels: per-CTA cycles (planner calibration)
-  double2 *ell_part;  // Workspace::ell_part / ell_cnt
-  int *ell_cnt;
 };
 
 // Canonical community sum R_c of the rblock partials: 8 lanes, lane t sums
@@ -1195,17 +1188,14 @@ __device__ __forceinline__ UnitChunks unit_chunks(const cdk_graph &g, int u, int
     r.nch = m1.x;
     return r;
   }
-  const int rb = g.ell_units[2 * u], code = g.ell_units[2 * u + 1];
-  const int part = code & 0xFFFF, nparts = code >> 16;
-  const int nch_rb = (int)((g.ell_off[rb + 1] - g.ell_off[rb]) >> 5);
-  const int ch0 = nch_rb * part / nparts, ch1 = nch_rb * (part + 1) / nparts;
+  const int rb = g.ell_units[u];
   UnitChunks r;
-  r.cp = reinterpret_cast<const uint4 *>(g.ell_col) + g.ell_off[rb] + 32 * (int64_t)ch0 + lane;
-  r.nch = ch1 - ch0;
+  r.cp = reinterpret_cast<const uint4 *>(g.ell_col) + g.ell_off[rb] + lane;
+  r.nch = (int)((g.ell_off[rb + 1] - g.ell_off[rb]) >> 5);
   return r;
 }
 
-// One work unit (an rblock, or one part of a split rblock): lane = row.  The
+// One work unit (an rblock): lane = row.  The
 // unit's chunk stream runs through the warp's ring in shared memory
 // (cp.async, ELL_DEPTH chunks in flight per lane, one commit group per
 // chunk): no registers held by loads in flight, no register moves between
@@ -1213,9 +1203,7 @@ __device__ __forceinline__ UnitChunks unit_chunks(const cdk_graph &g, int u, int
 // that load), and the depth is free of register pressure.
 template <bool STAGED>
 __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, const StageVar &v,
-                                           int rb,
-                                           int part, int nparts,
-                                           uint32_t zs_addr, const double2 *zs, int64_t w0,
+                                           int rb, uint32_t zs_addr, const double2 *zs, int64_t w0,
                                            const double2 *__restrict__ zglob, double2 R,
                                            const UnitChunks &uc, uint32_t ring,
                                            const int4 *mt = nullptr) {
@@ -1232,13 +1220,12 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
     r0 = g.rblk_row0[rb];
     r1 = g.rblk_row0[rb + 1];
     x0 = g.xell_off[rb];
-    nx = (part == 0) ? (int)((g.xell_off[rb + 1] - x0) >> 5) : 0;
+    nx = (int)((g.xell_off[rb + 1] - x0) >> 5);
   }
   const int64_t i = r0 + lane;
   const bool valid = i < r1;
   DBG_CHECK(r1 <= g.n_rows && r1 - r0 <= 32, "rblock %d: rows [%lld, %lld) vs n_rows %lld", rb,
             (long long)r0, (long long)r1, (long long)g.n_rows);
-  // this unit's chunks (part of a split rblock) and inter entries (part 0)
   const int nch = uc.nch;
   // epilogue inputs: in flight during the gathers
   double om = 0.0, th0 = 0.0, ks0 = 0.0;
@@ -1340,27 +1327,6 @@ __device__ __forceinline__ void ell_rblock(const int MODE, const StageArgs &a, c
       sr += xz[q].x;
       si += xz[q].y;
     }
-  }
-  if (nparts > 1) {  // split rblock: publish the partial; the last part finishes
-    // every part of an rblock is a unit of the same segment, hence of this
-    // CTA: CTA-scope fence and atomic (no device-scope drain)
-    const int64_t base = (int64_t)g.ell_part_base[rb] * 32 + lane;
-    __stcg(a.ell_part + base + 32 * part, make_double2(sr, si));
-    __threadfence_block();
-    int old = 0;
-    if (lane == 0) old = atomicAdd_block(a.ell_cnt + rb, 1);
-    old = __shfl_sync(FULL, old, 0);
-    if (old != nparts - 1) return;
-    __threadfence_block();
-    const double2 own = make_double2(sr, si);
-    sr = 0.0;
-    si = 0.0;
-    for (int q = 0; q < nparts; ++q) {  // fixed part order
-      const double2 v = (q == part) ? own : ldcg2(a.ell_part + base + 32 * q);
-      sr += v.x;
-      si += v.y;
-    }
-    if (lane == 0) a.ell_cnt[rb] = 0;  // ready for the next stage
   }
   // epilogue (same arithmetic as stage_body's)
   double zr = 0.0, zim = 0.0;
@@ -1535,11 +1501,9 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
                             mb.x};
         const int4 mt[2] = {ma, mb};
         if (staged) {
-          ell_rblock<true>(MODE, a, v, ma.w, (mb.w >> 8) & 0xFF, (mb.w >> 16) & 0xFF, zs_addr,
-                           sm.zs, w0, zglob, R, uc, sm.ring, mt);
+          ell_rblock<true>(MODE, a, v, ma.w, zs_addr, sm.zs, w0, zglob, R, uc, sm.ring, mt);
         } else {
-          ell_rblock<false>(MODE, a, v, ma.w, (mb.w >> 8) & 0xFF, (mb.w >> 16) & 0xFF, zs_addr,
-                            sm.zs, w0, zglob, R, uc, sm.ring, mt);
+          ell_rblock<false>(MODE, a, v, ma.w, zs_addr, sm.zs, w0, zglob, R, uc, sm.ring, mt);
         }
         int nxt = 0;
         if (lane == 0) nxt = atomicAdd(sm.next, 1);
@@ -1561,16 +1525,13 @@ __device__ __forceinline__ void ell_body(const int MODE, const StageArgs &a, con
     }
     while (u < uB) {
       const UnitChunks uc = unit_chunks(g, u, lane);
-      const int rb = g.ell_units[2 * u];
-      const int code = g.ell_units[2 * u + 1];
+      const int rb = g.ell_units[u];
       const int c = g.rblk_comm[rb];
       const double2 R = (c >= 0) ? sm.sR[c - cA] : make_double2(0.0, 0.0);
       if (staged) {
-        ell_rblock<true>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob,
-                         R, uc, sm.ring);
+        ell_rblock<true>(MODE, a, v, rb, zs_addr, sm.zs, w0, zglob, R, uc, sm.ring);
       } else {
-        ell_rblock<false>(MODE, a, v, rb, code & 0xFFFF, code >> 16, zs_addr, sm.zs, w0, zglob,
-                          R, uc, sm.ring);
+        ell_rblock<false>(MODE, a, v, rb, zs_addr, sm.zs, w0, zglob, R, uc, sm.ring);
       }
       int nxt = 0;
       if (lane == 0) nxt = atomicAdd(sm.next, 1);
@@ -1762,7 +1723,7 @@ static int check_graph(const cdk_graph *g) {
   }
   if (g->ell_off) {
     if (g->cta_threads != ELL_THREADS || !g->xell_off || !g->ell_units || !g->seg_unit ||
-        !g->ell_part_base || g->n_ell_parts < 0 || g->inter_blocks != 0 || g->intra_split) {
+        g->inter_blocks != 0 || g->intra_split) {
       set_error("cdk_graph (ELL): cta_threads must equal cdk_kuramoto_ell_threads(), xell_off "
                 "set, no inter_blocks / intra_split");
       return CDK_INPUT;
@@ -1853,10 +1814,6 @@ static int prepare(const cdk_graph *g, const double *theta, const Workspace &w, 
   }
   reset_status_kernel<<<1, 1, 0, st>>>(w.status);
   CDK_CHECK_LAUNCH("reset_status_kernel");
-  if (w.ell_cnt) {  // split-rblock arrival counters start at zero (finishers reset them)
-    cudaError_t e = cudaMemsetAsync(w.ell_cnt, 0, ((size_t)g->n_rblk + 1) * sizeof(int), st);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(ell counters)");
-  }
   return CDK_OK;
 }
 
@@ -1872,8 +1829,6 @@ static StageArgs base_args(const cdk_graph *g, const Workspace &w, double *theta
   a.omega = omega;
   a.ksum = w.ksum;
   a.xacc = w.xacc;
-  a.ell_part = w.ell_part;
-  a.ell_cnt = w.ell_cnt;
   a.peer_out = nullptr;
   a.n_peers = 1;
   a.rank = 0;

@@ -515,10 +515,8 @@ class EllLayout:
     ell_col: np.ndarray  # uint16[8 * ell_off[-1]]
     xell_off: np.ndarray  # int64[n_rblk+1], int32 units
     xell_col: np.ndarray  # int32[xell_off[-1]], -1 = none
-    ell_units: np.ndarray | None = None  # int32[2*n_units]: rblock, part | parts << 16
+    ell_units: np.ndarray | None = None  # int32[n_units]: rblock of each unit, claim order
     seg_unit: np.ndarray | None = None  # int32[n_seg+1]
-    ell_part_base: np.ndarray | None = None  # int32[n_rblk], -1 = not split
-    n_parts: int = 0  # partial-sum slots of split rblocks
     ell_meta: np.ndarray | None = None  # int32[8*n_units] packed unit metadata (or None)
 
     def slots(self) -> int:
@@ -604,10 +602,9 @@ def build_ell(lay: HostLayout, sch: Schedule) -> EllLayout:
         if np.any((r < rows[0]) | (r >= rows[-1])):
             raise InputError("inter entries outside the rblocks")
         xell_col[xell_off[b] + 32 * k + (r - rows[b])] = lay.inter_col
-    units, seg_unit, part_base, n_parts = _ell_units(ell_off, xell_off, sch)
+    units, seg_unit = _ell_units(ell_off, xell_off, sch)
     meta = _ell_meta(lay, sch, ell_off, xell_off, units, seg_unit)
-    return EllLayout(ell_off, ell_col, xell_off, xell_col, units, seg_unit, part_base, n_parts,
-                     meta)
+    return EllLayout(ell_off, ell_col, xell_off, xell_col, units, seg_unit, meta)
 
 
 def _ell_meta(lay: HostLayout, sch: Schedule, ell_off, xell_off, units, seg_unit):
@@ -617,67 +614,45 @@ def _ell_meta(lay: HostLayout, sch: Schedule, ell_off, xell_off, units, seg_unit
     int32"""
     if ell_off[-1] >= 2**31 or xell_off[-1] >= 2**31 or lay.n_rows >= 2**31:
         return None
-    u = units.reshape(-1, 2).astype(np.int64)
-    nu = u.shape[0]
+    rb = units.astype(np.int64)
+    nu = rb.shape[0]
     meta = np.zeros((nu, 8), dtype=np.int64)
     if nu == 0:
         return meta.astype(np.int32).reshape(-1)
-    rb, q, P = u[:, 0], u[:, 1] & 0xFFFF, u[:, 1] >> 16
     rows = lay.rblk_row0
-    nch_rb = (ell_off[rb + 1] - ell_off[rb]) // 32
-    ch0, ch1 = nch_rb * q // P, nch_rb * (q + 1) // P
     seg = np.repeat(np.arange(sch.n_seg), np.diff(seg_unit))
     c = lay.rblk_comm[rb].astype(np.int64)
     cA = lay.rblk_comm[sch.seg_rblk[seg]].astype(np.int64)
     ci = np.where(c >= 0, c - cA, 255)
-    if np.any((ci < 0) | ((ci >= SEG_MAX_COMM) & (ci != 255))) or np.any(P > 255):
+    if np.any((ci < 0) | ((ci >= SEG_MAX_COMM) & (ci != 255))):
         return None
-    meta[:, 0] = ell_off[rb] + 32 * ch0
+    meta[:, 0] = ell_off[rb]
     meta[:, 1] = xell_off[rb]
     meta[:, 2] = rows[rb]
     meta[:, 3] = rb
-    meta[:, 4] = ch1 - ch0
-    meta[:, 5] = np.where(q == 0, (xell_off[rb + 1] - xell_off[rb]) // 32, 0)
+    meta[:, 4] = (ell_off[rb + 1] - ell_off[rb]) // 32
+    meta[:, 5] = (xell_off[rb + 1] - xell_off[rb]) // 32
     meta[:, 6] = rows[rb + 1] - rows[rb]
-    meta[:, 7] = ci | (q << 8) | (P << 16)
+    meta[:, 7] = ci
     return meta.astype(np.int32).reshape(-1)
 
 
-# chunks per work unit of split rblocks; 0 = no splitting (the default: the
-# split parts meet through a device-scope fence that stalls on the warp's
-# in-flight chunk loads, measured slower on config 2)
-ELL_UNIT_CH = settings().ell_unit_ch
-
-
 def _ell_units(ell_off, xell_off, sch: Schedule):
-    """Work units of the ELL kernels: rblocks of more than 2 ELL_UNIT_CH chunks
-    are split into P = nch // ELL_UNIT_CH parts (a function of the rblock
-    alone); each segment's units are listed longest first (the warps' claim
-    order), ties by (rblock, part)."""
+    """Work units of the ELL kernels: one per rblock; each segment's units are
+    listed longest first (the warps' claim order), ties by rblock.  (Splitting
+    long rblocks into parts that meet through a counter was measured slower on
+    config 2 at every part size and removed.)"""
     nch = np.diff(ell_off) // 32
-    nparts = (np.maximum(1, nch // ELL_UNIT_CH) if ELL_UNIT_CH > 0
-              else np.ones_like(nch)).astype(np.int64)
-    split = nparts > 1
-    part_base = np.full(nch.shape[0], -1, dtype=np.int64)
-    cum = np.cumsum(np.where(split, nparts, 0))
-    part_base[split] = (cum - nparts)[split]
-    n_parts = int(cum[-1]) if cum.size else 0
     nx = np.diff(xell_off) // 32
     units, seg_unit = [], [0]
     for si in range(sch.n_seg):
         a, z = int(sch.seg_rblk[si]), int(sch.seg_rblk[si + 1])
-        rb = np.repeat(np.arange(a, z), nparts[a:z])
-        q = np.arange(rb.shape[0]) - np.repeat(np.cumsum(nparts[a:z]) - nparts[a:z], nparts[a:z])
-        P = nparts[rb]
-        work = (nch[rb] * (q + 1) // P - nch[rb] * q // P) * 8 + np.where(q == 0, nx[rb], 0)
-        order = np.lexsort((q, rb, -work))
-        u = np.empty((rb.shape[0], 2), dtype=np.int64)
-        u[:, 0], u[:, 1] = rb[order], q[order] | (P[order] << 16)
-        units.append(u)
+        rb = np.arange(a, z)
+        work = nch[rb] * 8 + nx[rb]
+        units.append(rb[np.lexsort((rb, -work))])
         seg_unit.append(seg_unit[-1] + rb.shape[0])
-    units = (np.concatenate(units) if units else np.zeros((0, 2), np.int64)).astype(np.int32)
-    return (units.reshape(-1), np.asarray(seg_unit, dtype=np.int32), part_base.astype(np.int32),
-            n_parts)
+    units = (np.concatenate(units) if units else np.zeros(0, np.int64)).astype(np.int32)
+    return units, np.asarray(seg_unit, dtype=np.int32)
 
 
 SEG_INTER_PHASE = 256  # include/commdyn_cuda.h CDK_SEG_INTER_PHASE
@@ -911,8 +886,6 @@ class DeviceGraph:
             self._t["xell_col"] = up(e.xell_col if e.xell_col.size else np.full(4, -1, np.int32))
             self._t["ell_units"] = up(e.ell_units if e.ell_units.size else np.zeros(2, np.int32))
             self._t["seg_unit"] = up(e.seg_unit)
-            self._t["ell_part_base"] = up(e.ell_part_base if e.ell_part_base.size
-                                          else np.full(1, -1, np.int32))
             if e.ell_meta is not None and settings().ell_meta:
                 self._t["ell_meta"] = up(e.ell_meta if e.ell_meta.size else np.zeros(8, np.int32))
         _attach_inter_split(self, lay.n_rows)
@@ -931,7 +904,7 @@ class DeviceGraph:
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
             inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
             inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
-            xs_cap=sch.xs_cap, n_ell_parts=sch.ell.n_parts if sch.ell is not None else 0,
+            xs_cap=sch.xs_cap,
             seg_xr=t["seg_xr"].data_ptr(),
             ell_off=t["ell_off"].data_ptr() if "ell_off" in t else None,
             ell_col=t["ell_col"].data_ptr() if "ell_off" in t else None,
@@ -939,7 +912,6 @@ class DeviceGraph:
             xell_col=t["xell_col"].data_ptr() if "ell_off" in t else None,
             ell_units=t["ell_units"].data_ptr() if "ell_off" in t else None,
             seg_unit=t["seg_unit"].data_ptr() if "ell_off" in t else None,
-            ell_part_base=t["ell_part_base"].data_ptr() if "ell_off" in t else None,
             ell_meta=t["ell_meta"].data_ptr() if "ell_meta" in t else None,
         )
 
@@ -1015,7 +987,7 @@ class DeviceGraph:
             intra_split=t["intra_split"].data_ptr() if "intra_split" in t else None,
             inter_blocks=self.inter_blocks, inter_block_nodes=self.inter_block_nodes,
             inter_split=t["inter_split"].data_ptr() if "inter_split" in t else None,
-            xs_cap=sch.xs_cap, n_ell_parts=sch.ell.n_parts if sch.ell is not None else 0,
+            xs_cap=sch.xs_cap,
             seg_xr=t["seg_xr"].data_ptr(),
         )
         return self

@@ -14,7 +14,6 @@ CDK_ELL                ell                     lane-per-row ELL kernels (0: row-
 CDK_ELL_CALIBRATE      ell_calibrate           measured CTA re-cuts at construction (0: off)
 CDK_ELL_WINDOW         ell_window              cap on the ELL window (nodes; 0: library's)
 CDK_ELL_META           ell_meta                packed per-unit metadata records
-CDK_ELL_UNIT           ell_unit_ch             chunks per split-rblock unit (0: no split)
 CDK_ELL_SLOT_COST ...  ell_slot_cost, ...      ELL cost model (cycles per slot / rblock / segment)
 CDK_ROWS_CAP           rows_cap                rows per segment of the row-group kernels
 CDK_SMEM_BUDGET        smem_budget             row-group kernels' shared-memory budget (bytes)
@@ -59,7 +58,6 @@ class Settings:
     ell_calibrate: int = 4
     ell_window: int = 0
     ell_meta: bool = True
-    ell_unit_ch: int = 0
     ell_slot_cost: float = 0.144
     ell_xslot_cost: float = 0.39
     ell_rblk_cost: float = 100.0
@@ -81,7 +79,6 @@ def settings() -> Settings:
         ell_calibrate=_int("CDK_ELL_CALIBRATE", d.ell_calibrate),
         ell_window=_int("CDK_ELL_WINDOW", d.ell_window),
         ell_meta=_flag("CDK_ELL_META", d.ell_meta),
-        ell_unit_ch=_int("CDK_ELL_UNIT", d.ell_unit_ch),
         ell_slot_cost=_float("CDK_ELL_SLOT_COST", d.ell_slot_cost),
         ell_xslot_cost=_float("CDK_ELL_XSLOT_COST", d.ell_xslot_cost),
         ell_rblk_cost=_float("CDK_ELL_RBLK_COST", d.ell_rblk_cost),

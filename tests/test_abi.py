@@ -36,8 +36,8 @@ def test_library_host_only_calls():
 
 
 def test_struct_layout_matches_header():
-    # 2 int64 + 5 pointers + 6 int32 + 9 pointers + ... + 4 ELL pointers
+    # 2 int64 + 5 pointers + 6 int32 + 9 pointers + ... + 7 ELL pointers
     assert ctypes.sizeof(_lib.CdkGraph) == (8 * 2 + 8 * 5 + 4 * 6 + 8 * 9 + 4 * 2 + 8 + 4 * 2 + 8
-                                            + 8 * 8)
+                                            + 8 * 7)
     assert _lib.CdkGraph.ell_off.offset == 184
     assert ctypes.sizeof(_lib.CdkRunStatus) == 32

@@ -22,10 +22,6 @@ def _ell_schedule(dec, sm_count=148, window=None, monkeypatch=None):
     return lay, sch
 
 
-def _parts(nch):
-    return max(1, int(nch) // PL.ELL_UNIT_CH) if PL.ELL_UNIT_CH > 0 else 1
-
-
 def _check(lay, sch):
     e = sch.ell
     assert e is not None
@@ -68,36 +64,25 @@ def _check(lay, sch):
             assert np.array_equal(got[got >= 0], np.asarray(want, np.int32))
             assert np.all(got[len(want):] == -1)
     assert slots == e.slots()
-    # work units: every (rblock, part) of a segment exactly once, parts a
-    # function of the rblock's chunk count, part slots disjoint
+    # work units: every rblock of a segment exactly once, longest first
     nch = np.diff(e.ell_off) // 32
-    units = e.ell_units.reshape(-1, 2)
+    nxs = np.diff(e.xell_off) // 32
+    units = e.ell_units
     for si in range(sch.n_seg):
         a, z = int(sch.seg_rblk[si]), int(sch.seg_rblk[si + 1])
         u = units[e.seg_unit[si]:e.seg_unit[si + 1]]
-        P = u[:, 1] >> 16
-        got = sorted(zip(u[:, 0].tolist(), (u[:, 1] & 0xFFFF).tolist()))
-        want = [(b, q) for b in range(a, z) for q in range(_parts(nch[b]))]
-        assert got == want
-        assert np.all(P == np.array([_parts(x) for x in nch[u[:, 0]]], dtype=P.dtype))
+        assert sorted(u.tolist()) == list(range(a, z))
+        work = nch[u] * 8 + nxs[u]
+        assert np.all(np.diff(work) <= 0)
     if e.ell_meta is not None:  # packed unit metadata agrees with the arrays
         m = e.ell_meta.reshape(-1, 8)
         assert m.shape[0] == units.shape[0]
         for k in range(m.shape[0]):
-            b, code = int(units[k, 0]), int(units[k, 1])
-            q, P = code & 0xFFFF, code >> 16
-            nb = int(nch[b])
+            b = int(units[k])
             assert m[k, 3] == b and m[k, 2] == rows[b] and m[k, 6] == rows[b + 1] - rows[b]
-            assert m[k, 0] == e.ell_off[b] + 32 * (nb * q // P)
-            assert m[k, 4] == nb * (q + 1) // P - nb * q // P
-            assert m[k, 5] == ((e.xell_off[b + 1] - e.xell_off[b]) // 32 if q == 0 else 0)
-            assert (m[k, 7] >> 8) & 0xFF == q and (m[k, 7] >> 16) & 0xFF == P
-    split = np.nonzero(e.ell_part_base >= 0)[0]
-    P = np.array([_parts(x) for x in nch], dtype=np.int64)
-    assert np.all(P[e.ell_part_base < 0] == 1)
-    ranges = sorted((int(e.ell_part_base[b]), int(P[b])) for b in split)
-    assert all(x[0] + x[1] <= y[0] for x, y in zip(ranges, ranges[1:]))
-    assert e.n_parts == sum(int(P[b]) for b in split)
+            assert m[k, 0] == e.ell_off[b]
+            assert m[k, 4] == nch[b]
+            assert m[k, 5] == nxs[b]
 
 
 def test_ell_layout_config1():
@@ -108,12 +93,7 @@ def test_ell_layout_config1():
     assert lay.nnz_intra <= sch.ell.slots() <= 2 * lay.nnz_intra + 256 * lay.n_rblk
 
 
-def _units_on(monkeypatch):
-    monkeypatch.setattr(PL, "ELL_UNIT_CH", 8)
-
-
 def test_ell_layout_edge_cases(monkeypatch):
-    _units_on(monkeypatch)
     """NONE pool, tiny communities, a community wider than the window
     (unstaged: global gathers, pads skipped), empty S."""
     rng = np.random.default_rng(3)
