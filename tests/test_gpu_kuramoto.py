@@ -98,6 +98,32 @@ def test_public_integrate_api(cfg1, golden_dir):
     assert tr.kernel_launches >= 1  # persistent RK4 kernel: one launch per recorded chunk
 
 
+def test_trajectories_do_not_alias(cfg1):
+    """integrate() hands its pinned readback buffer to the caller: a later
+    call (same shapes, other data) must leave an earlier trajectory intact,
+    a chunk whose last step keeps dt is one launch, and a short last step
+    still lands on t_end."""
+    from paper_2203_16657_b200 import IntegrationPlan, integrate, kuramoto_model
+
+    c, dec, omega, theta0 = cfg1
+    model = kuramoto_model(omega, c.coupling, c.n)
+    plan = IntegrationPlan(t_end=30 * c.dt, dt=c.dt, record_every=10)
+    tr1 = integrate(model, dec, theta0, plan)
+    keep = tr1.states.copy()
+    assert np.array_equal(tr1.states[0], theta0) and tr1.states.shape == (4, c.n)
+    tr2 = integrate(model, dec, theta0 + 0.25, plan)
+    tr3 = integrate(model, dec, theta0 - 0.25, plan)
+    assert np.array_equal(tr1.states, keep)
+    assert not np.array_equal(tr2.states[-1], tr1.states[-1])
+    assert not np.array_equal(tr3.states[-1], tr2.states[-1])
+    # T not a multiple of dt: the last step is shorter and has its own launch
+    tr4 = integrate(model, dec, theta0, IntegrationPlan(t_end=29.5 * c.dt, dt=c.dt))
+    assert tr4.times[-1] == pytest.approx(29.5 * c.dt) and tr4.meta["n_steps"] == 30
+    ref, _ = cia.rk4_integrate(_oracle_rhs(dec, omega, c.coupling, c.n), theta0, c.dt, 29)
+    ref, _ = cia.rk4_integrate(_oracle_rhs(dec, omega, c.coupling, c.n), ref, 0.5 * c.dt, 1)
+    assert cia.circ_dist(tr4.final, ref).max() <= TRAJ_TOL
+
+
 def _random_case(seed, sizes, p_in, p_out, pool=0):
     rng = np.random.default_rng(seed)
     g, part = G.planted_partition_graph(sizes, p_in, p_out, seed)
