@@ -444,6 +444,113 @@ def run_ours(args):
     return 0
 
 
+FP64_PEAK_TFLOPS = 36.4  # DFMA, measured on this pool (tools/fp64_peak.cu, profiles/r02_fp64_peak.txt)
+CFG4_FLOP_PER_STEP = 2.5e9  # ncu SASS counts of the four stages (profiles/r02_experiments.txt)
+
+
+def run_cfg34(args):
+    """Secondary bench lines: config 3 (higher-order Kuramoto, triangles) and
+    config 4 (Cucker-Smale, degree-8 P2).  Same contract as the config-2 line:
+    W warm-up steps, K RK4 steps timed one by one with CUDA events and the L2
+    flushed before each, e2e through the public integrate() with host arrays.
+    Canonical bytes per RHS: cfg3 = 4 nnz_dir + 8 triangle incidences + 8 (N+1)
+    + 24 N; cfg4 = 4 nnz_dir + 8 (N+1) + 64 N (state in, derivative out)."""
+    import torch
+
+    from paper_2203_16657_b200 import IntegrationPlan, _lib, configs, cs, ho, integrate
+
+    torch.cuda.set_device(0)
+    lib = _lib.lib()
+    K = args.steps if args.steps != 2000 else 200
+    W = max(3, args.warmup)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        flush.fill_(float(np.random.random()))
+
+    t0 = time.perf_counter()
+    if args.config == "cfg3":
+        c = configs.config3()
+        dec = c.decomposition()
+        omega, x0 = c.state()
+        eng = ho.HOEngine(dec, omega, c.k1, c.k2, norm=c.n)
+        eng.set_state(x0)
+        model = ho.ho_kuramoto_model(omega, c.k1, c.k2, norm=c.n)
+        b_rhs = 4 * dec.nnz_dir + 8 * int(eng.graph.tri_pairs) + 8 * (c.n + 1) + 24 * c.n
+        workload = ("cfg3 higher-order Kuramoto CIA RK4, SBM N=50000, 100 communities of 500, "
+                    "p_in .9, p_out 1e-4, K1=1, K2=.5, dt .005")
+        h2d = 2 * 8 * c.n
+    else:
+        c = configs.config4()
+        dec = c.decomposition()
+        pos, vel = c.state()
+        model = cs.CuckerSmale(c.K, c.sigma, c.beta)
+        eng = cs.CSEngine(dec, model, pos, vel, t_end=c.t_end)
+        x0 = np.concatenate([pos, vel], axis=1)
+        b_rhs = 4 * dec.nnz_dir + 8 * (c.n + 1) + 64 * c.n
+        workload = ("cfg4 Cucker-Smale CIA RK4 (degree-8 P2 in squared distance), SBM N=100000, "
+                    "100 communities of 1000, p_in .9, p_out 1e-4, dt .01")
+        h2d = 4 * 8 * c.n
+    t_setup = time.perf_counter() - t0
+    sampler = ClockSampler(0)
+    with sampler:
+        eng.rk4(c.dt, W)
+        torch.cuda.synchronize()
+        l0 = int(lib.cdk_launch_count())
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        for k in range(K):
+            flush_l2()
+            starts[k].record()
+            eng.rk4(c.dt, 1)
+            ends[k].record()
+        torch.cuda.synchronize()
+        launches = int(lib.cdk_launch_count()) - l0
+        eng.check()
+        step_ms = np.array([a.elapsed_time(b) for a, b in zip(starts, ends)])
+        e2e_times = []
+        for rep in range(3):  # the first call builds the engine; min over the warm ones
+            flush_l2()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            tr = integrate(model, dec, x0, IntegrationPlan(t_end=K * c.dt, dt=c.dt))
+            final = tr.final
+            torch.cuda.synchronize()
+            e2e_times.append(time.perf_counter() - t)
+    clocks = sampler.summary()
+    if not np.all(np.isfinite(final)):
+        raise RuntimeError("non-finite final state")
+    ms = float(step_ms.mean())
+    peak, peak_kind = _peaks()
+    achieved = 4 * b_rhs / (ms / 1e3) / 1e9
+    res = {
+        "metric": METRIC, "value": c.n / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": K,
+        "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "n_nodes": c.n, "nnz_dir": int(dec.nnz_dir), "dt": c.dt,
+                   "l2": "L2 flushed (512 MB write) before every timed step"},
+        "setup": {"setup_s": round(t_setup, 2), "parallelism": "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "one RK4 step (4 stages of %s kernels)" %
+                               ("ho_*" if args.config == "cfg3" else "cs_*"),
+                     "algorithmic_bytes_per_rhs": int(b_rhs), "launch_ms_mean": ms,
+                     "note": "achieved = 4 B_rhs / mean timed step; per-kernel ncu metrics in "
+                             "profiles/r02_cfg34_final_ncu_launch_metrics.txt"},
+        "e2e": {"value": c.n * K / min(e2e_times), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d / K), "d2h_bytes_per_step": int(h2d / K),
+                "note": "integrate() via the public API with host arrays"},
+        "gpu_launches": launches, "clocks": clocks, "cpu_baseline": None,
+    }
+    if args.config == "cfg4":
+        tf = CFG4_FLOP_PER_STEP / (ms / 1e3) / 1e12
+        res["fp64"] = {"achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                       "frac": tf / FP64_PEAK_TFLOPS,
+                       "note": "flop per step from ncu SASS counts; peak = measured DFMA rate"}
+    print(json.dumps(res), flush=True)
+    return 0
+
+
 def l1_pipe_floor(dg, n, launch_ms, clocks):
     """The bound that binds the ELL kernel: the SM's L1/shared
     data pipe moves one 128-byte wavefront per cycle, and every gather costs
@@ -643,12 +750,20 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg5"],
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg2 = the metric's config (default); cfg5 = the LFR-style N=8e6 "
-                         "config (steps default 200)")
+                         "config (steps default 200); cfg3 / cfg4 = higher-order Kuramoto / "
+                         "Cucker-Smale (secondary lines, steps default 200)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args.gpus)
+    if args.config in ("cfg3", "cfg4"):
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "the reference ships no CIA "
+                              "arithmetic for this model (its oracle here is a restatement of "
+                              "the SPEC: tests/test_ho_oracle.py, tests/test_cs_oracle.py)"}))
+            return 0
+        return run_cfg34(args)
     if args.config == "cfg5":
         if args.impl != "reference" and (int(os.environ.get("WORLD_SIZE", "1")) > 1
                                          or os.environ.get("CDK_BENCH_SHARDED") == "1"):
