@@ -63,16 +63,21 @@ __device__ __forceinline__ double eta_exact(double d2, double K, double sigma2, 
 
 // moments of node chunk q of community c: CTA (c, q) sums nodes
 // [b + q * CS_MOM_NODES, ...) in node order.  Thread t owns the outputs
-// (f, i, j0..j0+3) (a "quad" of consecutive y powers): per node it forms
-// x^i f once and adds it times four y powers — 1.5 shared loads and 1.25
-// fp64 ops per output instead of 3 and 2, four independent chains.  The
-// contraction adds the chunks' partials in q order.
-constexpr int CS_MOM_NODES = 256;
-constexpr int CS_NQUAD = 135;  // sum_i ceil((17 - i) / 4) x 3 functions
-__constant__ unsigned char c_quad_f[CS_NQUAD];
+// (f = 0..2, i, j0..j0+3): a "quad" of consecutive y powers for all three
+// functions.  Per node it reads x^i, four y powers and the three f values (8
+// shared loads) for 12 FMAs + 3 multiplies; one thread per (f, i, quad) read 6
+// for 5, and the kernel sat at 89 % of the L1/shared pipe.  Twelve
+// independent chains per thread.  The contraction adds the chunks' partials
+// in q order.
+#ifndef CDK_CS_MOM_NODES
+#define CDK_CS_MOM_NODES 256
+#endif
+constexpr int CS_MOM_NODES = CDK_CS_MOM_NODES;
+constexpr int CS_NQUAD = 45;  // sum_i ceil((17 - i) / 4)
+constexpr int CS_MOM_THREADS = 64;
 __constant__ unsigned char c_quad_i[CS_NQUAD];
 __constant__ unsigned char c_quad_j[CS_NQUAD];
-__global__ void __launch_bounds__(160) cs_moments_kernel(const CsArgs a) {
+__global__ void __launch_bounds__(CS_MOM_THREADS) cs_moments_kernel(const CsArgs a) {
   __shared__ double px[128][CS_D2 + 1];
   __shared__ double py[128][CS_D2 + 4];  // 3 zero pads: a quad may run past j = 16 - i
   __shared__ double pf[128][3];
@@ -84,8 +89,12 @@ __global__ void __launch_bounds__(160) cs_moments_kernel(const CsArgs a) {
   const double il = a.inv_L[c];
   const int t = threadIdx.x;
   const bool act = t < CS_NQUAD;
-  const int f = act ? c_quad_f[t] : 0, i = act ? c_quad_i[t] : 0, j0 = act ? c_quad_j[t] : 0;
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  const int i = act ? c_quad_i[t] : 0, j0 = act ? c_quad_j[t] : 0;
+  double acc[3][4];
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[f][k] = 0.0;
   for (int64_t base = b; base < e; base += 128) {
     const int cnt = (int)min((int64_t)128, e - base);
     __syncthreads();
@@ -108,21 +117,29 @@ __global__ void __launch_bounds__(160) cs_moments_kernel(const CsArgs a) {
     __syncthreads();
     if (act) {
       for (int n = 0; n < cnt; ++n) {
-        const double xf = px[n][i] * pf[n][f];
-        acc0 += xf * py[n][j0];
-        acc1 += xf * py[n][j0 + 1];
-        acc2 += xf * py[n][j0 + 2];
-        acc3 += xf * py[n][j0 + 3];
+        const double xi = px[n][i];
+        const double y0 = py[n][j0], y1 = py[n][j0 + 1], y2 = py[n][j0 + 2], y3 = py[n][j0 + 3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const double xf = xi * pf[n][f];
+          acc[f][0] += xf * y0;
+          acc[f][1] += xf * y1;
+          acc[f][2] += xf * y2;
+          acc[f][3] += xf * y3;
+        }
       }
     }
   }
   if (act) {
-    double *Mq = a.M + ((int64_t)c * a.mom_split + q) * CS_NOUT + f * CS_NMON + c_mono_row[i];
     const int nj = CS_D2 - i + 1;  // valid j of this i: 0..16-i
-    Mq[j0] = acc0;
-    if (j0 + 1 < nj) Mq[j0 + 1] = acc1;
-    if (j0 + 2 < nj) Mq[j0 + 2] = acc2;
-    if (j0 + 3 < nj) Mq[j0 + 3] = acc3;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      double *Mq = a.M + ((int64_t)c * a.mom_split + q) * CS_NOUT + f * CS_NMON + c_mono_row[i];
+      Mq[j0] = acc[f][0];
+      if (j0 + 1 < nj) Mq[j0 + 1] = acc[f][1];
+      if (j0 + 2 < nj) Mq[j0 + 2] = acc[f][2];
+      if (j0 + 3 < nj) Mq[j0 + 3] = acc[f][3];
+    }
   }
 }
 
@@ -483,21 +500,21 @@ static int cs_tables() {
     }
   }
   row[CS_D2 + 1] = (short)k;
-  unsigned char qf[CS_NQUAD], qi[CS_NQUAD], qj[CS_NQUAD];
+  unsigned char qi[CS_NQUAD], qj[CS_NQUAD];
   int nq = 0;
-  for (int f = 0; f < 3; ++f)
-    for (int i = 0; i <= CS_D2; ++i)
-      for (int j = 0; j <= CS_D2 - i; j += 4, ++nq) {
-        qf[nq] = (unsigned char)f;
+  for (int i = 0; i <= CS_D2; ++i)
+    for (int j = 0; j <= CS_D2 - i; j += 4) {
+      if (nq < CS_NQUAD) {
         qi[nq] = (unsigned char)i;
         qj[nq] = (unsigned char)j;
       }
+      ++nq;
+    }
   if (nq != CS_NQUAD) {
     set_error("cs quad table size");
     return CDK_INPUT;
   }
   cudaError_t e = cudaMemcpyToSymbol(c_mono_i, mi, sizeof(mi));
-  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_quad_f, qf, sizeof(qf));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_quad_i, qi, sizeof(qi));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_quad_j, qj, sizeof(qj));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mono_j, mj, sizeof(mj));
@@ -558,7 +575,7 @@ static int cs_stage(CsArgs a, cudaStream_t st) {
   AuxFork *fk = a.n_comm > 0 ? aux_fork(st) : nullptr;
   cudaStream_t sc = fk ? fk->aux : st;  // stream of the community part
   if (a.n_comm > 0) {
-    cs_moments_kernel<<<dim3(a.n_comm, a.mom_split), 160, 0, sc>>>(a);
+    cs_moments_kernel<<<dim3(a.n_comm, a.mom_split), CS_MOM_THREADS, 0, sc>>>(a);
     CDK_CHECK_LAUNCH("cs_moments_kernel");
     cs_contract_kernel<<<a.n_comm, 512, 0, sc>>>(a);
     CDK_CHECK_LAUNCH("cs_contract_kernel");
