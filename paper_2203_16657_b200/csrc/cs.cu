@@ -249,17 +249,33 @@ __global__ void __launch_bounds__(256, 4) cs_sparse_kernel(const CsArgs a) {
 // cs_sparse_kernel.
 constexpr int CS_WIN_RB = 4;      // rblocks (<= 128 rows) per CTA, CS_LPR lanes per row
 constexpr int CS_WIN_CAP = 3072;  // nodes: 96 KB of shared memory
+__device__ __forceinline__ int ld_col(const int32_t *p) {
+  int v;
+  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void cs_sparse_sum_win(const CsArgs &a, const int32_t *__restrict__ col,
                                                   int64_t p0, int64_t p1, double2 sm, double2 vm,
                                                   const double2 *__restrict__ sS,
                                                   const double2 *__restrict__ sV, int cb,
                                                   double &ax, double &ay) {
+  // the next batch's columns load while this batch's gathers and eta run: the
+  // column load's L2 latency was the kernel's top stall (24 % of the warp
+  // samples on its first use).  Volatile asm keeps the loads where they are
+  // written (the compiler sinks a plain __ldg back to its use).
+  int jn[CS_BATCH];
+#pragma unroll
+  for (int b = 0; b < CS_BATCH; ++b) {
+    const int64_t q = p0 + (int64_t)b * CS_LPR;
+    jn[b] = q < p1 ? ld_col(col + q) : -1;
+  }
   for (int64_t p = p0; p < p1; p += CS_BATCH * CS_LPR) {
     int jb[CS_BATCH];
 #pragma unroll
     for (int b = 0; b < CS_BATCH; ++b) {
-      const int64_t q = p + (int64_t)b * CS_LPR;
-      jb[b] = q < p1 ? __ldg(col + q) : -1;
+      jb[b] = jn[b];
+      const int64_t q = p + (int64_t)(CS_BATCH + b) * CS_LPR;
+      jn[b] = q < p1 ? ld_col(col + q) : -1;
     }
     double2 sj[CS_BATCH], vj[CS_BATCH];
 #pragma unroll
