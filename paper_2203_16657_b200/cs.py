@@ -33,6 +33,7 @@ import numpy as np
 from . import _lib
 from .errors import BlowUpError, DomainViolationError, InputError
 from .graph import Decomposition
+from .settings import settings
 from .plan import build_layout
 
 DEG = 8
@@ -159,6 +160,32 @@ def _csr(rows, cols, n):
     return ptr, cols.astype(np.int32)
 
 
+def _csr_bank_spread(rows, cols, n, base_of_row, parity_of_row):
+    """CSR of the missing intra edges with every row's entries ordered for the
+    shared-memory window of cs_sparse_win_kernel: a quarter-warp is two
+    consecutive rows x 4 lanes reading 4 consecutive entries each, 16 bytes
+    per lane, so its 8 loads are conflict-free iff their window indices differ
+    mod 8.  The even row of a pair lists its entries of bank groups 0-3 first
+    and 4-7 second, the odd row the other way round, and inside a half the
+    entries go round-robin over the half's four groups.  (Random order costs
+    ~2.3 wavefronts per ideal one.)  Any fixed order is a valid summation
+    order; both sparse kernels read the same one."""
+    j = cols - base_of_row[rows]
+    g = j & 7
+    first = np.lexsort((cols, g, rows))
+    r_s, g_s = rows[first], g[first]
+    key = r_s * 8 + g_s
+    start = np.r_[True, key[1:] != key[:-1]]
+    idx = np.arange(key.shape[0])
+    rank = idx - np.maximum.accumulate(np.where(start, idx, 0))
+    half = (g_s >> 2) ^ parity_of_row[r_s]
+    order = np.lexsort((g_s & 3, rank, half, r_s))
+    rows_o, cols_o = r_s[order], cols[first][order]
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows_o, minlength=n), out=ptr[1:])
+    return ptr, cols_o.astype(np.int32)
+
+
 class CsDeviceGraph:
     def __init__(self, dec: Decomposition, plan: CsPlan, device=None):
         import torch
@@ -167,7 +194,15 @@ class CsDeviceGraph:
         n = dec.n_nodes
         lay = build_layout(dec)
         rows, cols, sg = dec.directed()
-        mptr, mcol = _csr(rows[sg < 0], cols[sg < 0], n)
+        if settings().cs_bank_spread:
+            comm = dec.partition.comm_of_permuted()
+            base = np.where(comm >= 0, dec.offsets[np.maximum(comm, 0)], 0).astype(np.int64)
+            rb_of_row = np.searchsorted(lay.rblk_row0, np.arange(n), side="right") - 1
+            parity = ((np.arange(n) - lay.rblk_row0[np.minimum(rb_of_row, lay.n_rblk - 1)]) & 1
+                      ).astype(np.int64)
+            mptr, mcol = _csr_bank_spread(rows[sg < 0], cols[sg < 0], n, base, parity)
+        else:
+            mptr, mcol = _csr(rows[sg < 0], cols[sg < 0], n)
         xptr, xcol = _csr(rows[sg > 0], cols[sg > 0], n)
 
         def up(a):

@@ -23,6 +23,7 @@ CDK_LPR                lpr                     lanes per row of the row-group ga
 CDK_INTER_PHASE        inter_phase             force (1) / forbid (0) the separate inter phase
 CDK_INTER_BLOCKS       inter_blocks            force the block-phased inter sweep's block count
 CDK_P2P                p2p                     fused NVLink exchange on multi-GPU runs (0: NCCL)
+CDK_CS_BANK_SPREAD     cs_bank_spread          Cucker-Smale: missing columns ordered for the window's banks
 =====================  ======================  =========================================
 """
 
@@ -70,6 +71,7 @@ class Settings:
     inter_phase: int | None = None  # None: per community (mean inter degree)
     inter_blocks: int | None = None  # None: by the size of z
     p2p: bool = True
+    cs_bank_spread: bool = True
 
 
 def settings() -> Settings:
@@ -91,4 +93,5 @@ def settings() -> Settings:
         inter_phase=_opt_int("CDK_INTER_PHASE"),
         inter_blocks=_opt_int("CDK_INTER_BLOCKS"),
         p2p=_flag("CDK_P2P", d.p2p),
+        cs_bank_spread=_flag("CDK_CS_BANK_SPREAD", d.cs_bank_spread),
     )

@@ -73,3 +73,40 @@ def test_config4_plan_domain():
     plan = cs.cs_plan(cs.CuckerSmale(c.K, c.sigma, c.beta), dec, pos, vel, c.t_end)
     assert plan.T.shape == (100, cs.NMON, cs.NMON)
     assert np.all(plan.L > 0)
+
+
+def test_bank_spread_order_keeps_rows_and_spreads_banks():
+    """cs._csr_bank_spread: every row keeps its set of missing columns; a pair
+    of consecutive rows reading 4 consecutive entries each (one quarter-warp
+    step of cs_sparse_win_kernel) meets fewer shared-memory bank conflicts
+    than with sorted columns."""
+    from paper_2203_16657_b200 import cs as CS
+    from paper_2203_16657_b200 import graph as G
+    from paper_2203_16657_b200.plan import build_layout
+
+    dec = G.planted_partition_decomposition([600, 333], 0.9, 1e-3, 5)
+    n = dec.n_nodes
+    lay = build_layout(dec)
+    rows, cols, sg = dec.directed()
+    comm = dec.partition.comm_of_permuted()
+    base = np.where(comm >= 0, dec.offsets[np.maximum(comm, 0)], 0).astype(np.int64)
+    rb = np.searchsorted(lay.rblk_row0, np.arange(n), side="right") - 1
+    par = ((np.arange(n) - lay.rblk_row0[np.minimum(rb, lay.n_rblk - 1)]) & 1).astype(np.int64)
+    p0, c0 = CS._csr(rows[sg < 0], cols[sg < 0], n)
+    p1, c1 = CS._csr_bank_spread(rows[sg < 0], cols[sg < 0], n, base, par)
+    assert np.array_equal(p0, p1)
+    for r in range(n):
+        assert np.array_equal(np.sort(c1[p1[r]:p1[r + 1]]), c0[p0[r]:p0[r + 1]])
+
+    def load(ptr, col):
+        tot = steps = 0
+        for r in range(0, 600 - 1, 2):  # pairs inside the first community's rblocks
+            a = (col[ptr[r]:ptr[r + 1]] - base[r]) & 7
+            b = (col[ptr[r + 1]:ptr[r + 2]] - base[r + 1]) & 7
+            for k in range(0, max(len(a), len(b)), 4):
+                q = np.r_[a[k:k + 4], b[k:k + 4]]
+                tot += np.bincount(q, minlength=8).max()
+                steps += 1
+        return tot / steps
+
+    assert load(p1, c1) < 0.8 * load(p0, c0)
