@@ -353,6 +353,30 @@ __global__ void __launch_bounds__(32 * CS_WIN_RB * CS_LPR, 2) cs_sparse_win_kern
 constexpr int CS_RLPR = CDK_CS_RLPR;
 constexpr int CS_ROWS_PER_CTA = 256 / CS_RLPR;
 constexpr int CS_H_SLOTS = 4;  // communities staged per CTA (more: read from global)
+
+// G^f(x, y) = sum_pq H^f_pq x^p y^q for f = 0, x, y: lane t of a row's
+// CS_RLPR lanes takes p = t, t + CS_RLPR, ...; Horner in y, then one x^p term
+template <typename HPtr>
+__device__ __forceinline__ void cs_bivariate(HPtr Hc, double x, double y, int t, double &g0,
+                                             double &gx, double &gy) {
+  double xp = 1.0;
+  for (int k = 0; k < t; ++k) xp *= x;
+  double x8 = 1.0;  // x^CS_RLPR
+  for (int k = 0; k < CS_RLPR; ++k) x8 *= x;
+  for (int p = t; p <= CS_D2; p += CS_RLPR) {
+    const int r0 = c_mono_row[p], nq = CS_D2 - p;
+    double h0 = Hc[r0 + nq], hx = Hc[CS_NMON + r0 + nq], hy = Hc[2 * CS_NMON + r0 + nq];
+    for (int q = nq - 1; q >= 0; --q) {
+      h0 = fma(h0, y, Hc[r0 + q]);
+      hx = fma(hx, y, Hc[CS_NMON + r0 + q]);
+      hy = fma(hy, y, Hc[2 * CS_NMON + r0 + q]);
+    }
+    g0 = fma(xp, h0, g0);
+    gx = fma(xp, hx, gx);
+    gy = fma(xp, hy, gy);
+    xp *= x8;
+  }
+}
 template <int MODE>
 __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
   __shared__ double Hs[CS_H_SLOTS][CS_NOUT];
@@ -391,24 +415,12 @@ __global__ void __launch_bounds__(256, CS_MINB) cs_rows_kernel(const CsArgs a) {
       const double il = a.inv_L[c];
       const double x = (sm.x - mu.x) * il, y = (sm.y - mu.y) * il;
       out_of_domain = (x * x + y * y) > 1.0 + 1e-12;
-      const double *Hc = (c - c0 < CS_H_SLOTS) ? Hs[c - c0] : a.H + (int64_t)c * CS_NOUT;
-      double xp = 1.0;
-      for (int k = 0; k < t; ++k) xp *= x;
-      double x8 = 1.0;  // x^CS_RLPR
-      for (int k = 0; k < CS_RLPR; ++k) x8 *= x;
-      for (int p = t; p <= CS_D2; p += CS_RLPR) {
-        // Horner in y for the three functions, then one x^p term each
-        const int r0 = c_mono_row[p], nq = CS_D2 - p;
-        double h0 = Hc[r0 + nq], hx = Hc[CS_NMON + r0 + nq], hy = Hc[2 * CS_NMON + r0 + nq];
-        for (int q = nq - 1; q >= 0; --q) {
-          h0 = fma(h0, y, Hc[r0 + q]);
-          hx = fma(hx, y, Hc[CS_NMON + r0 + q]);
-          hy = fma(hy, y, Hc[2 * CS_NMON + r0 + q]);
-        }
-        g0 = fma(xp, h0, g0);
-        gx = fma(xp, hx, gx);
-        gy = fma(xp, hy, gy);
-        xp *= x8;
+      // two instantiations so the staged case reads with LDS (a pointer that
+      // may be shared or global compiles to generic loads)
+      if (c - c0 < CS_H_SLOTS) {
+        cs_bivariate(Hs[c - c0], x, y, t, g0, gx, gy);
+      } else {
+        cs_bivariate(a.H + (int64_t)c * CS_NOUT, x, y, t, g0, gx, gy);
       }
     }
 #pragma unroll
