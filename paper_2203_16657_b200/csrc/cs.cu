@@ -55,9 +55,27 @@ struct CsArgs {
   int64_t step_rel;
 };
 
+// x^(-1/2) for a positive normal x: the hardware seed (rsqrt.approx.f64, ~2^-22)
+// and one cubic step y (1 + e/2 + 3 e^2/8), e = 1 - x y^2 (error ~ e^3).  No
+// special-case branch or slow-path call, which the library sqrt/rsqrt carry
+// per evaluation (the sparse correction is issue-bound: ~100 instructions per
+// entry, a third of them this function).
+__device__ __forceinline__ double rsqrt_normal(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(x * y), y, 1.0);
+  return fma(y, e * fma(0.375, e, 0.5), y);
+}
+
 __device__ __forceinline__ double eta_exact(double d2, double K, double sigma2, double beta) {
   const double x = sigma2 + d2;
-  if (beta == 0.25) return K * rsqrt(sqrt(x));
+  if (beta == 0.25) {  // x^(-1/4) = sqrt(r), r = x^(-1/2): within 2 ulp of pow(x, -0.25)
+    if (x > 1e-280 && x < 1e280) {
+      const double r = rsqrt_normal(x);
+      return K * (r * rsqrt_normal(r));
+    }
+    return K * rsqrt(sqrt(x));
+  }
   return K / pow(x, beta);
 }
 
