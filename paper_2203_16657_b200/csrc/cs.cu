@@ -281,19 +281,20 @@ __device__ __forceinline__ void cs_sparse_sum_win(const CsArgs &a, const int32_t
   // column load's L2 latency was the kernel's top stall (24 % of the warp
   // samples on its first use).  Volatile asm keeps the loads where they are
   // written (the compiler sinks a plain __ldg back to its use).
+  // 32-bit entry counter relative to the lane's first entry (the kernel
+  // issues ~60 % of its slots: index arithmetic counts)
+  const int32_t *__restrict__ cp = col + p0;
+  const int cnt = (int)(p1 - p0);
   int jn[CS_BATCH];
 #pragma unroll
-  for (int b = 0; b < CS_BATCH; ++b) {
-    const int64_t q = p0 + (int64_t)b * CS_LPR;
-    jn[b] = q < p1 ? ld_col(col + q) : -1;
-  }
-  for (int64_t p = p0; p < p1; p += CS_BATCH * CS_LPR) {
+  for (int b = 0; b < CS_BATCH; ++b) jn[b] = b * CS_LPR < cnt ? ld_col(cp + b * CS_LPR) : -1;
+  for (int e = 0; e < cnt; e += CS_BATCH * CS_LPR) {
     int jb[CS_BATCH];
 #pragma unroll
     for (int b = 0; b < CS_BATCH; ++b) {
       jb[b] = jn[b];
-      const int64_t q = p + (int64_t)(CS_BATCH + b) * CS_LPR;
-      jn[b] = q < p1 ? ld_col(col + q) : -1;
+      const int q = e + (CS_BATCH + b) * CS_LPR;
+      jn[b] = q < cnt ? ld_col(cp + q) : -1;
     }
     double2 sj[CS_BATCH], vj[CS_BATCH];
 #pragma unroll
@@ -304,12 +305,11 @@ __device__ __forceinline__ void cs_sparse_sum_win(const CsArgs &a, const int32_t
     }
 #pragma unroll
     for (int b = 0; b < CS_BATCH; ++b) {
-      if (jb[b] >= 0) {
-        const double dx = sj[b].x - sm.x, dy = sj[b].y - sm.y;
-        const double w = eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta);
-        ax += w * (vj[b].x - vm.x);
-        ay += w * (vj[b].y - vm.y);
-      }
+      // pads evaluate node 0 of the window and add nothing (no divergent branch)
+      const double dx = sj[b].x - sm.x, dy = sj[b].y - sm.y;
+      const double w = jb[b] >= 0 ? eta_exact(dx * dx + dy * dy, a.K, a.sigma2, a.beta) : 0.0;
+      ax += w * (vj[b].x - vm.x);
+      ay += w * (vj[b].y - vm.y);
     }
   }
 }
